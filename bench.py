@@ -1,0 +1,358 @@
+"""Throughput bench: adaptive BS5 steps of the forced-HIT workload (BASELINE config 5)
+at N^3 fp64 on the B200 path, one JSON line on rank 0.
+
+A "step" = one accepted adaptive BS5 step through the drop-in API
+(adaptive_advance + energy-restoring forcing + cached-tendency refresh +
+diagnostics record), i.e. 8 RHS evaluations per accepted step (7 stages, FSAL
+invalidated by the forcing, simulation.py:165-182).  The metric is RK stages
+(RHS evaluations, the reference's rhs_evals accounting) per second.
+
+    python bench.py                       # N=1, 512^3, K=10, W=3
+    python bench.py --impl reference      # CPU oracle port (the reference's algorithm)
+    torchrun --nproc-per-node N bench.py --gpus N   # N independent replicas
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "RK stages/sec (BS5 adaptive, forced HIT, N^3 fp64)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def model_bytes(n):
+    """SURVEY §8(d) M3 byte model (3/2-rule padded algorithm, complex128)."""
+    m, k = 3 * n // 2, n // 2 + 1
+    sc, sx, sxy = n * n * k, m * n * k, m * m * k
+    b_rhs = 16 * (9 * sc + 18 * sx + 18 * sxy)
+    f = 3 * sc * 16
+    per_kernel = {  # algorithmic bytes each kernel of srk_rhs must move
+        "K1_xinv_curl": 16 * (3 * sc + 6 * sx),
+        "K2_yinv": 16 * (6 * sx + 6 * sxy),
+        "K3_z_c2r_cross_r2c": 16 * (6 * sxy + 3 * sxy),
+        "K4_yfwd": 16 * (3 * sxy + 3 * sx),
+        "K5_xfwd": 16 * (3 * sx + 3 * sc),
+        "K6_project": 16 * (3 * sc + 3 * sc + 3 * sc),
+    }
+    return dict(b_rhs=b_rhs, b_stage_bs5=b_rhs + 50.0 / 7.0 * f, per_kernel=per_kernel)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._th = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._th.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle leg (reference algorithm restated; bench-only use of oracle/)
+# ---------------------------------------------------------------------------
+def cpu_sample(n_target, steps=1, n_sample=128, workers=None):
+    import oracle as O
+
+    workers = workers or (os.cpu_count() or 1)
+    O.set_fft_workers(workers)
+    og = O.OGrid((n_sample,) * 3)
+    y = O.hit(og, a=4.0, energy=0.5, seed=42)
+    f = O.OracleRHS(og, 2000.0)
+    tab = O.tableau("bs5")
+    st = O.CtrlState(h=1e-3)
+    fnow = f(0.0, y)
+    t0 = time.perf_counter()
+    evals = 0
+    t = 0.0
+    for _ in range(steps):
+        o = O.adaptive_advance(y, t, tab, st, O.Ctrl(), f, fnow)
+        y = o.y_new.copy()
+        O.apply_forcing(y[:3], og, 0.5, 2.0)
+        fnow = f(t, y)
+        evals += o.evals + 1
+        t = o.t_new
+    dt = time.perf_counter() - t0
+    pts = float(n_sample) ** 3
+    value = evals / dt * pts / float(n_target) ** 3
+    return dict(value=value, unit="stages/s", cores=workers, kind="port",
+                sample=(f"oracle port (numpy/scipy, scipy.fft workers={workers}) on {n_sample}^3, {steps} BS5 "
+                        f"forced step(s) = {evals} RHS in {dt:.1f} s; scaled by points to {n_target}^3 "
+                        f"({evals / dt * pts / 1e9:.4f} Gpts*stage/s)"),
+                gpts_stage_per_s=evals / dt * pts / 1e9)
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    steps_per = 1
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_sample(args.n, steps=steps_per, n_sample=64 if args.n >= 64 else args.n)
+        if i >= args.warmup:
+            vals.append(r)
+    v = statistics.median([r["value"] for r in vals])
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "stages/s", "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded HIT spectrum, a=4, E=0.5)",
+        "config": {"workload": f"forced_hit_bs5_{args.n}^3", "n": args.n, "nu": 5e-4, "tol": 1e-6, "k_f": 2.0},
+        "cpu_baseline": {"value": v, "unit": "stages/s", "cores": vals[-1]["cores"], "kind": "port",
+                         "sample": vals[-1]["sample"]},
+        "e2e": {"value": v, "unit": "stages/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU leg
+# ---------------------------------------------------------------------------
+def run_native(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1810_10197_b200 as srk
+    from paper_1810_10197_b200 import _native
+    from paper_1810_10197_b200.diagnostics import diag_from_sums
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    n = args.n
+    g = srk.Grid((n, n, n))
+    params = srk.PhysParams(reynolds=2000.0)  # nu = 5e-4 (config 5)
+    energy, k_f = 0.5, 2.0
+    y0 = srk.hit_init(g, srk.ProblemSpec("hit", a=4.0, energy=energy, seed=42 + rank)).fields
+    rhs = srk.FlowRHS(g, params)
+    pair = srk.make_bs5()
+    cfg = srk.ControllerConfig(tol_abs=1e-6, tol_rel=1e-6)
+
+    def new_state():
+        y = y0.clone()
+        return dict(y=y, t=0.0, f=rhs(0.0, y), ctrl=srk.ControllerState(h=1e-3))
+
+    def step(s):
+        out = srk.adaptive_advance(s["y"], s["t"], pair, s["ctrl"], cfg, rhs, first_stage=s["f"], grid=g)
+        y = out.y_new
+        srk.apply_forcing(y, g, energy, k_f)
+        f = rhs(out.t_new, y)
+        q = srk.diagnostics.reduce_sums(g, y, fl=f, flags=2, ncomp=3).tolist()
+        s.update(y=y, t=out.t_new, f=f)
+        return out.rhs_evals + 1, diag_from_sums(q, g)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    s = new_state()
+    for _ in range(args.warmup):
+        step(s)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evals = 0
+    l0 = _native.LAUNCHES
+    with ClockSampler(local_rank) as clk:
+        e0.record(st)
+        for _ in range(args.steps):
+            ev, diag = step(s)
+            evals += ev
+        e1.record(st)
+        torch.cuda.synchronize()
+    launches = _native.LAUNCHES - l0
+    barrier()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    t_sec = torch.tensor([ms / 1e3], dtype=torch.float64, device=dev)
+    ev_t = torch.tensor([float(evals)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_sec, op=dist.ReduceOp.MAX)
+        dist.all_reduce(ev_t, op=dist.ReduceOp.SUM)
+    T = t_sec.item()
+    total_evals = ev_t.item()
+    value = total_evals / T
+
+    # ---- per-kernel live timing of the RHS (CUDA events between launches) ----
+    import ctypes
+
+    pl = rhs.plan
+    kn = list(model_bytes(n)["per_kernel"].keys())
+    acc = np.zeros(len(kn))
+    reps = 3
+    yk, fk = s["y"], torch.empty_like(s["y"])
+    for _ in range(reps):
+        ms_arr = (ctypes.c_float * 16)()
+        rc = pl.lib.srk_rhs_timed(pl.bind(), _native.ptr(yk), _native.ptr(fk), 1.0 / params.reynolds, 1.0,
+                                  params.reynolds, _native.stream_ptr(), ms_arr, 16)
+        if rc > 0:
+            _native.check(rc, "srk_rhs_timed")
+        acc += np.array(ms_arr[: len(kn)])
+    kms = acc / reps
+    mb = model_bytes(n)
+    shares = kms / kms.sum()
+    dom = int(np.argmax(kms))
+    peak, peak_src = peaks()
+    achieved = mb["per_kernel"][kn[dom]] / (kms[dom] * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_dram_bytes.json")) as fh:
+            traffic = json.load(fh).get(str(n), {}).get(kn[dom])
+    except Exception:
+        pass
+
+    # ---- e2e: through the public API with pinned host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        s2 = new_state()
+        y_h = torch.empty(s2["y"].shape, dtype=s2["y"].dtype, pin_memory=True)
+        f_h = torch.empty_like(y_h).pin_memory()
+        y_h.copy_(s2["y"])
+        f_h.copy_(s2["f"])
+        torch.cuda.synchronize()
+        nbytes = y_h.numel() * y_h.element_size()
+        barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev2 = 0
+        s2["y"] = torch.empty_like(s2["y"])
+        s2["f"] = torch.empty_like(s2["f"])
+        a0.record(st)
+        for _ in range(max(2, args.steps // 2)):
+            s2["y"].copy_(y_h, non_blocking=True)
+            s2["f"].copy_(f_h, non_blocking=True)
+            ev, _ = step(s2)
+            ev2 += ev
+            y_h.copy_(s2["y"], non_blocking=True)
+            f_h.copy_(s2["f"], non_blocking=True)
+        a1.record(st)
+        torch.cuda.synchronize()
+        t2 = torch.tensor([a0.elapsed_time(a1) / 1e3], dtype=torch.float64, device=dev)
+        e2t = torch.tensor([float(ev2)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+            dist.all_reduce(e2t, op=dist.ReduceOp.SUM)
+        e2e = {"value": e2t.item() / t2.item(), "unit": "stages/s", "h2d_bytes_per_step": 2 * nbytes,
+               "d2h_bytes_per_step": 2 * nbytes,
+               "path": "adaptive_advance + forcing + f_now through the Python API; y and f_now copied "
+                       "host->device (pinned) before and device->host after every step"}
+
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        cpu = cpu_sample(n, steps=1, n_sample=min(n, 128))
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    stage_frac = mb["b_stage_bs5"] * (value / world) / (peak * 1e9)
+    line = {
+        "metric": METRIC, "value": value, "unit": "stages/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": T * 1e3 / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded HIT spectrum E(k)~k^4 exp(-2(k/4)^2), E=0.5, reference hit_init)",
+        "config": {"workload": f"forced_hit_bs5_{n}^3", "n": n, "nu": 5e-4, "tol": 1e-6, "k_f": 2.0,
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (each field %.2f GB)" % (3 * g.mode_count * 16 / 1e9)},
+        "gpts_stage_per_s": value * n ** 3 / 1e9,
+        "rhs_evals": total_evals,
+        "stage_hbm_frac": stage_frac,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "kernel": kn[dom],
+                     "peak_source": peak_src,
+                     "kernel_ms": {k: round(float(v), 4) for k, v in zip(kn, kms)},
+                     "kernel_share": {k: round(float(v), 4) for k, v in zip(kn, shares)},
+                     "algorithmic_bytes_per_launch": mb["per_kernel"][kn[dom]]},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    run_native(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

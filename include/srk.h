@@ -1,0 +1,137 @@
+/*
+ * srk.h -- C ABI of libsrk, the sm_100a (B200) implementation of the hot path of
+ * the `spectralrk` reference (arxiv/paper_1810_10197): the 3/2-rule dealiased
+ * pseudo-spectral incompressible Navier-Stokes / Boussinesq right-hand side and
+ * the Runge-Kutta stage / error-norm arithmetic around it.
+ *
+ * The reference is pure Python; its "operator API" for this path is duck
+ * typing.  Each entry point below names the reference callable
+ * it replaces (paths relative to /root/reference/pkg/src/spectralrk/).  The
+ * ctypes binding that a reference maintainer would add is in INTEGRATION.md;
+ * the one this repo uses is paper_1810_10197_b200/_native.py.
+ *
+ * Conventions
+ *  - All arrays are DEVICE pointers to caller-owned memory (torch tensors),
+ *    C-order, complex128 spectra in the numpy rfftn layout
+ *    (ncomp, n0, n1, n2/2+1) [2D: (ncomp, n0, n1/2+1)], float64 physical fields
+ *    (ncomp, *shape).  The r2c axis is the LAST axis (grid.py:71).
+ *  - `stream` is a cudaStream_t (may be NULL = legacy default stream); every
+ *    call is asynchronous and stream-ordered.
+ *  - Return value 0 = success; non-zero = error, text in srk_last_error().
+ *    SRK_ERR_INVALID maps to the reference's ValueError (grid.py:55-66,
+ *    spectral.py:25-28,40-43, :212-214, :269-271).
+ *  - A plan is single-owner and not re-entrant, like FlowRHS's shared
+ *    DealiasWorkspace (physics.py:195-201).
+ */
+#ifndef SRK_H
+#define SRK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SRK_OK 0
+#define SRK_ERR_INVALID 1
+#define SRK_ERR_UNSUPPORTED 2
+#define SRK_ERR_CUDA 3
+#define SRK_ERR_WORKSPACE 4
+
+typedef struct srk_plan srk_plan;
+
+/* ABI version of this header (bumped on any signature change). */
+int srk_abi_version(void);
+
+/* Thread-local description of the last error. */
+const char* srk_last_error(void);
+
+/* Grid + dealiasing workspace geometry.
+ * Replaces Grid(shape, lengths) (grid.py:53-110) together with
+ * DealiasWorkspace(grid, ncomp) (spectral.py:187-207) and the workspace that
+ * FlowRHS(grid, params, density) owns (physics.py:195-201).
+ * dims = 2 or 3; shape[dims] even and >= 4; lengths[dims] > 0;
+ * density = 0|1 (Boussinesq); max_comps = largest component count passed to
+ * srk_widen / srk_narrow / the transforms (0 -> the RHS's own need). */
+int srk_plan_create(srk_plan** out, int dims, const int64_t* shape, const double* lengths,
+                    int density, int max_comps);
+void srk_plan_destroy(srk_plan* plan);
+
+/* Device workspace the caller must allocate (bytes) and bind before any
+ * compute call.  Replaces the numpy buffers of spectral.py:187-207. */
+int srk_plan_workspace_bytes(const srk_plan* plan, int64_t* bytes);
+int srk_plan_set_workspace(srk_plan* plan, void* ptr, int64_t bytes);
+
+/* FlowRHS.__call__(t, fields) (physics.py:203-206):
+ *   density == 0: ns_rhs         (physics.py:105-129), nu = 1/Re
+ *   density == 1: boussinesq_rhs (physics.py:132-185), ri = Ri, re_pr = Re*Pr
+ * y, f: (d [+1], ...kshape) complex128; f must not alias y. */
+int srk_rhs(srk_plan* plan, const void* y, void* f, double nu, double ri, double re_pr, void* stream);
+
+/* DealiasWorkspace.widen (spectral.py:215-261): spec (ncomp, kshape) ->
+ * phys (ncomp, 3n0/2, 3n1/2[, 3n2/2]) float64. */
+int srk_widen(srk_plan* plan, const void* spec, int ncomp, void* phys, void* stream);
+
+/* DealiasWorkspace.narrow (spectral.py:263-304): phys (ncomp, padded shape)
+ * float64 -> spec (ncomp, kshape) complex128 with Nyquist / self-conjugate
+ * zeroing. */
+int srk_narrow(srk_plan* plan, const void* phys, int ncomp, void* spec, void* stream);
+
+/* forward_transform (spectral.py:17-30), unnormalised rfftn over the grid axes. */
+int srk_forward_transform(srk_plan* plan, const void* phys, int ncomp, void* spec, void* stream);
+
+/* inverse_transform (spectral.py:33-44), irfftn with 1/points normalisation. */
+int srk_inverse_transform(srk_plan* plan, const void* spec, int ncomp, void* phys, void* stream);
+
+/* curl (spectral.py:47-65): 3D (3,kshape)->(3,kshape); 2D (2,kshape)->(1,kshape). */
+int srk_curl(srk_plan* plan, const void* u, void* w, void* stream);
+
+/* leray_project (physics.py:89-102): (d,kshape) -> (d,kshape). */
+int srk_leray_project(srk_plan* plan, const void* u, void* out, void* stream);
+
+/* rk_step stage input / update (integrators.py:327-339, 341-347):
+ *   out[i] = y[i] + sum_j coef[j] * F[j][i]   (ascending j; y may be NULL -> 0)
+ * n = number of complex128 elements; nterms <= 8; F is a HOST array of device
+ * pointers; coef is a HOST array. */
+int srk_combine(int64_t n, const void* y, int nterms, const void* const* F, const double* coef, void* out,
+                void* stream);
+
+/* Fused embedded-error norm + diagnostics reduction (deterministic):
+ *   flags & 1: error vector Delta = sum_j coef[j] F[j] (integrators.py:341-347),
+ *              sc = tol_abs + max(|y0|,|y1|) tol_rel (control.py:51-57),
+ *              out[c] = sum_modes (|Delta_c|/sc_c)^2 for c < 4 (control.py:72-79)
+ *   flags & 2: out[4] = sum_k w_k sum_{j<d} |y1_kj|^2    (diagnostics.py:39-50)
+ *              out[5] = sum_k w_k sum_{j<d} Re(y1 conj fl) (diagnostics.py:53-70)
+ *              out[8] = sum_k w_k |k|^2 sum_{j<d} |y1_kj|^2  (enstrophy)
+ *   always:    out[6] = number of non-finite entries in Delta and y1
+ *              (integrators.py:348-351), out[7] = count(sc <= 0).
+ * out_dev: DEVICE array of 9 doubles.  Needs no bound workspace. */
+int srk_step_reduce(srk_plan* plan, const void* y0, const void* y1, int nterms, const void* const* F,
+                    const double* coef, const void* fl, int ncomp, double tol_abs, double tol_rel, int flags,
+                    double* out_dev, void* stream);
+
+/* apply_forcing band helpers (physics.py:209-239):
+ * srk_band_energy: out_dev[0] = sum_{j<ncomp} sum_b w[b] |u_j[idx[b]]|^2
+ * srk_band_scale:  u_j[idx[b]] *= gamma for j < ncomp
+ * idx_dev: flat mode indices within one component; w_dev: Hermitian weights. */
+int srk_band_energy(srk_plan* plan, const void* u, int ncomp, const int64_t* idx_dev, const double* w_dev,
+                    int nb, double* out_dev, void* stream);
+int srk_band_scale(srk_plan* plan, void* u, int ncomp, const int64_t* idx_dev, int nb, double gamma,
+                   void* stream);
+
+/* srk_rhs with a CUDA event after every kernel (synchronises): writes the
+ * per-kernel device times [ms] in launch order to ms_out and returns
+ * -(number of kernels) on success, a positive error code otherwise.
+ * Used by bench.py for the live roofline figure. */
+int srk_rhs_timed(srk_plan* plan, const void* y, void* f, double nu, double ri, double re_pr, void* stream,
+                  float* ms_out, int max_kernels);
+
+/* Number of kernel launches the last srk_rhs issued (launch accounting for
+ * the bench's gpu_launches claim). */
+int srk_rhs_launch_count(const srk_plan* plan);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SRK_H */

@@ -1,0 +1,120 @@
+"""ctypes binding of libsrk (include/srk.h).
+
+The product's compute path is this library; there is no CPU fallback.  Loading
+fails loudly when the shared object is missing, and every compute entry point
+raises when no CUDA device is present.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libsrk.so")
+
+SRK_OK = 0
+SRK_ERR_INVALID = 1
+SRK_ERR_UNSUPPORTED = 2
+SRK_ERR_CUDA = 3
+SRK_ERR_WORKSPACE = 4
+
+# Every symbol include/srk.h declares (checked by tests/test_native_abi.py).
+EXPORTS = (
+    "srk_abi_version", "srk_last_error", "srk_plan_create", "srk_plan_destroy",
+    "srk_plan_workspace_bytes", "srk_plan_set_workspace", "srk_rhs", "srk_widen",
+    "srk_narrow", "srk_forward_transform", "srk_inverse_transform", "srk_curl",
+    "srk_leray_project", "srk_combine", "srk_step_reduce", "srk_band_energy",
+    "srk_band_scale", "srk_rhs_launch_count", "srk_rhs_timed",
+)
+
+_lib = None
+
+# Number of libsrk kernels launched through the Python API (bench.py's
+# gpu_launches claim reads the difference around its timed region).
+LAUNCHES = 0
+
+
+def count(n):
+    global LAUNCHES
+    LAUNCHES += int(n)
+
+
+class SrkError(RuntimeError):
+    """A libsrk call failed (CUDA error, workspace, unsupported size)."""
+
+
+def load():
+    """Load libsrk.so (once) and declare its signatures."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"libsrk.so not built at {LIB_PATH}; run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback for the B200 path)")
+    lib = ctypes.CDLL(LIB_PATH)
+    c_int, c_dbl, vp, i64 = ctypes.c_int, ctypes.c_double, ctypes.c_void_p, ctypes.c_int64
+    P = ctypes.POINTER
+    sig = {
+        "srk_abi_version": (c_int, []),
+        "srk_last_error": (ctypes.c_char_p, []),
+        "srk_plan_create": (c_int, [P(vp), c_int, P(i64), P(c_dbl), c_int, c_int]),
+        "srk_plan_destroy": (None, [vp]),
+        "srk_plan_workspace_bytes": (c_int, [vp, P(i64)]),
+        "srk_plan_set_workspace": (c_int, [vp, vp, i64]),
+        "srk_rhs": (c_int, [vp, vp, vp, c_dbl, c_dbl, c_dbl, vp]),
+        "srk_widen": (c_int, [vp, vp, c_int, vp, vp]),
+        "srk_narrow": (c_int, [vp, vp, c_int, vp, vp]),
+        "srk_forward_transform": (c_int, [vp, vp, c_int, vp, vp]),
+        "srk_inverse_transform": (c_int, [vp, vp, c_int, vp, vp]),
+        "srk_curl": (c_int, [vp, vp, vp, vp]),
+        "srk_leray_project": (c_int, [vp, vp, vp, vp]),
+        "srk_combine": (c_int, [i64, vp, c_int, P(vp), P(c_dbl), vp, vp]),
+        "srk_step_reduce": (c_int, [vp, vp, vp, c_int, P(vp), P(c_dbl), vp, c_int, c_dbl, c_dbl, c_int, vp, vp]),
+        "srk_band_energy": (c_int, [vp, vp, c_int, vp, vp, c_int, vp, vp]),
+        "srk_band_scale": (c_int, [vp, vp, c_int, vp, c_int, c_dbl, vp]),
+        "srk_rhs_launch_count": (c_int, [vp]),
+        "srk_rhs_timed": (c_int, [vp, vp, vp, c_dbl, c_dbl, c_dbl, vp, P(ctypes.c_float), c_int]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(rc, what=""):
+    """Map a non-zero libsrk status to the reference's exception classes."""
+    if rc == SRK_OK:
+        return
+    msg = load().srk_last_error().decode(errors="replace")
+    if rc == SRK_ERR_INVALID:
+        raise ValueError(msg)
+    raise SrkError(f"{what}: {msg}" if what else msg)
+
+
+def ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def stream_ptr(stream=None):
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def ptr_array(tensors):
+    arr = (ctypes.c_void_p * max(1, len(tensors)))()
+    for i, t in enumerate(tensors):
+        arr[i] = t.data_ptr()
+    return arr
+
+
+def dbl_array(vals):
+    arr = (ctypes.c_double * max(1, len(vals)))()
+    for i, v in enumerate(vals):
+        arr[i] = float(v)
+    return arr

@@ -1,0 +1,204 @@
+// FFT engines for the strided-axis (x, y) and contiguous-axis (z) passes.
+//
+// A CTA owns a tile of C independent length-M FFT "columns".  Both engines use
+// the self-sorting Stockham formulation: at a stage with radix R after a
+// cumulative length Ls,
+//     j in [0, M/R):  k = j mod Ls
+//     v[t] = x[j + t*M/R] * W^{t*k*M/(Ls*R)}            (t = 0..R-1)
+//     x'[(j-k)*R + k + q*Ls] = DFT_R(v)[q]              (q = 0..R-1)
+// The first stage pulls its inputs straight from the caller's loader (global
+// memory, with the 3/2-rule pad applied on the fly) and the last stage pushes
+// its outputs straight to the caller's storer (global memory with truncation /
+// epilogue), so intermediate data crosses shared memory only between stages.
+//
+// FastFFT: compile-time plan (radices, E = elements per thread, TPC = M/E
+// threads per column); every stage keeps E values per thread in registers and
+// works in place on one shared-memory tile (load all -> barrier -> store all).
+// GenericFFT: runtime radix list for small odd-factor sizes used by the
+// reference's own tests; one thread per column, local-memory ping-pong.
+#pragma once
+
+#include "srk_common.cuh"
+
+// ---------------------------------------------------------------------------
+// Shared-memory tile layouts.
+// RowTile:  [row][col], col fastest.  For C >= 8 any warp access pattern of the
+//           engines is bank-conflict free (8 lanes x 16 B cover all 32 banks).
+//           Thread map: col = tid % C, tj = tid / C  (global accesses coalesce
+//           along the C consecutive columns).
+// ColTile:  [col][row] with one 16 B pad every 8 rows.  Thread map:
+//           tj = tid % TPC, col = tid / TPC (lanes run along the FFT axis, which
+//           is the contiguous z axis in global memory).
+// ---------------------------------------------------------------------------
+template <int M_, int C_>
+struct RowTile {
+  static constexpr int M = M_, C = C_;
+  static constexpr int SIZE = M_ * C_;  // in cplx
+  SRK_DEV static int idx(int row, int col) { return row * C_ + col; }
+  SRK_DEV static int col_of(int tid, int) { return tid % C_; }
+  SRK_DEV static int tj_of(int tid, int) { return tid / C_; }
+};
+
+template <int M_, int C_>
+struct ColTile {
+  static constexpr int M = M_, C = C_;
+  static constexpr int PITCH = M_ + (M_ + 7) / 8 + 1;
+  static constexpr int SIZE = PITCH * C_;
+  SRK_DEV static int idx(int row, int col) { return col * PITCH + row + (row >> 3); }
+  SRK_DEV static int col_of(int tid, int tpc) { return tid / tpc; }
+  SRK_DEV static int tj_of(int tid, int tpc) { return tid % tpc; }
+};
+
+struct GenPlan {
+  int M;
+  int nr;
+  int r[10];
+};
+
+// ---------------------------------------------------------------------------
+// Compile-time engine
+// ---------------------------------------------------------------------------
+template <int M, int E, class L, int SIGN, bool LD_SMEM, bool ST_SMEM, int Ls, int R, int... Rest>
+struct FastStage {
+  template <class LD, class ST>
+  __device__ __forceinline__ static void go(cplx* sm, const cplx* __restrict__ tw, int col, int tj,
+                                            bool act, LD& ld, ST& st) {
+    constexpr int TPC = M / E;
+    constexpr int NB = E / R;
+    constexpr int STRIDE = M / R;
+    constexpr bool FIRST = (Ls == 1);
+    constexpr bool LAST = (sizeof...(Rest) == 0);
+    static_assert(E % R == 0, "radix must divide elements-per-thread");
+    cplx v[NB][R];
+    if (act) {
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int j = tj + b * TPC;
+#pragma unroll
+        for (int t = 0; t < R; ++t) {
+          const int row = j + t * STRIDE;
+          if constexpr (FIRST)
+            v[b][t] = ld(row, col);
+          else
+            v[b][t] = sm[L::idx(row, col)];
+        }
+      }
+    }
+    if constexpr ((!FIRST || LD_SMEM) && (!LAST || ST_SMEM)) __syncthreads();
+    if (act) {
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int j = tj + b * TPC;
+        const int k = j % Ls;
+        if constexpr (Ls > 1) {
+          constexpr int TS = M / (Ls * R);
+#pragma unroll
+          for (int t = 1; t < R; ++t) {
+            cplx w = __ldg(&tw[t * k * TS]);
+            if (SIGN > 0) w.y = -w.y;
+            v[b][t] = cmul(v[b][t], w);
+          }
+        }
+        DFT<R, SIGN>::run(v[b]);
+        const int base = (j - k) * R + k;
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const int row = base + q * Ls;
+          if constexpr (LAST)
+            st(row, col, v[b][q]);
+          else
+            sm[L::idx(row, col)] = v[b][q];
+        }
+      }
+    }
+    if constexpr (!LAST) {
+      __syncthreads();
+      FastStage<M, E, L, SIGN, LD_SMEM, ST_SMEM, Ls * R, Rest...>::go(sm, tw, col, tj, act, ld, st);
+    }
+  }
+};
+
+template <int M_, int E_, class L, int... Rs>
+struct FastFFT {
+  static constexpr int M = M_, E = E_, TPC = M_ / E_;
+  static constexpr int C = L::C;
+  static constexpr int NT = C * TPC;
+  static constexpr bool kFast = true;
+  static_assert((1 * ... * Rs) == M_, "radices must multiply to M");
+  SRK_DEV static int col_of(int tid) { return L::col_of(tid, TPC); }
+  // ncols: columns of the tile that carry data (<= C); idle threads still hit barriers.
+  template <int SIGN, bool LD_SMEM, bool ST_SMEM, class LD, class ST>
+  __device__ __forceinline__ static void run(const GenPlan&, cplx* sm, const cplx* __restrict__ tw,
+                                             int ncols, LD& ld, ST& st) {
+    const int tid = threadIdx.x;
+    const int col = L::col_of(tid, TPC);
+    const int tj = L::tj_of(tid, TPC);
+    const bool act = (tid < NT) && (col < ncols);
+    FastStage<M_, E_, L, SIGN, LD_SMEM, ST_SMEM, 1, Rs...>::go(sm, tw, col, tj, act, ld, st);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Runtime engine (one thread per column, radices in {2,3,4,5,7,8})
+// ---------------------------------------------------------------------------
+#define SRK_GEN_MAXM 96
+#define SRK_GEN_MAXR 8
+
+
+template <int SIGN>
+__device__ __forceinline__ void gen_dft(int R, cplx* v) {
+  switch (R) {
+    case 2: DFT<2, SIGN>::run(v); break;
+    case 3: DFT<3, SIGN>::run(v); break;
+    case 4: DFT<4, SIGN>::run(v); break;
+    case 5: DFT<5, SIGN>::run(v); break;
+    case 7: DFT<7, SIGN>::run(v); break;
+    case 8: DFT<8, SIGN>::run(v); break;
+    default: break;
+  }
+}
+
+template <class L>
+struct GenericFFT {
+  static constexpr bool kFast = false;
+  static constexpr int C = L::C;
+  static constexpr int NT = L::C;
+  SRK_DEV static int col_of(int tid) { return tid; }
+  template <int SIGN, bool LD_SMEM, bool ST_SMEM, class LD, class ST>
+  __device__ static void run(const GenPlan& p, cplx*, const cplx* __restrict__ tw, int ncols, LD& ld, ST& st) {
+    const int col = threadIdx.x;
+    if (col >= ncols || col >= C) return;
+    const int M = p.M;
+    cplx a[SRK_GEN_MAXM], b[SRK_GEN_MAXM];
+    for (int r = 0; r < M; ++r) a[r] = ld(r, col);
+    cplx* x = a;
+    cplx* y = b;
+    int Ls = 1;
+    for (int s = 0; s < p.nr; ++s) {
+      const int R = p.r[s];
+      const int stride = M / R;
+      const int ts = M / (Ls * R);
+      for (int j = 0; j < stride; ++j) {
+        const int k = j % Ls;
+        cplx v[SRK_GEN_MAXR];
+        for (int t = 0; t < R; ++t) {
+          cplx z = x[j + t * stride];
+          if (t > 0 && k > 0) {
+            cplx w = tw[t * k * ts];
+            if (SIGN > 0) w.y = -w.y;
+            z = cmul(z, w);
+          }
+          v[t] = z;
+        }
+        gen_dft<SIGN>(R, v);
+        const int base = (j - k) * R + k;
+        for (int q = 0; q < R; ++q) y[base + q * Ls] = v[q];
+      }
+      cplx* tmp = x;
+      x = y;
+      y = tmp;
+      Ls *= R;
+    }
+    for (int r = 0; r < M; ++r) st(r, col, x[r]);
+  }
+};

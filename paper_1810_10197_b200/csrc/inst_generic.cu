@@ -1,0 +1,25 @@
+// Runtime-plan (GenericFFT) instantiations for small lengths with factors in
+// {2,3,4,5,7,8} that have no compile-time plan -- the odd grids of the
+// reference's own test suite, e.g. (8, 6, 4) and (8, 10, 6).
+#include "registry.cuh"
+
+void srk_reg_generic(KEntry* t) {
+  using SE = GenericFFT<GenCols<32>>;
+  t[KK_INV] = SRK_ENTRY((k_colpass<SE, PK_INV, +1>), SE, 0);
+  t[KK_INV_RHS] = SRK_ENTRY((k_colpass<SE, PK_INV_RHS, +1>), SE, 0);
+  t[KK_FWD] = SRK_ENTRY((k_colpass<SE, PK_FWD, -1>), SE, 0);
+  using Z4 = ColTile<SRK_GEN_MAXM, 4>;
+  using Z3 = ColTile<SRK_GEN_MAXM, 3>;
+  using Z6 = ColTile<SRK_GEN_MAXM, 6>;
+  using Z7 = ColTile<SRK_GEN_MAXM, 7>;
+  using E4 = GenericFFT<Z4>;
+  using E3 = GenericFFT<Z3>;
+  using E6 = GenericFFT<Z6>;
+  using E7 = GenericFFT<Z7>;
+  t[KK_Z_C2R] = SRK_ENTRY((k_zpass<E4, Z4, ZOP_C2R>), E4, Z4::SIZE * 16);
+  t[KK_Z_R2C] = SRK_ENTRY((k_zpass<E4, Z4, ZOP_R2C>), E4, Z4::SIZE * 16);
+  t[KK_Z_NS3] = SRK_ENTRY((k_zpass<E6, Z6, ZOP_NS3>), E6, Z6::SIZE * 16);
+  t[KK_Z_NS2] = SRK_ENTRY((k_zpass<E3, Z3, ZOP_NS2>), E3, Z3::SIZE * 16);
+  t[KK_Z_B3] = SRK_ENTRY((k_zpass<E7, Z7, ZOP_B3>), E7, Z7::SIZE * 16);
+  t[KK_Z_B2] = SRK_ENTRY((k_zpass<E4, Z4, ZOP_B2>), E4, Z4::SIZE * 16);
+}

@@ -1,0 +1,302 @@
+// Axis-pass kernels of the dealiased pseudo-spectral RHS (templates; instantiated
+// per FFT length in inst_*.cu).  Data layout in HBM everywhere: component-major,
+// C-order, complex128, last (z) axis contiguous -- the reference's rfftn layout
+// (grid.py:11-18).  Kernel map:
+//
+//   K1 k_colpass<INV_RHS>  : curl on load + x zero-pad + inverse C2C along x
+//                            (spectral.py:47-65 curl, :229-258 widen x-pass)
+//   K2 k_colpass<INV>      : y zero-pad + inverse C2C along y (:249-258)
+//   K3 k_zpass<NS*/B*>     : per z-pencil C2R (:259-261), u x w / rho u in
+//                            registers (physics.py:62-82,151-158), R2C (:275)
+//   K4 k_colpass<FWD>      : forward C2C along y + truncation (:276-291)
+//   K5 k_colpass<FWD>      : forward C2C along x + truncation + 1/1.5^d,
+//                            Nyquist / self-conjugate zeroing (:292-303)
+//   K6 k_project           : Leray projection + viscous term, Boussinesq
+//                            buoyancy / density tendency (physics.py:119-129,
+//                            :163-184)   [rhs_kernels.cu]
+#pragma once
+
+#include "fft_engine.cuh"
+
+enum PassKind { PK_INV = 0, PK_INV_RHS = 1, PK_FWD = 2 };
+enum ZOp { ZOP_C2R = 0, ZOP_R2C = 1, ZOP_NS3 = 2, ZOP_NS2 = 3, ZOP_B3 = 4, ZOP_B2 = 5 };
+
+// Strided-axis pass.  Global column g within a plane (plane = signal for the
+// x pass, (signal, x) for the y pass); element (plane, row, w) lives at
+//   plane * plane_stride + row * row_stride + w.
+struct PassArgs {
+  const cplx* in;
+  cplx* out;
+  const cplx* tw;
+  GenPlan gp;
+  int M;          // FFT length on this axis
+  int n;          // coarse length on this axis (pad / truncate maps)
+  int planes;     // number of planes
+  int Qp;         // columns per plane
+  int tpp;        // column tiles per plane
+  int sig_minor;  // 1: plane index varies fastest over blocks (L2 reuse of curl reads)
+  long long row_stride;
+  long long in_plane_stride;
+  long long out_plane_stride;
+  double scale;
+  int zero_nyq;      // FWD: zero the Nyquist row (narrow)
+  int zero_dc_imag;  // FWD (x pass of narrow): Im of (0,0,0) -> 0
+  // INV_RHS (x pass with curl): planes = signals [u(d), w(wc), rho?]
+  int dims;
+  int n1;  // 3D: coarse y extent (columns are w = y*K + kz); 2D: 1
+  int K;   // r2c extent n_last/2+1
+  double ck0, ck1, ck2;  // 2*pi/L per axis (x, y, z) -- 2D uses ck0, ck2
+  long long comp_stride;  // between state components
+};
+
+template <class Eng, int KIND, int SIGN>
+__global__ void __launch_bounds__(Eng::NT) k_colpass(const PassArgs a) {
+  extern __shared__ __align__(16) cplx sm[];
+  const int bid = blockIdx.x;
+  int plane, wt;
+  if (a.sig_minor) {
+    plane = bid % a.planes;
+    wt = bid / a.planes;
+  } else {
+    plane = bid / a.tpp;
+    wt = bid % a.tpp;
+  }
+  const int w0 = wt * Eng::C;
+  const int ncols = min(Eng::C, a.Qp - w0);
+  const long long rs = a.row_stride;
+  const cplx* __restrict__ inp = a.in + plane * a.in_plane_stride + w0;
+  cplx* __restrict__ outp = a.out + plane * a.out_plane_stride + w0;
+
+  if constexpr (KIND == PK_INV) {
+    auto ld = [&](int row, int col) -> cplx {
+      const int cr = pad_src(row, a.n, a.M);
+      if (cr < 0) return cmk(0.0, 0.0);
+      return cscale(inp[cr * rs + col], a.scale);
+    };
+    auto st = [&](int row, int col, cplx v) { outp[row * rs + col] = v; };
+    Eng::template run<SIGN, false, false>(a.gp, sm, a.tw, ncols, ld, st);
+  } else if constexpr (KIND == PK_INV_RHS) {
+    // plane = signal s: [u_0..u_{d-1}, w (3 comps in 3D, 1 in 2D), rho]
+    const int d = a.dims;
+    const int wc = (d == 3) ? 3 : 1;
+    const int s = plane;
+    const cplx* __restrict__ base = a.in + w0;  // component 0
+    auto ld = [&](int row, int col) -> cplx {
+      const int cr = pad_src(row, a.n, a.M);
+      if (cr < 0) return cmk(0.0, 0.0);
+      const long long off = cr * rs + col;
+      cplx v;
+      if (s < d) {
+        v = base[s * a.comp_stride + off];
+      } else if (s < d + wc) {
+        // spectral.py:47-65: w = i k x u (k_a = mode_a * 2pi/L_a, grid.py:75-93)
+        const int q = w0 + col;
+        const double kx = mode_full(cr, a.n) * a.ck0;
+        if (d == 3) {
+          const int y = q / a.K, kzi = q - (q / a.K) * a.K;
+          const double ky = mode_full(y, a.n1) * a.ck1;
+          const double kz = (double)kzi * a.ck2;
+          cplx p, m;
+          if (s == 3) {  // i(ky u2 - kz u1)
+            cplx u2 = base[2 * a.comp_stride + off], u1 = base[1 * a.comp_stride + off];
+            p = cscale(u2, ky);
+            m = cscale(u1, kz);
+          } else if (s == 4) {  // i(kz u0 - kx u2)
+            cplx u0 = base[off], u2 = base[2 * a.comp_stride + off];
+            p = cscale(u0, kz);
+            m = cscale(u2, kx);
+          } else {  // i(kx u1 - ky u0)
+            cplx u1 = base[1 * a.comp_stride + off], u0 = base[off];
+            p = cscale(u1, kx);
+            m = cscale(u0, ky);
+          }
+          cplx df = csub(p, m);
+          v = cmk(-df.y, df.x);
+        } else {
+          const double kz = (double)q * a.ck2;
+          cplx u1 = base[1 * a.comp_stride + off], u0 = base[off];
+          cplx df = csub(cscale(u1, kx), cscale(u0, kz));
+          v = cmk(-df.y, df.x);
+        }
+      } else {
+        v = base[d * a.comp_stride + off];  // density
+      }
+      return cscale(v, a.scale);
+    };
+    auto st = [&](int row, int col, cplx v) { outp[row * rs + col] = v; };
+    Eng::template run<SIGN, false, false>(a.gp, sm, a.tw, ncols, ld, st);
+  } else {  // PK_FWD: forward C2C + truncation (+ scale, Nyquist / DC-imag zeroing)
+    const bool zn = a.zero_nyq != 0;
+    const bool zdc = (a.zero_dc_imag != 0) && (w0 == 0);
+    auto ld = [&](int row, int col) -> cplx { return inp[row * rs + col]; };
+    auto st = [&](int row, int col, cplx v) {
+      const int c = trunc_dst(row, a.n, a.M, zn);
+      if (c == -1) return;
+      if (c == -2) {
+        outp[(a.n >> 1) * rs + col] = cmk(0.0, 0.0);
+        return;
+      }
+      cplx o = cscale(v, a.scale);
+      if (zdc && c == 0 && col == 0) o.y = 0.0;
+      outp[c * rs + col] = o;
+    };
+    Eng::template run<SIGN, false, false>(a.gp, sm, a.tw, ncols, ld, st);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// z-pencil pass.  Pencil p (= x*m1 + y; m1 = 1 in 2D) of signal s lives at
+// s * sig_stride + p * K in the spectral buffers, at s * rsig_stride + p * M in
+// the real physical buffers.  One CTA = two pencils; the 2*S real signals are
+// packed pairwise into S complex FFTs (two-for-one real transforms).
+// ---------------------------------------------------------------------------
+struct ZArgs {
+  const cplx* in;
+  cplx* out;
+  const double* in_real;
+  double* out_real;
+  const cplx* tw;
+  GenPlan gp;
+  int M;  // padded z length (real)
+  int n;  // coarse z length
+  int K;  // stored modes n/2+1
+  int P;  // pencils
+  int S;  // input real signals per pencil
+  int So; // output real signals per pencil
+  long long in_sig_stride, out_sig_stride;  // complex elements (P*K) or real (P*M)
+  int zero_nyq;  // R2C: zero the kz = n/2 plane (narrow)
+};
+
+template <int OP>
+struct ZSig {
+  static constexpr int S = (OP == ZOP_NS3) ? 6 : (OP == ZOP_NS2) ? 3 : (OP == ZOP_B3) ? 7 : (OP == ZOP_B2) ? 4 : 0;
+  static constexpr int So = (OP == ZOP_NS3) ? 3 : (OP == ZOP_NS2) ? 2 : (OP == ZOP_B3) ? 6 : (OP == ZOP_B2) ? 4 : 0;
+};
+
+// physics.py:62-82 (u x w) and :151-158 (rho u) on one padded grid point
+template <int OP>
+SRK_DEV void zphys(const double* r, double* o) {
+  if constexpr (OP == ZOP_NS3 || OP == ZOP_B3) {
+    o[0] = r[1] * r[5] - r[2] * r[4];
+    o[1] = r[2] * r[3] - r[0] * r[5];
+    o[2] = r[0] * r[4] - r[1] * r[3];
+    if constexpr (OP == ZOP_B3) {
+      o[3] = r[6] * r[0];
+      o[4] = r[6] * r[1];
+      o[5] = r[6] * r[2];
+    }
+  } else if constexpr (OP == ZOP_NS2 || OP == ZOP_B2) {
+    o[0] = r[1] * r[2];
+    o[1] = -(r[0] * r[2]);
+    if constexpr (OP == ZOP_B2) {
+      o[2] = r[3] * r[0];
+      o[3] = r[3] * r[1];
+    }
+  }
+}
+
+template <class Eng, class L, int OP>
+__global__ void __launch_bounds__(Eng::NT) k_zpass(const ZArgs a, int S_rt, int So_rt) {
+  extern __shared__ __align__(16) cplx sm[];
+  const int p0 = 2 * blockIdx.x;
+  const int S = (OP >= ZOP_NS3) ? ZSig<OP>::S : S_rt;
+  const int So = (OP >= ZOP_NS3) ? ZSig<OP>::So : So_rt;
+  const int M = a.M, K = a.K;
+  // spectral value of real signal g (= pp*S + s) at padded mode k, Hermitian-extended
+  auto herm = [&](int g, int k) -> cplx {
+    const int pp = g / S, s = g - (g / S) * S;
+    const int pen = p0 + pp;
+    if (pen >= a.P) return cmk(0.0, 0.0);
+    const cplx* __restrict__ src = a.in + s * a.in_sig_stride + (long long)pen * K;
+    if (k < K) {
+      cplx X = src[k];
+      if (k == 0 || 2 * k == M) X.y = 0.0;  // irfft ignores Im of DC / Nyquist
+      return X;
+    }
+    if (k >= M - (K - 1)) return cconj(src[M - k]);
+    return cmk(0.0, 0.0);
+  };
+
+  if constexpr (OP != ZOP_R2C) {
+    // ---- inverse: S complex columns, column c carries real signals 2c, 2c+1 ----
+    auto ld = [&](int k, int c) -> cplx {
+      cplx A = herm(2 * c, k), B = herm(2 * c + 1, k);
+      return cmk(A.x - B.y, A.y + B.x);
+    };
+    if constexpr (OP == ZOP_C2R) {
+      auto st = [&](int n, int c, cplx v) {
+        const int g0 = 2 * c, g1 = 2 * c + 1;
+        {
+          const int pp = g0 / S, s = g0 - pp * S, pen = p0 + pp;
+          if (pen < a.P) a.out_real[s * a.out_sig_stride + (long long)pen * M + n] = v.x;
+        }
+        if (g1 < 2 * S) {
+          const int pp = g1 / S, s = g1 - pp * S, pen = p0 + pp;
+          if (pen < a.P) a.out_real[s * a.out_sig_stride + (long long)pen * M + n] = v.y;
+        }
+      };
+      Eng::template run<+1, false, false>(a.gp, sm, a.tw, S, ld, st);
+      return;
+    } else {
+      auto st = [&](int n, int c, cplx v) { sm[L::idx(n, c)] = v; };
+      Eng::template run<+1, false, true>(a.gp, sm, a.tw, S, ld, st);
+      __syncthreads();
+      // ---- physical space: per row n, both pencils ----
+      for (int n = threadIdx.x; n < M; n += blockDim.x) {
+        double r[2 * 7];
+#pragma unroll
+        for (int c = 0; c < ZSig<OP>::S; ++c) {
+          cplx z = sm[L::idx(n, c)];
+          r[2 * c] = z.x;
+          r[2 * c + 1] = z.y;
+        }
+        double o[2 * 6];
+        zphys<OP>(r, o);
+        zphys<OP>(r + ZSig<OP>::S, o + ZSig<OP>::So);
+#pragma unroll
+        for (int c = 0; c < ZSig<OP>::So; ++c) sm[L::idx(n, c)] = cmk(o[2 * c], o[2 * c + 1]);
+      }
+      __syncthreads();
+    }
+  }
+  // ---- forward: So complex columns ----
+  if constexpr (OP == ZOP_R2C) {
+    auto ld = [&](int n, int c) -> cplx {
+      double v[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int g = 2 * c + h;
+        const int pp = g / So, s = g - pp * So, pen = p0 + pp;
+        v[h] = (g < 2 * So && pen < a.P) ? a.in_real[s * a.in_sig_stride + (long long)pen * M + n] : 0.0;
+      }
+      return cmk(v[0], v[1]);
+    };
+    auto st = [&](int n, int c, cplx v) { sm[L::idx(n, c)] = v; };
+    Eng::template run<-1, false, true>(a.gp, sm, a.tw, So, ld, st);
+  } else {
+    auto ld = [&](int n, int c) -> cplx { return sm[L::idx(n, c)]; };
+    auto st = [&](int n, int c, cplx v) { sm[L::idx(n, c)] = v; };
+    Eng::template run<-1, true, true>(a.gp, sm, a.tw, So, ld, st);
+  }
+  __syncthreads();
+  // ---- extraction: two real spectra from each complex column, keep K modes ----
+  const bool zn = a.zero_nyq != 0;
+  for (int i = threadIdx.x; i < So * K; i += blockDim.x) {
+    const int c = i / K, k = i - (i / K) * K;
+    const cplx Zk = sm[L::idx(k, c)];
+    const cplx Zm = sm[L::idx(k == 0 ? 0 : M - k, c)];
+    cplx A = cmk(0.5 * (Zk.x + Zm.x), 0.5 * (Zk.y - Zm.y));
+    cplx B = cmk(0.5 * (Zk.y + Zm.y), -0.5 * (Zk.x - Zm.x));
+    if (zn && k == K - 1) {
+      A = cmk(0.0, 0.0);
+      B = A;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int g = 2 * c + h;
+      if (g >= 2 * So) break;
+      const int pp = g / So, s = g - pp * So, pen = p0 + pp;
+      if (pen < a.P) a.out[s * a.out_sig_stride + (long long)pen * K + k] = h ? B : A;
+    }
+  }
+}

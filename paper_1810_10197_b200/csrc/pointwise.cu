@@ -1,0 +1,291 @@
+// Pointwise and reduction kernels: projection/viscous epilogue (K6), curl and
+// Leray projection (API helpers), RK stage combination (K6b), the fused
+// embedded-error-norm + diagnostics reduction (K7) and the forcing band ops (K9).
+//
+// Where the reference's numpy op order is cheap to mirror (projection, stage
+// sums, norms) the kernels use explicit _rn intrinsics so no FMA contraction
+// changes the rounding relative to physics.py / integrators.py.
+#include "pointwise.cuh"
+
+#define DMUL __dmul_rn
+#define DADD __dadd_rn
+#define DSUB __dsub_rn
+
+__device__ __forceinline__ cplx rmul(double s, cplx a) { return make_double2(DMUL(s, a.x), DMUL(s, a.y)); }
+__device__ __forceinline__ cplx radd(cplx a, cplx b) { return make_double2(DADD(a.x, b.x), DADD(a.y, b.y)); }
+__device__ __forceinline__ cplx rsub(cplx a, cplx b) { return make_double2(DSUB(a.x, b.x), DSUB(a.y, b.y)); }
+
+struct KVec {
+  double k[3];
+  double k2, inv_k2;
+};
+
+// grid.py:75-100: k_a = mode_a * (2 pi / L_a); k2 accumulated 0 + k0^2 + k1^2 (+ k2^2)
+__device__ __forceinline__ KVec kvec(long long idx, const GeomArgs& g) {
+  KVec r;
+  const int kz = (int)(idx % g.K);
+  const long long xy = idx / g.K;
+  if (g.dims == 3) {
+    const int y = (int)(xy % g.n1), x = (int)(xy / g.n1);
+    r.k[0] = DMUL(mode_full(x, g.n0), g.ck0);
+    r.k[1] = DMUL(mode_full(y, g.n1), g.ck1);
+    r.k[2] = DMUL((double)kz, g.ck2);
+    r.k2 = DADD(DADD(DMUL(r.k[0], r.k[0]), DMUL(r.k[1], r.k[1])), DMUL(r.k[2], r.k[2]));
+  } else {
+    const int x = (int)xy;
+    r.k[0] = DMUL(mode_full(x, g.n0), g.ck0);
+    r.k[1] = DMUL((double)kz, g.ck2);
+    r.k[2] = 0.0;
+    r.k2 = DADD(DMUL(r.k[0], r.k[0]), DMUL(r.k[1], r.k[1]));
+  }
+  r.inv_k2 = (r.k2 == 0.0) ? 0.0 : __ddiv_rn(1.0, r.k2);
+  return r;
+}
+
+// K6: f = P[G] - nu k^2 u (physics.py:119-129); Boussinesq adds the buoyancy
+// before the projection and the density tendency (physics.py:163-184).
+__global__ void k_project(const ProjArgs a) {
+  const GeomArgs& g = a.g;
+  const long long n = a.modes;
+  const int d = g.dims;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const KVec kv = kvec(i, g);
+    cplx G[3];
+    for (int j = 0; j < d; ++j) G[j] = a.G[j * n + i];
+    cplx rho = make_double2(0.0, 0.0);
+    if (a.density) {
+      rho = a.y[d * n + i];
+      G[d - 1] = rsub(G[d - 1], rmul(a.ri, rho));
+    }
+    cplx kd = rmul(kv.k[0], G[0]);
+    for (int j = 1; j < d; ++j) kd = radd(kd, rmul(kv.k[j], G[j]));
+    kd = rmul(kv.inv_k2, kd);
+    const double nuk2 = DMUL(a.nu, kv.k2);
+    for (int j = 0; j < d; ++j) {
+      cplx o = rsub(G[j], rmul(kv.k[j], kd));
+      o = rsub(o, rmul(nuk2, a.y[j * n + i]));
+      a.f[j * n + i] = o;
+    }
+    if (a.density) {
+      cplx div = rmul(kv.k[0], a.G[d * n + i]);
+      for (int j = 1; j < d; ++j) div = radd(div, rmul(kv.k[j], a.G[(d + j) * n + i]));
+      cplx o = make_double2(div.y, -div.x);  // -1j * div
+      o = rsub(o, rmul(__ddiv_rn(kv.k2, a.re_pr), rho));
+      a.f[d * n + i] = o;
+    }
+  }
+}
+
+// spectral.py:47-65
+__global__ void k_curl(const GeomArgs g, const cplx* __restrict__ u, cplx* __restrict__ w, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const KVec kv = kvec(i, g);
+    auto im = [](cplx z) { return make_double2(-z.y, z.x); };
+    if (g.dims == 3) {
+      cplx u0 = u[i], u1 = u[n + i], u2 = u[2 * n + i];
+      w[i] = im(rsub(rmul(kv.k[1], u2), rmul(kv.k[2], u1)));
+      w[n + i] = im(rsub(rmul(kv.k[2], u0), rmul(kv.k[0], u2)));
+      w[2 * n + i] = im(rsub(rmul(kv.k[0], u1), rmul(kv.k[1], u0)));
+    } else {
+      cplx u0 = u[i], u1 = u[n + i];
+      w[i] = im(rsub(rmul(kv.k[0], u1), rmul(kv.k[1], u0)));
+    }
+  }
+}
+
+// physics.py:89-102
+__global__ void k_leray(const GeomArgs g, const cplx* __restrict__ u, cplx* __restrict__ out, long long n) {
+  const int d = g.dims;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const KVec kv = kvec(i, g);
+    cplx kd = make_double2(0.0, 0.0);
+    for (int j = 0; j < d; ++j) kd = radd(kd, rmul(kv.k[j], u[j * n + i]));
+    kd = rmul(kv.inv_k2, kd);
+    for (int j = 0; j < d; ++j) out[j * n + i] = rsub(u[j * n + i], rmul(kv.k[j], kd));
+  }
+}
+
+// integrators.py:327-339: out = y + sum_j (h a_ij) F_j, ascending j, one rounding
+// per multiply and per add (y == nullptr starts from zeros, :343-347).
+template <int NT>
+__global__ void k_combine(const CombArgs a) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.n;
+       i += (long long)gridDim.x * blockDim.x) {
+    cplx acc = a.y ? a.y[i] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc = radd(acc, rmul(a.c[j], a.F[j][i]));
+    a.out[i] = acc;
+  }
+}
+
+void srk_launch_combine(const CombArgs& a, cudaStream_t st) {
+  const int threads = 256;
+  long long blocks = (a.n + threads - 1) / threads;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  switch (a.nt) {
+#define CASE(N) \
+  case N: k_combine<N><<<(int)blocks, threads, 0, st>>>(a); break;
+    CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+    default: break;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K7: fused step reduction.  Deterministic: fixed grid, per-thread sequential
+// sums, fixed shuffle tree, per-block partials summed in fixed order.
+//   q[c]   (c < 4) : sum |Delta_c|^2 / sc_c^2      (control.py:51-79)
+//   q[4]           : sum_w |y1|^2 over velocity     (diagnostics.py:48-50)
+//   q[5]           : sum_w Re(y1 conj fl) velocity  (diagnostics.py:53-70)
+//   q[6]           : non-finite entries of Delta / y1 (integrators.py:341-351)
+//   q[7]           : count of sc <= 0 (control.py:74-75)
+//   q[8]           : sum_w |k|^2 |y1|^2 velocity    (enstrophy)
+// ---------------------------------------------------------------------------
+template <int NT>
+__global__ void __launch_bounds__(256) k_reduce(const RedArgs a) {
+  double acc[SRK_NQ];
+#pragma unroll
+  for (int q = 0; q < SRK_NQ; ++q) acc[q] = 0.0;
+  const long long n = a.modes;
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long nthr = (long long)gridDim.x * blockDim.x;
+  for (int c = 0; c < a.ncomp; ++c) {
+    double r2 = 0.0, e = 0.0, ep = 0.0, bad = 0.0, neg = 0.0, z = 0.0;
+    const bool vel = c < a.dvel;
+    for (long long i = tid; i < n; i += nthr) {
+      const long long ix = c * n + i;
+      const cplx y1 = a.y1[ix];
+      if (a.do_norm) {
+        cplx dl = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dl = radd(dl, rmul(a.c[j], a.F[j][ix]));
+        const cplx y0 = a.y0[ix];
+        const double sc = DADD(a.atol, DMUL(fmax(hypot(y0.x, y0.y), hypot(y1.x, y1.y)), a.rtol));
+        const double rt = __ddiv_rn(hypot(dl.x, dl.y), sc);
+        r2 = DADD(r2, DMUL(rt, rt));
+        if (!(isfinite(dl.x) && isfinite(dl.y))) bad += 1.0;
+        if (sc <= 0.0) neg += 1.0;
+      }
+      if (!(isfinite(y1.x) && isfinite(y1.y))) bad += 1.0;
+      if (a.do_diag && vel) {
+        const int kz = (int)(i % a.K);
+        const double w = (kz == 0 || kz == a.K - 1) ? 1.0 : 2.0;
+        e = DADD(e, DMUL(w, DADD(DMUL(y1.x, y1.x), DMUL(y1.y, y1.y))));
+        const cplx fl = a.fl[ix];
+        ep = DADD(ep, DMUL(w, DADD(DMUL(y1.x, fl.x), DMUL(y1.y, fl.y))));
+        const double k2 = kvec(i, a.g).k2;
+        z = DADD(z, DMUL(DMUL(w, k2), DADD(DMUL(y1.x, y1.x), DMUL(y1.y, y1.y))));
+      }
+    }
+    if (c < 4) acc[c] = r2;
+    acc[4] += e;
+    acc[5] += ep;
+    acc[6] += bad;
+    acc[7] += neg;
+    acc[8] += z;
+  }
+  __shared__ double red[SRK_NQ][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < SRK_NQ; ++q) {
+    double v = acc[q];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+    if (lane == 0) red[q][warp] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < SRK_NQ) {
+    double v = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += red[threadIdx.x][w];
+    a.partial[threadIdx.x * gridDim.x + blockIdx.x] = v;
+  }
+}
+
+__global__ void k_finalize(const double* __restrict__ partial, int nblk, double* __restrict__ out) {
+  __shared__ double sh[256];
+  for (int q = 0; q < SRK_NQ; ++q) {
+    double v = 0.0;
+    for (int i = threadIdx.x; i < nblk; i += blockDim.x) v += partial[q * nblk + i];
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+      if ((int)threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[q] = sh[0];
+    __syncthreads();
+  }
+}
+
+void srk_launch_reduce(const RedArgs& a, double* out, cudaStream_t st) {
+  switch (a.nt) {
+#define CASE(N) \
+  case N: k_reduce<N><<<SRK_RED_BLOCKS, 256, 0, st>>>(a); break;
+    CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+    default: break;
+  }
+  k_finalize<<<1, 256, 0, st>>>(a.partial, SRK_RED_BLOCKS, out);
+}
+
+// ---------------------------------------------------------------------------
+// K9 forcing helpers (physics.py:209-239): weighted |u|^2 over a small list of
+// band modes (one block, fixed order) and the in-place band rescale.
+// ---------------------------------------------------------------------------
+__global__ void k_band_energy(const cplx* __restrict__ u, const long long* __restrict__ idx,
+                              const double* __restrict__ w, int nb, int ncomp, long long modes,
+                              double* __restrict__ out) {
+  __shared__ double sh[256];
+  double v = 0.0;
+  for (int c = 0; c < ncomp; ++c)
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+      const cplx z = u[c * modes + idx[b]];
+      v = DADD(v, DMUL(w[b], DADD(DMUL(z.x, z.x), DMUL(z.y, z.y))));
+    }
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = sh[0];
+}
+
+__global__ void k_band_scale(cplx* __restrict__ u, const long long* __restrict__ idx, int nb, int ncomp,
+                             long long modes, double gamma) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nb * ncomp) return;
+  const int c = t / nb, b = t - (t / nb) * nb;
+  cplx* p = u + c * modes + idx[b];
+  *p = rmul(gamma, *p);
+}
+
+void srk_launch_project(const ProjArgs& a, cudaStream_t st) {
+  long long blocks = (a.modes + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_project<<<(int)blocks, 256, 0, st>>>(a);
+}
+void srk_launch_curl(const GeomArgs& g, const cplx* u, cplx* w, long long n, cudaStream_t st) {
+  long long blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_curl<<<(int)blocks, 256, 0, st>>>(g, u, w, n);
+}
+void srk_launch_leray(const GeomArgs& g, const cplx* u, cplx* o, long long n, cudaStream_t st) {
+  long long blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_leray<<<(int)blocks, 256, 0, st>>>(g, u, o, n);
+}
+void srk_launch_band_energy(const cplx* u, const long long* idx, const double* w, int nb, int ncomp,
+                            long long modes, double* out, cudaStream_t st) {
+  k_band_energy<<<1, 256, 0, st>>>(u, idx, w, nb, ncomp, modes, out);
+}
+void srk_launch_band_scale(cplx* u, const long long* idx, int nb, int ncomp, long long modes, double gamma,
+                           cudaStream_t st) {
+  const int tot = nb * ncomp;
+  if (tot <= 0) return;
+  k_band_scale<<<(tot + 127) / 128, 128, 0, st>>>(u, idx, nb, ncomp, modes, gamma);
+}

@@ -1,0 +1,60 @@
+// Argument structs / launchers for pointwise.cu (internal to libsrk).
+#pragma once
+
+#include "srk_common.cuh"
+
+#define SRK_NQ 9
+#define SRK_RED_BLOCKS 592  // 4 x 148 SMs; fixed so reductions are run-to-run deterministic
+#define SRK_MAX_TERMS 8
+
+struct GeomArgs {
+  int dims;
+  int n0, n1, K;  // 2D: n1 = 1, K = n_last/2+1
+  double ck0, ck1, ck2;  // 2*pi/L per axis; 2D uses ck0 (x) and ck2 (last)
+};
+
+struct ProjArgs {
+  GeomArgs g;
+  const cplx* G;  // narrow output: [u x w (d), (rho u)(d) if density]
+  const cplx* y;  // state [u (d), rho]
+  cplx* f;
+  long long modes;  // n0*n1*K
+  int density;
+  double nu, ri, re_pr;
+};
+
+struct CombArgs {
+  const cplx* y;  // may be null (start from zero)
+  const cplx* F[SRK_MAX_TERMS];
+  double c[SRK_MAX_TERMS];
+  int nt;
+  cplx* out;
+  long long n;
+};
+
+struct RedArgs {
+  GeomArgs g;
+  const cplx* y0;  // pre-step state (norm)
+  const cplx* y1;  // new state
+  const cplx* F[SRK_MAX_TERMS];
+  double c[SRK_MAX_TERMS];  // h*(b - b_hat) for the error vector
+  int nt;
+  const cplx* fl;  // tendency at y1 (diag)
+  int ncomp;
+  int dvel;
+  long long modes;
+  int K;
+  double atol, rtol;
+  int do_norm, do_diag;
+  double* partial;  // SRK_NQ * SRK_RED_BLOCKS
+};
+
+void srk_launch_project(const ProjArgs& a, cudaStream_t st);
+void srk_launch_curl(const GeomArgs& g, const cplx* u, cplx* w, long long n, cudaStream_t st);
+void srk_launch_leray(const GeomArgs& g, const cplx* u, cplx* o, long long n, cudaStream_t st);
+void srk_launch_combine(const CombArgs& a, cudaStream_t st);
+void srk_launch_reduce(const RedArgs& a, double* out, cudaStream_t st);
+void srk_launch_band_energy(const cplx* u, const long long* idx, const double* w, int nb, int ncomp,
+                            long long modes, double* out, cudaStream_t st);
+void srk_launch_band_scale(cplx* u, const long long* idx, int nb, int ncomp, long long modes, double gamma,
+                           cudaStream_t st);

@@ -1,0 +1,76 @@
+// Kernel registry: one entry per (FFT length, kernel kind).  Fast sizes are
+// compile-time plans instantiated in inst_<M>.cu; anything else small falls back
+// to the runtime GenericFFT entries in inst_generic.cu.
+#pragma once
+
+#include "pass_kernels.cuh"
+
+enum KernelKind {
+  KK_INV = 0,      // strided inverse C2C (+ pad)             K1 plain / K2
+  KK_INV_RHS = 1,  // strided inverse C2C with curl on load   K1
+  KK_FWD = 2,      // strided forward C2C (+ truncation)      K4 / K5
+  KK_Z_C2R = 3,
+  KK_Z_R2C = 4,
+  KK_Z_NS3 = 5,
+  KK_Z_NS2 = 6,
+  KK_Z_B3 = 7,
+  KK_Z_B2 = 8,
+  KK_COUNT = 9
+};
+
+struct KEntry {
+  const void* fn;
+  int nt;    // threads per block
+  int cols;  // columns per block (strided) / complex columns capacity (z)
+  int smem;  // dynamic shared memory bytes
+};
+
+// plain z ops process up to this many real signals per pencil per launch
+#define SRK_Z_PLAIN_C 4
+
+typedef void (*srk_reg_fn)(KEntry* tab);
+
+// Layout used only for the column count of the generic strided engine.
+template <int C_>
+struct GenCols {
+  static constexpr int C = C_;
+};
+
+#define SRK_ENTRY(KFN, ENG, SMB) KEntry{(const void*)(KFN), ENG::NT, ENG::C, (int)(SMB)}
+
+// Instantiate every kernel kind for one fast FFT length.
+#define SRK_DEFINE_SIZE(NAME, M, E, CS, ...)                                                       \
+  void NAME(KEntry* t) {                                                                           \
+    using SL = RowTile<M, CS>;                                                                     \
+    using SE = FastFFT<M, E, SL, __VA_ARGS__>;                                                     \
+    t[KK_INV] = SRK_ENTRY((k_colpass<SE, PK_INV, +1>), SE, SL::SIZE * 16);                         \
+    t[KK_INV_RHS] = SRK_ENTRY((k_colpass<SE, PK_INV_RHS, +1>), SE, SL::SIZE * 16);                 \
+    t[KK_FWD] = SRK_ENTRY((k_colpass<SE, PK_FWD, -1>), SE, SL::SIZE * 16);                         \
+    using Z4 = ColTile<M, 4>;                                                                      \
+    using Z3 = ColTile<M, 3>;                                                                      \
+    using Z6 = ColTile<M, 6>;                                                                      \
+    using Z7 = ColTile<M, 7>;                                                                      \
+    using E4 = FastFFT<M, E, Z4, __VA_ARGS__>;                                                     \
+    using E3 = FastFFT<M, E, Z3, __VA_ARGS__>;                                                     \
+    using E6 = FastFFT<M, E, Z6, __VA_ARGS__>;                                                     \
+    using E7 = FastFFT<M, E, Z7, __VA_ARGS__>;                                                     \
+    t[KK_Z_C2R] = SRK_ENTRY((k_zpass<E4, Z4, ZOP_C2R>), E4, Z4::SIZE * 16);                        \
+    t[KK_Z_R2C] = SRK_ENTRY((k_zpass<E4, Z4, ZOP_R2C>), E4, Z4::SIZE * 16);                        \
+    t[KK_Z_NS3] = SRK_ENTRY((k_zpass<E6, Z6, ZOP_NS3>), E6, Z6::SIZE * 16);                        \
+    t[KK_Z_NS2] = SRK_ENTRY((k_zpass<E3, Z3, ZOP_NS2>), E3, Z3::SIZE * 16);                        \
+    t[KK_Z_B3] = SRK_ENTRY((k_zpass<E7, Z7, ZOP_B3>), E7, Z7::SIZE * 16);                          \
+    t[KK_Z_B2] = SRK_ENTRY((k_zpass<E4, Z4, ZOP_B2>), E4, Z4::SIZE * 16);                          \
+  }
+
+// Unpadded power-of-two lengths only need the plain kinds.
+#define SRK_DEFINE_SIZE_PLAIN(NAME, M, E, CS, ...)                                                 \
+  void NAME(KEntry* t) {                                                                           \
+    using SL = RowTile<M, CS>;                                                                     \
+    using SE = FastFFT<M, E, SL, __VA_ARGS__>;                                                     \
+    t[KK_INV] = SRK_ENTRY((k_colpass<SE, PK_INV, +1>), SE, SL::SIZE * 16);                         \
+    t[KK_FWD] = SRK_ENTRY((k_colpass<SE, PK_FWD, -1>), SE, SL::SIZE * 16);                         \
+    using Z4 = ColTile<M, 4>;                                                                      \
+    using E4 = FastFFT<M, E, Z4, __VA_ARGS__>;                                                     \
+    t[KK_Z_C2R] = SRK_ENTRY((k_zpass<E4, Z4, ZOP_C2R>), E4, Z4::SIZE * 16);                        \
+    t[KK_Z_R2C] = SRK_ENTRY((k_zpass<E4, Z4, ZOP_R2C>), E4, Z4::SIZE * 16);                        \
+  }

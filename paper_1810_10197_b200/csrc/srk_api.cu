@@ -1,0 +1,664 @@
+// libsrk C ABI (include/srk.h): plans, kernel dispatch, RHS / widen / narrow
+// pipelines.  See DESIGN.md for the pass structure and the HBM layout.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/srk.h"
+#include "pointwise.cuh"
+#include "registry.cuh"
+
+// ---------------------------------------------------------------------------
+// registry
+// ---------------------------------------------------------------------------
+void srk_reg_48(KEntry*);
+void srk_reg_96(KEntry*);
+void srk_reg_192(KEntry*);
+void srk_reg_384(KEntry*);
+void srk_reg_768(KEntry*);
+void srk_reg_1536(KEntry*);
+void srk_reg_32(KEntry*);
+void srk_reg_64(KEntry*);
+void srk_reg_128(KEntry*);
+void srk_reg_256(KEntry*);
+void srk_reg_512(KEntry*);
+void srk_reg_1024(KEntry*);
+void srk_reg_generic(KEntry*);
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+struct Table {
+  KEntry e[KK_COUNT];
+};
+
+std::mutex g_mu;
+std::map<int, Table>* g_fast = nullptr;
+Table* g_generic = nullptr;
+std::map<const void*, int> g_smem_set;
+
+void init_registry() {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_fast) return;
+  auto* m = new std::map<int, Table>();
+  struct {
+    int M;
+    srk_reg_fn f;
+  } fs[] = {{48, srk_reg_48},   {96, srk_reg_96},   {192, srk_reg_192}, {384, srk_reg_384},
+            {768, srk_reg_768}, {1536, srk_reg_1536}, {32, srk_reg_32}, {64, srk_reg_64},
+            {128, srk_reg_128}, {256, srk_reg_256}, {512, srk_reg_512}, {1024, srk_reg_1024}};
+  for (auto& x : fs) {
+    Table t;
+    memset(&t, 0, sizeof(t));
+    x.f(t.e);
+    (*m)[x.M] = t;
+  }
+  g_generic = new Table();
+  memset(g_generic, 0, sizeof(Table));
+  srk_reg_generic(g_generic->e);
+  g_fast = m;
+}
+
+bool gen_factor(int M, GenPlan& gp) {
+  gp.M = M;
+  gp.nr = 0;
+  int m = M;
+  const int rs[] = {8, 4, 2, 3, 5, 7};
+  for (int r : rs) {
+    while (m % r == 0) {
+      if (gp.nr >= 10) return false;
+      gp.r[gp.nr++] = r;
+      m /= r;
+    }
+  }
+  return m == 1;
+}
+
+// Find the kernel for (kind, M): a compile-time plan if one exists, else the
+// runtime engine for M <= SRK_GEN_MAXM with factors in {2,3,5,7}.
+int get_entry(int kind, int M, KEntry& e, GenPlan& gp) {
+  init_registry();
+  memset(&gp, 0, sizeof(gp));
+  auto it = g_fast->find(M);
+  if (it != g_fast->end() && it->second.e[kind].fn) {
+    e = it->second.e[kind];
+    gp.M = M;
+    return SRK_OK;
+  }
+  if (M <= SRK_GEN_MAXM && gen_factor(M, gp) && g_generic->e[kind].fn) {
+    e = g_generic->e[kind];
+    return SRK_OK;
+  }
+  return fail(SRK_ERR_UNSUPPORTED, "FFT length " + std::to_string(M) +
+                                       " has no sm_100a plan (supported: 3*2^k and 2^k up to 1536, or "
+                                       "<= 96 with factors 2,3,5,7)");
+}
+
+int ensure_smem(const KEntry& e) {
+  if (e.smem <= 48 * 1024) return SRK_OK;
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_smem_set.find(e.fn);
+  if (it != g_smem_set.end()) return SRK_OK;
+  cudaError_t err = cudaFuncSetAttribute(e.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, e.smem);
+  if (err != cudaSuccess) return fail(SRK_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(err));
+  g_smem_set[e.fn] = 1;
+  return SRK_OK;
+}
+
+int check_launch(const char* what) {
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return fail(SRK_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(err));
+  return SRK_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// plan
+// ---------------------------------------------------------------------------
+struct srk_plan {
+  int dims, density, max_comps;
+  int n0, n1, n2, K, m0, m1, m2;  // 2D: n1 = m1 = 1 and n2 = last axis
+  double ck0, ck1, ck2;
+  long long modes;  // n0*n1*K per component
+  int S, So;        // rhs signal counts (widened, products)
+  std::map<int, cplx*> tw;
+  long long A_elems = 0, B_elems = 0;
+  char* ws = nullptr;
+  long long ws_bytes = 0, need_bytes = 0;
+  cplx* A = nullptr;
+  cplx* B = nullptr;
+  double* partial = nullptr;
+  int last_launches = 0;
+  // optional per-kernel timing of srk_rhs (srk_rhs_timed)
+  bool timing = false;
+  cudaEvent_t ev[16];
+  int nev = 0;
+  cudaStream_t tstream = nullptr;
+};
+
+namespace {
+
+long long align256(long long b) { return (b + 255) / 256 * 256; }
+
+int get_tw(srk_plan* p, int M, const cplx** out) {
+  auto it = p->tw.find(M);
+  if (it != p->tw.end()) {
+    *out = it->second;
+    return SRK_OK;
+  }
+  std::vector<double2> h(M);
+  for (int e = 0; e < M; ++e) {
+    // exp(-2 pi i e / M) with the angle reduced exactly in integers, long double math
+    const long double ang = 2.0L * 3.14159265358979323846264338327950288L * (long double)e / (long double)M;
+    h[e] = make_double2((double)cosl(ang), (double)-sinl(ang));
+  }
+  cplx* d = nullptr;
+  cudaError_t err = cudaMalloc(&d, sizeof(cplx) * M);
+  if (err != cudaSuccess) return fail(SRK_ERR_CUDA, std::string("cudaMalloc(twiddles): ") + cudaGetErrorString(err));
+  err = cudaMemcpy(d, h.data(), sizeof(cplx) * M, cudaMemcpyHostToDevice);
+  if (err != cudaSuccess) return fail(SRK_ERR_CUDA, std::string("cudaMemcpy(twiddles): ") + cudaGetErrorString(err));
+  p->tw[M] = d;
+  *out = d;
+  return SRK_OK;
+}
+
+int need_ws(srk_plan* p) {
+  if (!p->A) return fail(SRK_ERR_WORKSPACE, "plan has no workspace bound (srk_plan_set_workspace)");
+  return SRK_OK;
+}
+
+// ---- strided pass launch -------------------------------------------------
+int launch_col(srk_plan* p, int kind, PassArgs a, cudaStream_t st) {
+  KEntry e;
+  int rc = get_entry(kind, a.M, e, a.gp);
+  if (rc) return rc;
+  if ((rc = get_tw(p, a.M, &a.tw))) return rc;
+  if ((rc = ensure_smem(e))) return rc;
+  a.tpp = (a.Qp + e.cols - 1) / e.cols;
+  const long long grid = (long long)a.planes * a.tpp;
+  if (grid <= 0) return SRK_OK;
+  void* args[] = {&a};
+  cudaError_t err = cudaLaunchKernel(e.fn, dim3((unsigned)grid), dim3(e.nt), args, e.smem, st);
+  if (err != cudaSuccess) return fail(SRK_ERR_CUDA, std::string("colpass launch: ") + cudaGetErrorString(err));
+  p->last_launches++;
+  if (p->timing && p->nev < 16) cudaEventRecord(p->ev[p->nev++], st);
+  return SRK_OK;
+}
+
+// ---- z pass launch (pairs of pencils) ---------------------------------------
+int launch_z(srk_plan* p, int kind, ZArgs a, int S_rt, int So_rt, cudaStream_t st) {
+  KEntry e;
+  int rc = get_entry(kind, a.M, e, a.gp);
+  if (rc) return rc;
+  if ((rc = get_tw(p, a.M, &a.tw))) return rc;
+  if ((rc = ensure_smem(e))) return rc;
+  const int grid = (a.P + 1) / 2;
+  void* args[] = {&a, &S_rt, &So_rt};
+  cudaError_t err = cudaLaunchKernel(e.fn, dim3(grid), dim3(e.nt), args, e.smem, st);
+  if (err != cudaSuccess) return fail(SRK_ERR_CUDA, std::string("zpass launch: ") + cudaGetErrorString(err));
+  p->last_launches++;
+  if (p->timing && p->nev < 16) cudaEventRecord(p->ev[p->nev++], st);
+  return SRK_OK;
+}
+
+GeomArgs geom(const srk_plan* p) {
+  GeomArgs g;
+  g.dims = p->dims;
+  g.n0 = p->n0;
+  g.n1 = p->n1;
+  g.K = p->K;
+  g.ck0 = p->ck0;
+  g.ck1 = p->ck1;
+  g.ck2 = p->ck2;
+  return g;
+}
+
+PassArgs base_pass() {
+  PassArgs a;
+  memset(&a, 0, sizeof(a));
+  a.scale = 1.0;
+  return a;
+}
+
+// x pass: planes = signals, columns = (y, kz) flattened
+PassArgs x_pass(const srk_plan* p, const cplx* in, cplx* out, int nsig, int n_in_rows, int n_out_rows, int M,
+                int n) {
+  PassArgs a = base_pass();
+  a.in = in;
+  a.out = out;
+  a.M = M;
+  a.n = n;
+  a.planes = nsig;
+  a.Qp = p->n1 * p->K;
+  a.sig_minor = 1;
+  a.row_stride = (long long)p->n1 * p->K;
+  a.in_plane_stride = (long long)n_in_rows * a.row_stride;
+  a.out_plane_stride = (long long)n_out_rows * a.row_stride;
+  return a;
+}
+
+// y pass (3D): planes = (signal, x), columns = kz
+PassArgs y_pass(const srk_plan* p, const cplx* in, cplx* out, int nsig, int xrows, int n_in_rows,
+                int n_out_rows, int M, int n) {
+  PassArgs a = base_pass();
+  a.in = in;
+  a.out = out;
+  a.M = M;
+  a.n = n;
+  a.planes = nsig * xrows;
+  a.Qp = p->K;
+  a.sig_minor = 0;
+  a.row_stride = p->K;
+  a.in_plane_stride = (long long)n_in_rows * p->K;
+  a.out_plane_stride = (long long)n_out_rows * p->K;
+  return a;
+}
+
+ZArgs z_args(const srk_plan* p, int M, int n, int P) {
+  ZArgs z;
+  memset(&z, 0, sizeof(z));
+  z.M = M;
+  z.n = n;
+  z.K = p->K;
+  z.P = P;
+  return z;
+}
+
+// inverse 3/2-padded (pad=true) or plain (pad=false) transform of c signals:
+// spec (c, n0, n1, K) -> phys (c, M0, M1, M2)
+int inverse_chain(srk_plan* p, const cplx* spec, int c, double* phys, bool pad, cudaStream_t st) {
+  const int M0 = pad ? p->m0 : p->n0, M1 = pad ? p->m1 : p->n1, M2 = pad ? p->m2 : p->n2;
+  const double scale = (pad ? std::pow(1.5, p->dims) : 1.0) / ((double)M0 * M1 * M2);
+  PassArgs a = x_pass(p, spec, p->A, c, p->n0, M0, M0, p->n0);
+  a.scale = scale;
+  int rc = launch_col(p, KK_INV, a, st);
+  if (rc) return rc;
+  const cplx* zin = p->A;
+  if (p->dims == 3) {
+    PassArgs b = y_pass(p, p->A, p->B, c, M0, p->n1, M1, M1, p->n1);
+    if ((rc = launch_col(p, KK_INV, b, st))) return rc;
+    zin = p->B;
+  }
+  const int P = M0 * M1;
+  for (int s0 = 0; s0 < c; s0 += SRK_Z_PLAIN_C) {
+    const int sc = std::min(SRK_Z_PLAIN_C, c - s0);
+    ZArgs z = z_args(p, M2, p->n2, P);
+    z.in_sig_stride = (long long)P * p->K;
+    z.out_sig_stride = (long long)P * M2;
+    z.in = zin + s0 * z.in_sig_stride;
+    z.out_real = phys + s0 * z.out_sig_stride;
+    if ((rc = launch_z(p, KK_Z_C2R, z, sc, 0, st))) return rc;
+  }
+  return SRK_OK;
+}
+
+// forward (narrow when trunc=true, plain rfftn otherwise): phys -> spec
+int forward_chain(srk_plan* p, const double* phys, int c, cplx* spec, bool trunc, cudaStream_t st) {
+  const int M0 = trunc ? p->m0 : p->n0, M1 = trunc ? p->m1 : p->n1, M2 = trunc ? p->m2 : p->n2;
+  const int P = M0 * M1;
+  int rc;
+  for (int s0 = 0; s0 < c; s0 += SRK_Z_PLAIN_C) {
+    const int sc = std::min(SRK_Z_PLAIN_C, c - s0);
+    ZArgs z = z_args(p, M2, p->n2, P);
+    z.in_sig_stride = (long long)P * M2;
+    z.out_sig_stride = (long long)P * p->K;
+    z.in_real = phys + s0 * z.in_sig_stride;
+    z.out = p->A + s0 * z.out_sig_stride;
+    z.zero_nyq = trunc ? 1 : 0;
+    if ((rc = launch_z(p, KK_Z_R2C, z, 0, sc, st))) return rc;
+  }
+  const cplx* xin = p->A;
+  if (p->dims == 3) {
+    PassArgs b = y_pass(p, p->A, p->B, c, M0, M1, p->n1, M1, p->n1);
+    b.zero_nyq = trunc ? 1 : 0;
+    if ((rc = launch_col(p, KK_FWD, b, st))) return rc;
+    xin = p->B;
+  }
+  PassArgs a = x_pass(p, xin, spec, c, M0, p->n0, M0, p->n0);
+  a.scale = trunc ? std::pow(1.0 / 1.5, p->dims) : 1.0;
+  a.zero_nyq = trunc ? 1 : 0;
+  a.zero_dc_imag = trunc ? 1 : 0;
+  return launch_col(p, KK_FWD, a, st);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int srk_abi_version(void) { return 1; }
+
+const char* srk_last_error(void) { return g_err.c_str(); }
+
+int srk_plan_create(srk_plan** out, int dims, const int64_t* shape, const double* lengths, int density,
+                    int max_comps) {
+  if (!out) return fail(SRK_ERR_INVALID, "null plan pointer");
+  *out = nullptr;
+  if (dims != 2 && dims != 3) return fail(SRK_ERR_INVALID, "grid must be 2D or 3D, got " + std::to_string(dims) + " axes");
+  for (int i = 0; i < dims; ++i) {
+    if (shape[i] < 4 || shape[i] % 2)
+      return fail(SRK_ERR_INVALID, "grid extent " + std::to_string(shape[i]) + " must be even and >= 4");
+    if (!(lengths[i] > 0)) return fail(SRK_ERR_INVALID, "domain lengths must be positive");
+  }
+  srk_plan* p = new srk_plan();
+  p->dims = dims;
+  p->density = density ? 1 : 0;
+  const double two_pi = 2.0 * 3.141592653589793;
+  if (dims == 3) {
+    p->n0 = (int)shape[0];
+    p->n1 = (int)shape[1];
+    p->n2 = (int)shape[2];
+    p->ck0 = two_pi / lengths[0];
+    p->ck1 = two_pi / lengths[1];
+    p->ck2 = two_pi / lengths[2];
+  } else {
+    p->n0 = (int)shape[0];
+    p->n1 = 1;
+    p->n2 = (int)shape[1];
+    p->ck0 = two_pi / lengths[0];
+    p->ck1 = 0.0;
+    p->ck2 = two_pi / lengths[1];
+  }
+  p->K = p->n2 / 2 + 1;
+  p->m0 = 3 * p->n0 / 2;
+  p->m1 = dims == 3 ? 3 * p->n1 / 2 : 1;
+  p->m2 = 3 * p->n2 / 2;
+  p->modes = (long long)p->n0 * p->n1 * p->K;
+  const int d = dims, wc = dims == 3 ? 3 : 1;
+  p->S = d + wc + p->density;
+  p->So = p->density ? 2 * d : d;
+  const int nstate = d + p->density;
+  p->max_comps = std::max(max_comps, nstate);
+  // every padded length must have a kernel
+  {
+    KEntry e;
+    GenPlan gp;
+    int lens[3] = {p->m0, p->m1, p->m2};
+    for (int i = 0; i < 3; ++i) {
+      if (lens[i] == 1) continue;
+      int rc = get_entry(i == 2 ? KK_Z_C2R : KK_INV, lens[i], e, gp);
+      if (rc) {
+        delete p;
+        return rc;
+      }
+    }
+  }
+  // workspace regions (complex elements)
+  const long long K = p->K, n0 = p->n0, n1 = p->n1, m0 = p->m0, m1 = p->m1;
+  const long long c = std::max<long long>(p->max_comps, 1);
+  long long A = 0, B = 0;
+  auto upA = [&](long long v) { A = std::max(A, v); };
+  auto upB = [&](long long v) { B = std::max(B, v); };
+  if (dims == 3) {
+    upA(p->S * m0 * n1 * K);   // K1 out
+    upB(p->S * m0 * m1 * K);   // K2 out
+    upA(p->So * m0 * m1 * K);  // K3 out
+    upB(p->So * m0 * n1 * K);  // K4 out
+    upA(p->So * n0 * n1 * K);  // K5 out (G)
+    upA(c * m0 * n1 * K);
+    upB(c * m0 * m1 * K);
+    upA(c * m0 * m1 * K);
+    upB(c * m0 * n1 * K);
+  } else {
+    upA(p->S * m0 * K);
+    upB(p->So * m0 * K);
+    upA(p->So * n0 * K);
+    upA(c * m0 * K);
+  }
+  p->A_elems = A;
+  p->B_elems = B;
+  p->need_bytes = align256(A * 16) + align256(std::max<long long>(B, 1) * 16);
+  {
+    cudaError_t err = cudaMalloc(&p->partial, sizeof(double) * SRK_NQ * SRK_RED_BLOCKS);
+    if (err != cudaSuccess) {
+      delete p;
+      return fail(SRK_ERR_CUDA, std::string("cudaMalloc(partials): ") + cudaGetErrorString(err));
+    }
+  }
+  *out = p;
+  return SRK_OK;
+}
+
+void srk_plan_destroy(srk_plan* p) {
+  if (!p) return;
+  for (auto& kv : p->tw) cudaFree(kv.second);
+  if (p->partial) cudaFree(p->partial);
+  delete p;
+}
+
+int srk_plan_workspace_bytes(const srk_plan* p, int64_t* bytes) {
+  if (!p || !bytes) return fail(SRK_ERR_INVALID, "null argument");
+  *bytes = p->need_bytes;
+  return SRK_OK;
+}
+
+int srk_plan_set_workspace(srk_plan* p, void* ptr, int64_t bytes) {
+  if (!p) return fail(SRK_ERR_INVALID, "null plan");
+  if (bytes < p->need_bytes)
+    return fail(SRK_ERR_WORKSPACE, "workspace too small: " + std::to_string(bytes) + " < " + std::to_string(p->need_bytes));
+  if (((uintptr_t)ptr) % 256) return fail(SRK_ERR_WORKSPACE, "workspace must be 256-byte aligned");
+  char* b = (char*)ptr;
+  p->ws = b;
+  p->ws_bytes = bytes;
+  p->A = (cplx*)b;
+  b += align256(p->A_elems * 16);
+  p->B = (cplx*)b;
+  return SRK_OK;
+}
+
+int srk_rhs(srk_plan* p, const void* y_, void* f_, double nu, double ri, double re_pr, void* stream) {
+  if (!p) return fail(SRK_ERR_INVALID, "null plan");
+  int rc = need_ws(p);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const cplx* y = (const cplx*)y_;
+  cplx* f = (cplx*)f_;
+  p->last_launches = 0;
+  const int d = p->dims;
+  // K1: curl + x pad + inverse x
+  PassArgs a = x_pass(p, y, p->A, p->S, p->n0, p->m0, p->m0, p->n0);
+  a.scale = std::pow(1.5, d) / ((double)p->m0 * p->m1 * p->m2);
+  a.dims = d;
+  a.n1 = p->n1;
+  a.K = p->K;
+  a.ck0 = p->ck0;
+  a.ck1 = p->ck1;
+  a.ck2 = p->ck2;
+  a.comp_stride = p->modes;
+  if ((rc = launch_col(p, KK_INV_RHS, a, st))) return rc;
+  const cplx* zin = p->A;
+  cplx* zout = p->B;
+  if (d == 3) {
+    // K2: y pad + inverse y
+    PassArgs b = y_pass(p, p->A, p->B, p->S, p->m0, p->n1, p->m1, p->m1, p->n1);
+    if ((rc = launch_col(p, KK_INV, b, st))) return rc;
+    zin = p->B;
+    zout = p->A;
+  }
+  // K3: z C2R -> products -> z R2C
+  const int P = p->m0 * p->m1;
+  ZArgs z = z_args(p, p->m2, p->n2, P);
+  z.in = zin;
+  z.out = zout;
+  z.in_sig_stride = (long long)P * p->K;
+  z.out_sig_stride = (long long)P * p->K;
+  z.zero_nyq = 1;
+  const int kind = d == 3 ? (p->density ? KK_Z_B3 : KK_Z_NS3) : (p->density ? KK_Z_B2 : KK_Z_NS2);
+  if ((rc = launch_z(p, kind, z, 0, 0, st))) return rc;
+  const cplx* xin = zout;
+  cplx* gbuf = p->A;
+  if (d == 3) {
+    // K4: forward y + truncate
+    PassArgs b = y_pass(p, p->A, p->B, p->So, p->m0, p->m1, p->n1, p->m1, p->n1);
+    b.zero_nyq = 1;
+    if ((rc = launch_col(p, KK_FWD, b, st))) return rc;
+    xin = p->B;
+  }
+  // K5: forward x + truncate + 1/1.5^d + Nyquist / DC-imag zeroing -> G
+  PassArgs c5 = x_pass(p, xin, gbuf, p->So, p->m0, p->n0, p->m0, p->n0);
+  c5.scale = std::pow(1.0 / 1.5, d);
+  c5.zero_nyq = 1;
+  c5.zero_dc_imag = 1;
+  if ((rc = launch_col(p, KK_FWD, c5, st))) return rc;
+  // K6: projection + viscous (+ Boussinesq terms)
+  ProjArgs pa;
+  pa.g = geom(p);
+  pa.G = gbuf;
+  pa.y = y;
+  pa.f = f;
+  pa.modes = p->modes;
+  pa.density = p->density;
+  pa.nu = nu;
+  pa.ri = ri;
+  pa.re_pr = re_pr;
+  srk_launch_project(pa, st);
+  p->last_launches++;
+  if (p->timing && p->nev < 16) cudaEventRecord(p->ev[p->nev++], st);
+  return check_launch("k_project");
+}
+
+int srk_rhs_timed(srk_plan* p, const void* y, void* f, double nu, double ri, double re_pr, void* stream,
+                  float* ms_out, int max_kernels) {
+  if (!p) return fail(SRK_ERR_INVALID, "null plan");
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int i = 0; i < 16; ++i) cudaEventCreate(&p->ev[i]);
+  p->timing = true;
+  p->nev = 0;
+  cudaEventRecord(p->ev[p->nev++], st);
+  int rc = srk_rhs(p, y, f, nu, ri, re_pr, stream);
+  p->timing = false;
+  if (rc == SRK_OK) {
+    cudaError_t err = cudaEventSynchronize(p->ev[p->nev - 1]);
+    if (err != cudaSuccess) rc = fail(SRK_ERR_CUDA, std::string("srk_rhs_timed: ") + cudaGetErrorString(err));
+  }
+  int n = p->nev - 1;
+  if (rc == SRK_OK)
+    for (int i = 0; i < n && i < max_kernels; ++i) cudaEventElapsedTime(&ms_out[i], p->ev[i], p->ev[i + 1]);
+  for (int i = 0; i < 16; ++i) cudaEventDestroy(p->ev[i]);
+  return rc == SRK_OK ? -n : rc;  // negative = kernel count on success
+}
+
+int srk_rhs_launch_count(const srk_plan* p) { return p ? p->last_launches : 0; }
+
+int srk_widen(srk_plan* p, const void* spec, int ncomp, void* phys, void* stream) {
+  if (!p) return fail(SRK_ERR_INVALID, "null plan");
+  int rc = need_ws(p);
+  if (rc) return rc;
+  if (ncomp < 1 || ncomp > p->max_comps)
+    return fail(SRK_ERR_INVALID, std::to_string(ncomp) + " components exceed workspace size " + std::to_string(p->max_comps));
+  return inverse_chain(p, (const cplx*)spec, ncomp, (double*)phys, true, (cudaStream_t)stream);
+}
+
+int srk_narrow(srk_plan* p, const void* phys, int ncomp, void* spec, void* stream) {
+  if (!p) return fail(SRK_ERR_INVALID, "null plan");
+  int rc = need_ws(p);
+  if (rc) return rc;
+  if (ncomp < 1 || ncomp > p->max_comps)
+    return fail(SRK_ERR_INVALID, std::to_string(ncomp) + " components exceed workspace size " + std::to_string(p->max_comps));
+  return forward_chain(p, (const double*)phys, ncomp, (cplx*)spec, true, (cudaStream_t)stream);
+}
+
+int srk_forward_transform(srk_plan* p, const void* phys, int ncomp, void* spec, void* stream) {
+  if (!p) return fail(SRK_ERR_INVALID, "null plan");
+  int rc = need_ws(p);
+  if (rc) return rc;
+  if (ncomp < 1 || ncomp > p->max_comps) return fail(SRK_ERR_INVALID, "component count exceeds the plan's workspace");
+  return forward_chain(p, (const double*)phys, ncomp, (cplx*)spec, false, (cudaStream_t)stream);
+}
+
+int srk_inverse_transform(srk_plan* p, const void* spec, int ncomp, void* phys, void* stream) {
+  if (!p) return fail(SRK_ERR_INVALID, "null plan");
+  int rc = need_ws(p);
+  if (rc) return rc;
+  if (ncomp < 1 || ncomp > p->max_comps) return fail(SRK_ERR_INVALID, "component count exceeds the plan's workspace");
+  return inverse_chain(p, (const cplx*)spec, ncomp, (double*)phys, false, (cudaStream_t)stream);
+}
+
+int srk_curl(srk_plan* p, const void* u, void* w, void* stream) {
+  if (!p) return fail(SRK_ERR_INVALID, "null plan");
+  srk_launch_curl(geom(p), (const cplx*)u, (cplx*)w, p->modes, (cudaStream_t)stream);
+  return check_launch("k_curl");
+}
+
+int srk_leray_project(srk_plan* p, const void* u, void* out, void* stream) {
+  if (!p) return fail(SRK_ERR_INVALID, "null plan");
+  srk_launch_leray(geom(p), (const cplx*)u, (cplx*)out, p->modes, (cudaStream_t)stream);
+  return check_launch("k_leray");
+}
+
+int srk_combine(int64_t n, const void* y, int nterms, const void* const* F, const double* coef, void* out,
+                void* stream) {
+  if (nterms < 0 || nterms > SRK_MAX_TERMS) return fail(SRK_ERR_INVALID, "srk_combine: at most 8 terms");
+  CombArgs a;
+  memset(&a, 0, sizeof(a));
+  a.y = (const cplx*)y;
+  for (int j = 0; j < nterms; ++j) {
+    a.F[j] = (const cplx*)F[j];
+    a.c[j] = coef[j];
+  }
+  a.nt = nterms;
+  a.out = (cplx*)out;
+  a.n = n;
+  srk_launch_combine(a, (cudaStream_t)stream);
+  return check_launch("k_combine");
+}
+
+int srk_step_reduce(srk_plan* p, const void* y0, const void* y1, int nterms, const void* const* F,
+                    const double* coef, const void* fl, int ncomp, double tol_abs, double tol_rel, int flags,
+                    double* out_dev, void* stream) {
+  if (!p) return fail(SRK_ERR_INVALID, "null plan");
+  if (nterms < 0 || nterms > SRK_MAX_TERMS) return fail(SRK_ERR_INVALID, "srk_step_reduce: at most 8 terms");
+  if (ncomp < 1 || ncomp > 4) return fail(SRK_ERR_INVALID, "srk_step_reduce: 1..4 components");
+  RedArgs a;
+  memset(&a, 0, sizeof(a));
+  a.g = geom(p);
+  a.y0 = (const cplx*)y0;
+  a.y1 = (const cplx*)y1;
+  a.do_norm = (flags & 1) ? 1 : 0;
+  a.do_diag = (flags & 2) ? 1 : 0;
+  a.nt = a.do_norm ? nterms : 0;
+  for (int j = 0; j < a.nt; ++j) {
+    a.F[j] = (const cplx*)F[j];
+    a.c[j] = coef[j];
+  }
+  a.fl = (const cplx*)fl;
+  a.ncomp = ncomp;
+  a.dvel = std::min(p->dims, ncomp);
+  a.modes = p->modes;
+  a.K = p->K;
+  a.atol = tol_abs;
+  a.rtol = tol_rel;
+  a.partial = p->partial;
+  srk_launch_reduce(a, out_dev, (cudaStream_t)stream);
+  return check_launch("k_reduce");
+}
+
+int srk_band_energy(srk_plan* p, const void* u, int ncomp, const int64_t* idx, const double* w, int nb,
+                    double* out_dev, void* stream) {
+  if (!p) return fail(SRK_ERR_INVALID, "null plan");
+  srk_launch_band_energy((const cplx*)u, (const long long*)idx, w, nb, ncomp, p->modes, out_dev,
+                         (cudaStream_t)stream);
+  return check_launch("k_band_energy");
+}
+
+int srk_band_scale(srk_plan* p, void* u, int ncomp, const int64_t* idx, int nb, double gamma, void* stream) {
+  if (!p) return fail(SRK_ERR_INVALID, "null plan");
+  srk_launch_band_scale((cplx*)u, (const long long*)idx, nb, ncomp, p->modes, gamma, (cudaStream_t)stream);
+  return check_launch("k_band_scale");
+}
+
+}  // extern "C"

@@ -1,0 +1,210 @@
+// Common device helpers for the sm_100a spectral NS path: complex fp64 arithmetic
+// and the in-register DFT butterflies used by the FFT engines (fft_engine.cuh).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "twiddle_consts.h"
+
+typedef double2 cplx;
+
+#define SRK_DEV __host__ __device__ __forceinline__
+
+SRK_DEV cplx cmk(double r, double i) { return make_double2(r, i); }
+SRK_DEV cplx cadd(cplx a, cplx b) { return make_double2(a.x + b.x, a.y + b.y); }
+SRK_DEV cplx csub(cplx a, cplx b) { return make_double2(a.x - b.x, a.y - b.y); }
+SRK_DEV cplx cscale(cplx a, double s) { return make_double2(a.x * s, a.y * s); }
+SRK_DEV cplx cconj(cplx a) { return make_double2(a.x, -a.y); }
+SRK_DEV cplx cmul(cplx a, cplx b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// multiply by SIGN*i
+template <int SIGN>
+SRK_DEV cplx cmul_si(cplx a) {
+  return SIGN > 0 ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
+}
+
+// ---------------------------------------------------------------------------
+// Multiply by the compile-time constant exp(SIGN * 2*pi*i * m / 48).
+// Cheap paths for multiples of pi/4; generic complex multiply otherwise.
+// ---------------------------------------------------------------------------
+template <int M48, int SIGN>
+SRK_DEV cplx twc(cplx a) {
+  constexpr int m = ((M48 % 48) + 48) % 48;
+  if constexpr (m == 0) {
+    return a;
+  } else if constexpr (m == 12) {
+    return cmul_si<SIGN>(a);
+  } else if constexpr (m == 24) {
+    return make_double2(-a.x, -a.y);
+  } else if constexpr (m == 36) {
+    return cmul_si<-SIGN>(a);
+  } else if constexpr (m == 6 || m == 18 || m == 30 || m == 42) {
+    constexpr double r = 0.7071067811865476;  // sqrt(2)/2
+    constexpr double c = kcos48(m) > 0 ? 1.0 : -1.0;
+    constexpr double s = (ksin48(m) > 0 ? 1.0 : -1.0) * (SIGN > 0 ? 1.0 : -1.0);
+    // (a.x + i a.y)(c + i s) r
+    return make_double2((c * a.x - s * a.y) * r, (s * a.x + c * a.y) * r);
+  } else {
+    constexpr double c = kcos48(m);
+    constexpr double s = (SIGN > 0 ? 1.0 : -1.0) * ksin48(m);
+    return make_double2(fma(a.x, c, -a.y * s), fma(a.x, s, a.y * c));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// DFT_R in registers: v'[q] = sum_t v[t] exp(SIGN*2*pi*i*t*q/R), in place.
+// ---------------------------------------------------------------------------
+template <int R, int SIGN>
+struct DFT;
+
+template <int SIGN>
+struct DFT<1, SIGN> {
+  SRK_DEV static void run(cplx*) {}
+};
+
+template <int SIGN>
+struct DFT<2, SIGN> {
+  SRK_DEV static void run(cplx* v) {
+    cplx a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+  }
+};
+
+template <int SIGN>
+struct DFT<3, SIGN> {
+  SRK_DEV static void run(cplx* v) {
+    constexpr double h = 0.8660254037844386;  // sqrt(3)/2
+    cplx s = cadd(v[1], v[2]);
+    cplx d = csub(v[1], v[2]);
+    cplx m = make_double2(fma(-0.5, s.x, v[0].x), fma(-0.5, s.y, v[0].y));
+    cplx r = cmul_si<SIGN>(cscale(d, h));
+    v[0] = cadd(v[0], s);
+    v[1] = cadd(m, r);
+    v[2] = csub(m, r);
+  }
+};
+
+template <int SIGN>
+struct DFT<4, SIGN> {
+  SRK_DEV static void run(cplx* v) {
+    cplx a = cadd(v[0], v[2]), b = csub(v[0], v[2]);
+    cplx c = cadd(v[1], v[3]), d = cmul_si<SIGN>(csub(v[1], v[3]));
+    v[0] = cadd(a, c);
+    v[2] = csub(a, c);
+    v[1] = cadd(b, d);
+    v[3] = csub(b, d);
+  }
+};
+
+// odd prime radix via symmetric pairs (generic engine only)
+template <int R, int SIGN>
+struct DFTPrime {
+  SRK_DEV static double co(int m) { return R == 5 ? kcos5(m) : kcos7(m); }
+  SRK_DEV static double si(int m) { return R == 5 ? ksin5(m) : ksin7(m); }
+  SRK_DEV static void run(cplx* v) {
+    cplx out[R];
+    cplx sum = v[0];
+#pragma unroll
+    for (int t = 1; t < R; ++t) sum = cadd(sum, v[t]);
+    out[0] = sum;
+#pragma unroll
+    for (int q = 1; q < R; ++q) {
+      cplx acc = v[0];
+#pragma unroll
+      for (int t = 1; t <= (R - 1) / 2; ++t) {
+        double c = co(t * q), s = (SIGN > 0 ? 1.0 : -1.0) * si(t * q);
+        cplx p = cadd(v[t], v[R - t]);
+        cplx m = csub(v[t], v[R - t]);
+        acc.x += p.x * c - m.y * s;
+        acc.y += p.y * c + m.x * s;
+      }
+      out[q] = acc;
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) v[q] = out[q];
+  }
+};
+template <int SIGN>
+struct DFT<5, SIGN> : DFTPrime<5, SIGN> {};
+template <int SIGN>
+struct DFT<7, SIGN> : DFTPrime<7, SIGN> {};
+
+// Composite radix R = A*B: t = B*a + b, q = q1 + A*q2.
+template <int A, int B, int SIGN>
+struct DFTComposite {
+  static constexpr int R = A * B;
+  static_assert(48 % R == 0, "composite radix must divide 48");
+  template <int b, int q1>
+  SRK_DEV static void tw(cplx (&u)[B][A]) {
+    u[b][q1] = twc<(b * q1 * (48 / R)), SIGN>(u[b][q1]);
+  }
+  template <int b, int q1>
+  SRK_DEV static void tw_row(cplx (&u)[B][A]) {
+    if constexpr (q1 < A) {
+      tw<b, q1>(u);
+      tw_row<b, q1 + 1>(u);
+    }
+  }
+  template <int b>
+  SRK_DEV static void tw_all(cplx (&u)[B][A]) {
+    if constexpr (b < B) {
+      tw_row<b, 0>(u);
+      tw_all<b + 1>(u);
+    }
+  }
+  SRK_DEV static void run(cplx* v) {
+    cplx u[B][A];
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+#pragma unroll
+      for (int a = 0; a < A; ++a) u[b][a] = v[B * a + b];
+      DFT<A, SIGN>::run(u[b]);
+    }
+    tw_all<0>(u);
+#pragma unroll
+    for (int q1 = 0; q1 < A; ++q1) {
+      cplx z[B];
+#pragma unroll
+      for (int b = 0; b < B; ++b) z[b] = u[b][q1];
+      DFT<B, SIGN>::run(z);
+#pragma unroll
+      for (int q2 = 0; q2 < B; ++q2) v[q1 + A * q2] = z[q2];
+    }
+  }
+};
+template <int SIGN>
+struct DFT<6, SIGN> : DFTComposite<2, 3, SIGN> {};
+template <int SIGN>
+struct DFT<8, SIGN> : DFTComposite<2, 4, SIGN> {};
+template <int SIGN>
+struct DFT<12, SIGN> : DFTComposite<4, 3, SIGN> {};
+template <int SIGN>
+struct DFT<16, SIGN> : DFTComposite<4, 4, SIGN> {};
+template <int SIGN>
+struct DFT<24, SIGN> : DFTComposite<8, 3, SIGN> {};
+
+// ---------------------------------------------------------------------------
+// Row maps for the 3/2-rule padding (spectral.py:229-258 widen, :276-301 narrow).
+// pad_src: padded row r -> coarse row, or -1 inside the zero band.
+// trunc_dst: padded row r -> coarse row, -1 = discard, -2 = write zero at n/2.
+// With m == n both are the identity (unpadded transforms).
+// ---------------------------------------------------------------------------
+SRK_DEV int pad_src(int r, int n, int m) {
+  const int h = n >> 1;
+  if (r <= h) return r;
+  if (r >= m - (h - 1)) return r - (m - n);
+  return -1;
+}
+SRK_DEV int trunc_dst(int r, int n, int m, bool zero_nyq) {
+  const int h = n >> 1;
+  if (r < h) return r;
+  if (r == h) return zero_nyq ? -2 : (m == n ? r : -1);
+  if (r >= m - (h - 1)) return r - (m - n);
+  return -1;
+}
+
+// full-axis mode label (grid.py:75-82): Nyquist relabelled +n/2
+SRK_DEV double mode_full(int i, int n) { return (double)(i <= (n >> 1) ? i : i - n); }

@@ -1,0 +1,78 @@
+"""Per-step diagnostics on the device (mirrors diagnostics.py:27-70 of the reference).
+
+E_kin, eps and the enstrophy come from one deterministic fused
+reduction kernel (csrc/pointwise.cu k_reduce, flags=2).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _native
+from .grid import Grid
+from .spectral import get_plan, to_device
+
+__all__ = ["DiagnosticsRecord", "kinetic_energy", "dissipation_rate", "enstrophy", "reduce_sums",
+           "diag_from_sums"]
+
+
+@dataclass
+class DiagnosticsRecord:
+    """One per-step row (diagnostics.py:27-36) plus the enstrophy (D2)."""
+
+    t: float
+    h: float
+    e_kin: float
+    eps: float
+    rhs_evals: int
+    rejections: int
+    enstrophy: float = float("nan")
+
+
+def reduce_sums(grid: Grid, y1, fl=None, y0=None, terms=(), tol_abs=0.0, tol_rel=0.0, flags=2, ncomp=None,
+                stream=None):
+    """Launch srk_step_reduce; returns the 9 device sums as a CUDA float64 tensor (no sync)."""
+    p = get_plan(grid)
+    ncomp = y1.shape[0] if ncomp is None else ncomp
+    out = torch.empty(9, dtype=torch.float64, device=y1.device)
+    Fs = [t for _, t in terms]
+    cs = [c for c, _ in terms]
+    _native.check(p.lib.srk_step_reduce(
+        p.h, _native.ptr(y0), _native.ptr(y1), len(Fs), _native.ptr_array(Fs), _native.dbl_array(cs),
+        _native.ptr(fl if fl is not None else y1), ncomp, float(tol_abs), float(tol_rel), int(flags),
+        _native.ptr(out), _native.stream_ptr(stream)), "srk_step_reduce")
+    _native.count(2)
+    return out
+
+
+def diag_from_sums(q, grid: Grid):
+    """(E_kin, eps, Z) from reduce sums (diagnostics.py:48-70)."""
+    pts2 = float(grid.points) ** 2
+    return q[4] / (2.0 * pts2), -q[5] / pts2, q[8] / (2.0 * pts2)
+
+
+def kinetic_energy(u_hat, grid: Grid):
+    """E = sum_k w_k sum_j |u_kj|^2 / (2 points^2) (diagnostics.py:48-50)."""
+    u, _ = to_device(u_hat, torch.complex128)
+    q = reduce_sums(grid, u, flags=2, ncomp=u.shape[0]).tolist()
+    return q[4] / (2.0 * float(grid.points) ** 2)
+
+
+def dissipation_rate(u_hat, f_hat, grid: Grid):
+    """eps = -sum_k w_k sum_{j<d} Re(u conj f) / points^2 (diagnostics.py:53-70)."""
+    u, _ = to_device(u_hat, torch.complex128)
+    f, _ = to_device(f_hat, torch.complex128)
+    if tuple(u.shape[1:]) != grid.kshape or tuple(f.shape) != tuple(u.shape):
+        raise ValueError(f"shape mismatch: fields {tuple(u.shape)}, tendency {tuple(f.shape)}, "
+                         f"grid modes {grid.kshape}")
+    q = reduce_sums(grid, u, fl=f, flags=2, ncomp=min(u.shape[0], grid.dims)).tolist()
+    return -q[5] / float(grid.points) ** 2
+
+
+def enstrophy(u_hat, grid: Grid):
+    """Z = sum_k w_k |k|^2 sum_{j<d} |u_kj|^2 / (2 points^2)."""
+    u, _ = to_device(u_hat, torch.complex128)
+    q = reduce_sums(grid, u, flags=2, ncomp=min(u.shape[0], grid.dims)).tolist()
+    return q[8] / (2.0 * float(grid.points) ** 2)

@@ -1,0 +1,143 @@
+"""Device Navier-Stokes / Boussinesq tendencies (mirrors physics.py of the reference).
+
+``FlowRHS(grid, params, density)`` is the drop-in operator: ``f(t, fields)``
+evaluates physics.py:105-129 (ns_rhs) or :132-185 (boussinesq_rhs) with one
+srk_rhs call (6 sm_100a kernels in 3D, 4 in 2D).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native
+from .grid import Grid
+from .spectral import from_device, get_plan, to_device
+
+__all__ = ["ForcingError", "PhysParams", "FlowState", "FlowRHS", "ns_rhs", "boussinesq_rhs",
+           "leray_project", "apply_forcing", "forcing_band"]
+
+
+class ForcingError(RuntimeError):
+    """The forcing band cannot reach the requested target energy (physics.py:23)."""
+
+
+@dataclass
+class PhysParams:
+    reynolds: float
+    richardson: float = 1.0
+    prandtl: float = 1.0
+
+
+@dataclass
+class FlowState:
+    grid: Grid
+    fields: object
+
+    @property
+    def has_density(self):
+        return self.fields.shape[0] == self.grid.dims + 1
+
+    @property
+    def velocity(self):
+        return self.fields[: self.grid.dims]
+
+    @property
+    def density(self):
+        if not self.has_density:
+            raise ValueError("state carries no density component")
+        return self.fields[self.grid.dims]
+
+
+class FlowRHS:
+    """Callable ``f(t, fields)`` (physics.py:188-206); returns a fresh caller-owned array."""
+
+    def __init__(self, grid: Grid, params: PhysParams, density=False):
+        self.grid = grid
+        self.params = params
+        self.density = bool(density)
+        self.plan = get_plan(grid, density=self.density)
+        self.ncomp = grid.dims + (1 if self.density else 0)
+        self.calls = 0
+
+    def __call__(self, t, fields, out=None):
+        y, was_np = to_device(fields, torch.complex128)
+        want = (self.ncomp,) + self.grid.kshape
+        if tuple(y.shape) != want:
+            raise ValueError(f"fields shape {tuple(y.shape)} != {want}")
+        f = out if out is not None else torch.empty_like(y)
+        p = self.params
+        pl = self.plan
+        _native.check(pl.lib.srk_rhs(pl.bind(), _native.ptr(y), _native.ptr(f), 1.0 / p.reynolds,
+                                     float(p.richardson), float(p.reynolds) * float(p.prandtl),
+                                     _native.stream_ptr()), "srk_rhs")
+        self.calls += 1
+        _native.count(pl.lib.srk_rhs_launch_count(pl.h))
+        return from_device(f, was_np)
+
+    def launches_per_call(self):
+        return int(self.plan.lib.srk_rhs_launch_count(self.plan.h))
+
+
+def ns_rhs(u_hat, grid: Grid, params: PhysParams, workspace=None):
+    return FlowRHS(grid, params)(0.0, u_hat)
+
+
+def boussinesq_rhs(fields, grid: Grid, params: PhysParams, workspace=None):
+    return FlowRHS(grid, params, density=True)(0.0, fields)
+
+
+def leray_project(u_hat, grid: Grid):
+    """u - k (k.u)/|k|^2, k=0 untouched (physics.py:89-102)."""
+    u, was_np = to_device(u_hat, torch.complex128)
+    out = torch.empty_like(u)
+    p = get_plan(grid)
+    _native.check(p.lib.srk_leray_project(p.h, _native.ptr(u), _native.ptr(out), _native.stream_ptr()))
+    return from_device(out, was_np)
+
+
+_BANDS = {}
+
+
+def forcing_band(grid: Grid, k_f, device):
+    """Flat indices + Hermitian weights of the modes 0 < |k|^2 <= k_f^2 (1+1e-12)."""
+    key = (grid.shape, grid.lengths, float(k_f), str(device))
+    if key not in _BANDS:
+        band = (grid.k2 > 0.0) & (grid.k2 <= k_f * k_f * (1.0 + 1e-12))
+        idx = np.flatnonzero(band.ravel()).astype(np.int64)
+        w = np.broadcast_to(grid.hermitian_weights, grid.kshape).ravel()[idx].astype(np.float64)
+        _BANDS[key] = (torch.from_numpy(idx).to(device), torch.from_numpy(np.ascontiguousarray(w)).to(device),
+                       len(idx))
+    return _BANDS[key]
+
+
+def apply_forcing(u_hat, grid: Grid, target_energy, k_f):
+    """Rescale 0<|k|<=k_f in place to restore ``target_energy`` (physics.py:209-239)."""
+    from .diagnostics import reduce_sums
+
+    u = u_hat
+    if not (isinstance(u, torch.Tensor) and u.is_cuda and u.is_contiguous()):
+        raise TypeError("apply_forcing works in place on a contiguous CUDA tensor")
+    idx, w, nb = forcing_band(grid, k_f, u.device)
+    p = get_plan(grid)
+    ncomp = u.shape[0]
+    pts2 = 2.0 * float(grid.points) ** 2
+    q = reduce_sums(grid, u, flags=2, ncomp=ncomp)
+    eb = torch.empty(1, dtype=torch.float64, device=u.device)
+    _native.check(p.lib.srk_band_energy(p.h, _native.ptr(u), ncomp, _native.ptr(idx), _native.ptr(w), nb,
+                                        _native.ptr(eb), _native.stream_ptr()))
+    e_total = q[4].item() / pts2
+    e_band = eb.item() / pts2
+    e_rest = e_total - e_band
+    if e_band <= 0.0:
+        raise ForcingError("forcing band carries no energy")
+    radicand = (target_energy - e_rest) / e_band
+    if radicand < 0.0:
+        raise ForcingError(f"energy outside the band ({e_rest:.6e}) exceeds target ({target_energy:.6e})")
+    gamma = float(np.sqrt(radicand))
+    _native.check(p.lib.srk_band_scale(p.h, _native.ptr(u), ncomp, _native.ptr(idx), nb, gamma,
+                                       _native.stream_ptr()))
+    _native.count(2)
+    return gamma

@@ -1,0 +1,307 @@
+"""Device-resident stepping loops (mirrors simulation.py:64-368 of the reference).
+
+Same bookkeeping as the reference driver: cached tendency f_now, FSAL reuse,
+evaluation accounting (RK4 4/step + 1, BS5 7/step + 1), lattice timestamps,
+final-step clamping with the working-h restore, forcing after every accepted
+step.  Additions: an initial-condition hook (``initial_state``) and an
+accepted-step cap (``max_steps``) -- SURVEY D4 / D6.  Per accepted step there
+is one device->host read (the fused error-norm + E/eps/Z sums).
+"""
+
+from __future__ import annotations
+
+import warnings
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .control import ControllerConfig, ControllerState, adaptive_advance
+from .diagnostics import DiagnosticsRecord, diag_from_sums, reduce_sums
+from .grid import Grid
+from .integrators import NonFiniteStateError, make_pair, make_rk4, run_stages
+from .physics import FlowRHS, FlowState, apply_forcing
+from .problems import ProblemSpec, hit_init, rayleigh_taylor_init, taylor_green_init
+from .spectral import to_device
+
+__all__ = ["RunConfig", "ConfigError", "default_lengths", "make_initial_state", "SimulationResult",
+           "run_simulation", "INTEGRATORS", "ADAPTIVE_CAPABLE"]
+
+INTEGRATORS = ("ab2", "rk4", "dp5", "kcl5", "bs5")
+ADAPTIVE_CAPABLE = ("dp5", "kcl5", "bs5")
+
+
+class ConfigError(ValueError):
+    """Invalid or inconsistent configuration (config.py:16)."""
+
+
+@dataclass
+class RunConfig:
+    """Same fields as the reference RunConfig (config.py:55-117)."""
+
+    grid_shape: tuple
+    problem: ProblemSpec
+    integrator: str
+    mode: str
+    t_end: float
+    lengths: tuple | None = None
+    h: float | None = None
+    tol_abs: float = 1e-6
+    tol_rel: float = 1e-6
+    h0: float = 1e-3
+    output_dir: str | None = None
+    checkpoint_interval: float | None = None
+    forcing: bool = False
+    k_f: float = 2.0
+    controller: ControllerConfig = field(default_factory=ControllerConfig)
+
+    def validate(self):
+        if self.integrator not in INTEGRATORS:
+            raise ConfigError(f"unknown integrator {self.integrator!r}")
+        if self.mode not in ("fixed", "adaptive"):
+            raise ConfigError(f"mode must be fixed or adaptive, got {self.mode!r}")
+        if self.mode == "adaptive" and self.integrator not in ADAPTIVE_CAPABLE:
+            raise ConfigError(f"integrator {self.integrator} has no embedded error estimate")
+        if self.mode == "fixed" and (self.h is None or self.h <= 0.0):
+            raise ConfigError("fixed mode requires a positive step size h")
+        if self.mode == "adaptive":
+            for name, tol in (("tol_abs", self.tol_abs), ("tol_rel", self.tol_rel)):
+                if tol <= 0.0:
+                    raise ConfigError(f"{name} must be positive, got {tol}")
+                if not 1e-10 <= tol <= 1e-2:
+                    warnings.warn(f"{name} = {tol:g} lies outside the tested range", stacklevel=2)
+            if self.h0 <= 0.0:
+                raise ConfigError("adaptive mode requires a positive initial step h0")
+        if self.t_end <= 0.0:
+            raise ConfigError(f"t_end must be positive, got {self.t_end}")
+        if self.problem.kind not in ("taylor_green", "rayleigh_taylor", "hit"):
+            raise ConfigError(f"unknown problem kind {self.problem.kind!r}")
+        if self.problem.kind == "hit" and self.problem.seed is None:
+            raise ConfigError("hit requires a seed")
+        if self.forcing and self.problem.kind != "hit":
+            raise ConfigError("forcing is only meaningful for the hit problem")
+        self.controller.tol_abs = self.tol_abs
+        self.controller.tol_rel = self.tol_rel
+        return self
+
+    @property
+    def has_density(self):
+        return self.problem.kind == "rayleigh_taylor"
+
+
+def default_lengths(kind, shape):
+    """config.py:142-152."""
+    if kind == "rayleigh_taylor":
+        base = 2.0 * np.pi
+        return tuple([base] * (len(shape) - 1) + [base * shape[-1] / shape[0]])
+    return (2.0 * np.pi,) * len(shape)
+
+
+def make_initial_state(config) -> FlowState:
+    """simulation.py:64-77."""
+    lengths = config.lengths if config.lengths is not None else default_lengths(config.problem.kind,
+                                                                                config.grid_shape)
+    grid = Grid(config.grid_shape, lengths)
+    kind = config.problem.kind
+    if kind == "taylor_green":
+        return taylor_green_init(grid)
+    if kind == "rayleigh_taylor":
+        return rayleigh_taylor_init(grid, config.problem)
+    return hit_init(grid, config.problem)
+
+
+@dataclass
+class SimulationResult:
+    records: list
+    state: FlowState
+    t: float
+    rhs_evals: int
+    rejections: int
+    steps: int
+    errs: list = field(default_factory=list)
+
+
+class _Driver:
+    """simulation.py:93-219 (device tensors; checkpointing out of scope)."""
+
+    def __init__(self, config, initial_state=None):
+        self.config = config
+        if initial_state is None:
+            st = make_initial_state(config)
+        elif callable(initial_state):
+            st = initial_state(config)
+        else:
+            st = initial_state
+        if isinstance(st, FlowState):
+            self.grid, y = st.grid, st.fields
+        else:
+            lengths = config.lengths or default_lengths(config.problem.kind, config.grid_shape)
+            self.grid, y = Grid(config.grid_shape, lengths), st
+        self.y = to_device(y, torch.complex128)[0].clone()
+        self.t = 0.0
+        self.evals = 0
+        self.rejections = 0
+        self.steps = 0
+        self.h_ctrl = config.h if config.mode == "fixed" else config.h0
+        self.prev_rejected = False
+        self.rhs = FlowRHS(self.grid, config.problem.params, density=config.has_density)
+        self.f_now = self.rhs(self.t, self.y)
+        self.evals += 1
+        self.records = []
+        self.errs = []
+        self._pending = None  # device sums for the next record
+
+    def record(self, h, sums=None):
+        d = self.grid.dims
+        if sums is None:
+            sums = reduce_sums(self.grid, self.y, fl=self.f_now, flags=2, ncomp=min(d, self.y.shape[0])).tolist()
+            if sums[6] > 0:
+                raise NonFiniteStateError(f"non-finite state at t={self.t}")
+        e, eps, z = diag_from_sums(sums, self.grid)
+        self.records.append(DiagnosticsRecord(t=self.t, h=h, e_kin=e, eps=eps, rhs_evals=self.evals,
+                                              rejections=self.rejections, enstrophy=z))
+
+    def after_accept(self, last_stage, fsal_ok):
+        """simulation.py:165-182. Returns True when f_now is the FSAL stage."""
+        cfg = self.config
+        forced = False
+        if cfg.forcing:
+            apply_forcing(self.y[: self.grid.dims], self.grid, cfg.problem.energy, cfg.k_f)
+            forced = True
+        self.steps += 1
+        if fsal_ok and not forced and last_stage is not None:
+            self.f_now = last_stage
+            return True
+        self.f_now = self.rhs(self.t, self.y)
+        self.evals += 1
+        return False
+
+    def result(self):
+        return SimulationResult(records=self.records, state=FlowState(grid=self.grid, fields=self.y), t=self.t,
+                                rhs_evals=self.evals, rejections=self.rejections, steps=self.steps, errs=self.errs)
+
+
+def _fixed_step_times(drv, h, t_end):
+    """simulation.py:222-247."""
+    t0 = drv.t
+    remaining = t_end - t0
+    n_full = int(np.floor(remaining / h + 1e-9))
+    h_last = remaining - n_full * h
+    if h_last < 1e-12 * h:
+        h_last = 0.0
+    base = drv.steps
+    on_lattice = abs(t0 - base * h) <= 1e-9 * max(1.0, abs(t0))
+
+    def time_at(i):
+        if i >= n_full:
+            return t_end
+        if on_lattice:
+            return (base + i + 1) * h
+        return t0 + (i + 1) * h
+
+    total = n_full + (1 if h_last > 0.0 else 0)
+    return total, n_full, h_last, time_at
+
+
+def _run_fixed(drv, max_steps=None):
+    """simulation.py:250-271 (RK pairs; AB2 bootstraps with RK4, :274-310)."""
+    cfg = drv.config
+    h, t_end = cfg.h, cfg.t_end
+    drv.record(h)
+    if cfg.integrator == "ab2":
+        return _run_ab2(drv, h, t_end, max_steps)
+    pair = make_pair(cfg.integrator)
+    total, n_full, h_last, time_at = _fixed_step_times(drv, h, t_end)
+    if max_steps is not None:
+        total = min(total, max_steps)
+    for i in range(total):
+        h_i = h if i < n_full else h_last
+        stages, y_new, ev = run_stages(drv.rhs, drv.y, drv.t, h_i, pair, drv.f_now)
+        drv.evals += ev
+        drv.y = y_new
+        drv.t = time_at(i)
+        drv.after_accept(stages[-1] if pair.fsal else None, fsal_ok=pair.fsal)
+        drv.record(h_i)
+
+
+def _run_ab2(drv, h, t_end, max_steps=None):
+    from .integrators import ab2_combine, combine
+
+    total, n_full, h_last, time_at = _fixed_step_times(drv, h, t_end)
+    if max_steps is not None:
+        total = min(total, max_steps)
+    if total == 0:
+        return
+    rk4 = make_rk4()
+    f_prev = drv.f_now
+    h0 = h if n_full > 0 else h_last
+    _, y_new, ev = run_stages(drv.rhs, drv.y, drv.t, h0, rk4, f_prev)
+    drv.evals += ev
+    drv.y = y_new
+    drv.t = time_at(0)
+    drv.after_accept(None, fsal_ok=False)
+    drv.record(h0)
+    for i in range(1, total):
+        h_i = h if i < n_full else h_last
+        if h_i != h:
+            _, y_new, ev = run_stages(drv.rhs, drv.y, drv.t, h_i, rk4, drv.f_now)
+            drv.evals += ev
+            drv.y = y_new
+        else:
+            drv.y = combine(drv.y, [(h * 1.5, drv.f_now), (-h * 0.5, f_prev)])
+        f_prev = drv.f_now
+        drv.t = time_at(i)
+        drv.after_accept(None, fsal_ok=False)
+        drv.record(h_i)
+
+
+def _run_adaptive(drv, max_steps=None):
+    """simulation.py:313-347 (+ accepted-step cap)."""
+    cfg = drv.config
+    pair = make_pair(cfg.integrator)
+    t_end = cfg.t_end
+    ctrl = ControllerState(h=drv.h_ctrl, prev_rejected=drv.prev_rejected, rejections=drv.rejections)
+    drv.record(drv.h_ctrl)
+    n = 0
+    while drv.t < t_end and (max_steps is None or n < max_steps):
+        remaining = t_end - drv.t
+        clamped = ctrl.h >= remaining
+        h_saved = ctrl.h
+        if clamped:
+            ctrl.h = remaining
+        out = adaptive_advance(drv.y, drv.t, pair, ctrl, cfg.controller, drv.rhs, first_stage=drv.f_now,
+                               grid=drv.grid)
+        drv.evals += out.rhs_evals
+        drv.rejections += out.rejections
+        drv.y = out.y_new
+        if clamped and out.rejections == 0:
+            drv.t = t_end
+            ctrl.h = h_saved
+        else:
+            drv.t = out.t_new
+            if clamped and out.t_new >= t_end - 1e-12 * t_end:
+                drv.t = t_end
+        drv.h_ctrl = ctrl.h
+        drv.prev_rejected = ctrl.prev_rejected
+        drv.errs.append(out.errs)
+        fsal_used = drv.after_accept(out.last_stage, fsal_ok=pair.fsal)
+        drv.record(out.h_used, sums=out.diag_sums if fsal_used else None)
+        n += 1
+
+
+def run_simulation(config, resume=None, initial_state=None, max_steps=None):
+    """simulation.py:350-368 on the device.
+
+    ``initial_state``: optional FlowState / array / callable(config) replacing
+    make_initial_state (IC hook).  ``max_steps``: accepted-step cap
+    (SURVEY D6).  Checkpoint/resume and CSV output are out of scope this round.
+    """
+    if resume is not None:
+        raise NotImplementedError("checkpoint resume is not part of the device path yet")
+    config.validate()
+    drv = _Driver(config, initial_state)
+    if config.mode == "fixed":
+        _run_fixed(drv, max_steps)
+    else:
+        _run_adaptive(drv, max_steps)
+    return drv.result()

@@ -1,0 +1,299 @@
+"""CUDA path vs the oracle / reference goldens (needs a B200).
+
+Tolerances (north_star): single evaluations <= 1e-12 relative L2 (observed
+~1e-15); trajectories: fields <= 1e-10 relative L2, step sizes / E / eps / Z
+histories <= 1e-9 relative.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+srk = pytest.importorskip("paper_1810_10197_b200")
+
+
+def rel(a, b):
+    a = a.cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a)
+    b = b.cpu().numpy() if isinstance(b, torch.Tensor) else np.asarray(b)
+    return float(np.linalg.norm((a - b).ravel()) / max(np.linalg.norm(b.ravel()), 1e-300))
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+RHS = load_golden("rhs_cases")
+
+
+@pytest.mark.parametrize("case", sorted(RHS))
+def test_rhs_matches_reference_golden(case):
+    c = RHS[case]
+    g = srk.Grid(tuple(c["shape"]), tuple(c["lengths"]))
+    p = srk.PhysParams(float(c["re"]), float(c["ri"]), float(c["pr"]))
+    f = srk.FlowRHS(g, p, density=bool(c["density"]))(0.0, dev(c["y"]))
+    assert rel(f, c["f"]) <= 1e-12
+
+
+def test_rhs_numpy_in_numpy_out():
+    c = RHS["hit16_s1"]
+    g = srk.Grid(tuple(c["shape"]))
+    f = srk.FlowRHS(g, srk.PhysParams(1000.0))(0.0, c["y"])
+    assert isinstance(f, np.ndarray) and rel(f, c["f"]) <= 1e-12
+
+
+DEAL = load_golden("dealias_cases")
+
+
+@pytest.mark.parametrize("case", sorted(DEAL))
+def test_widen_narrow_match_reference_golden(case):
+    c = DEAL[case]
+    g = srk.Grid(tuple(c["shape"]))
+    ws = srk.DealiasWorkspace(g, c["spec"].shape[0])
+    assert rel(ws.widen(dev(c["spec"])), c["phys"]) <= 1e-13
+    assert rel(ws.narrow(dev(c["pin"])), c["narrow"]) <= 1e-13
+
+
+@pytest.mark.parametrize("shape", [(32, 32, 32), (64, 64, 64), (16, 32, 48), (64, 256), (128, 128, 128)])
+def test_rhs_fast_plans_vs_oracle(shape):
+    """Sizes that run the compile-time FFT plans (M = 48, 96, 192, 384)."""
+    og = O.OGrid(shape)
+    y = O.hit(og, a=4.0, energy=0.5, seed=11) if len(shape) == 3 else O.taylor_green(og)
+    if len(shape) == 2:
+        rng = np.random.default_rng(2)
+        y = y + 1e-3 * O.fwd(rng.standard_normal((2,) + shape), og)
+    f_ref = O.OracleRHS(og, 700.0)(0.0, y)
+    f = srk.FlowRHS(srk.Grid(shape), srk.PhysParams(700.0))(0.0, dev(y))
+    assert rel(f, f_ref) <= 1e-12
+
+
+def test_rhs_nonhermitian_nyquist_fast_plan():
+    """Random non-Hermitian input incl. all Nyquist planes at a fast-plan size."""
+    shape = (32, 32, 64)
+    og = O.OGrid(shape)
+    rng = np.random.default_rng(5)
+    y = rng.standard_normal((3,) + og.kshape) + 1j * rng.standard_normal((3,) + og.kshape)
+    f_ref = O.OracleRHS(og, 90.0)(0.0, y)
+    f = srk.FlowRHS(srk.Grid(shape), srk.PhysParams(90.0))(0.0, dev(y))
+    assert rel(f, f_ref) <= 1e-12
+
+
+def test_boussinesq_2d_1024():
+    """Config-4 geometry (2D 1024^2, M = 1536) with the tanh interface IC."""
+    shape = (1024, 1024)
+    og = O.OGrid(shape)
+    y = O.rt_tanh_ic(og, seed=4)
+    f_ref = O.OracleRHS(og, 1e4, ri=1.0, pr=1.0, density=True)(0.0, y)
+    f = srk.FlowRHS(srk.Grid(shape), srk.PhysParams(1e4, 1.0, 1.0), density=True)(0.0, dev(y))
+    assert rel(f, f_ref) <= 1e-12
+
+
+@pytest.mark.parametrize("shape", [(16, 12), (8, 10, 6), (32, 32, 32), (64, 128), (64, 64, 64)])
+def test_transforms_vs_scipy(shape, rng):
+    g = srk.Grid(shape)
+    og = O.OGrid(shape)
+    u = rng.standard_normal((2,) + shape)
+    spec = srk.forward_transform(dev(u), g)
+    assert rel(spec, O.fwd(u, og)) <= 1e-13
+    back = srk.inverse_transform(spec, g)
+    assert rel(back, u) <= 1e-13
+
+
+def test_curl_and_leray_vs_oracle(rng):
+    og = O.OGrid((16, 16, 16))
+    g = srk.Grid((16, 16, 16))
+    u = rng.standard_normal((3,) + og.kshape) + 1j * rng.standard_normal((3,) + og.kshape)
+    assert rel(srk.curl(dev(u), g), O.curl(u, og)) <= 1e-15
+    assert rel(srk.leray_project(dev(u), g), O.leray(u, og)) <= 1e-15
+
+
+def _brute_force_conv(a_hat, b_hat, og):
+    """Alias-free direct convolution (reference tests/helpers.py:62-87 method)."""
+    from scipy.signal import fftconvolve
+
+    def centered(spec):
+        full = np.fft.fftn(np.fft.irfftn(spec, s=og.shape, axes=range(-og.dims, 0))) / og.points
+        half = [n // 2 for n in og.shape]
+        return full[np.ix_(*[np.arange(-(h - 1), h) % n for h, n in zip(half, og.shape)])]
+
+    conv = fftconvolve(centered(a_hat), centered(b_hat), mode="full")
+    half = [n // 2 for n in og.shape]
+    keep = tuple(slice((h - 1) * 2 - (h - 1), (h - 1) * 2 + h) for h in half)
+    out = np.zeros(og.shape, dtype=complex)
+    out[np.ix_(*[np.arange(-(h - 1), h) % n for h, n in zip(half, og.shape)])] = conv[keep] * og.points
+    return out[..., : og.shape[-1] // 2 + 1]
+
+
+def _band(og, rng):
+    spec = rng.standard_normal(og.kshape) + 1j * rng.standard_normal(og.kshape)
+    spec = spec[None]
+    O.symmetrize_planes(spec, og)
+    O.zero_nyquist(spec, og)
+    return np.fft.rfftn(np.fft.irfftn(spec, s=og.shape, axes=range(-og.dims, 0)), axes=range(-og.dims, 0))[0]
+
+
+@pytest.mark.parametrize("shape", [(12, 12), (16, 16), (8, 12), (8, 8, 8), (8, 6, 4), (32, 32, 32)])
+def test_dealiased_product_vs_brute_force(shape, rng):
+    """test_spectral.py:191-201 / test_acceptance.py:253-262 on the device path."""
+    og = O.OGrid(shape)
+    g = srk.Grid(shape)
+    for _ in range(2):
+        a, b = _band(og, rng), _band(og, rng)
+        prod = srk.dealiased_product(lambda f: (f[0] * f[1])[None], [dev(a[None]), dev(b[None])], g)[0]
+        ref = _brute_force_conv(a, b, og)
+        w = og.w
+        num = np.sum(np.abs(prod.cpu().numpy() - ref) ** 2 * w)
+        den = np.sum(np.abs(ref) ** 2 * w)
+        assert np.sqrt(num / den) < 1e-12
+
+
+def test_dealiased_output_nyquist_clean(rng):
+    og = O.OGrid((8, 8))
+    g = srk.Grid((8, 8))
+    a = _band(og, rng)
+    prod = srk.dealiased_product(lambda f: (f[0] * f[1])[None], [dev(a[None]), dev(a[None])], g)[0].cpu().numpy()
+    assert np.all(prod[4, :] == 0) and np.all(prod[:, 4] == 0) and prod[0, 0].imag == 0.0
+
+
+def test_combine_matches_numpy_bitwise(rng):
+    n = 4096
+    y = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    Fs = [rng.standard_normal(n) + 1j * rng.standard_normal(n) for _ in range(5)]
+    cs = [0.3, -1.7e-3, 2.5, 1e-9, -0.125]
+    ref = y.copy()
+    for c, F in zip(cs, Fs):
+        ref += c * F
+    from paper_1810_10197_b200.integrators import combine
+
+    out = combine(dev(y), [(c, dev(F)) for c, F in zip(cs, Fs)]).cpu().numpy()
+    assert np.array_equal(out, ref)
+
+
+def test_diagnostics_vs_oracle():
+    c = RHS["hit32_s42"]
+    og = O.OGrid((32, 32, 32))
+    g = srk.Grid((32, 32, 32))
+    y, f = dev(c["y"]), dev(c["f"])
+    assert abs(srk.kinetic_energy(y, g) - O.kinetic_energy(c["y"], og)) <= 1e-14 * O.kinetic_energy(c["y"], og)
+    e_ref = O.dissipation_rate(c["y"], c["f"], og)
+    assert abs(srk.dissipation_rate(y, f, g) - e_ref) <= 1e-13 * abs(e_ref)
+    z_ref = O.enstrophy(c["y"], og)
+    assert abs(srk.enstrophy(y, g) - z_ref) <= 1e-14 * z_ref
+
+
+def test_error_norm_fused_vs_oracle(rng):
+    og = O.OGrid((16, 16, 16))
+    g = srk.Grid((16, 16, 16))
+    f = O.OracleRHS(og, 300.0)
+    y = O.hit(og, a=4.0, energy=0.5, seed=9)
+    tab = O.tableau("bs5")
+    o = O.rk_step(f, y, 0.0, 2e-2, tab)
+    err_ref = O.error_norm_delta(o.err_vec, O.scale_vector(y, o.y_new, O.Ctrl()))
+    st = srk.ControllerState(h=2e-2)
+    out = srk.adaptive_advance(dev(y), 0.0, srk.make_bs5(), st, srk.ControllerConfig(),
+                               srk.FlowRHS(g, srk.PhysParams(300.0)), grid=g)
+    # Delta = h sum (b - b_hat) F cancels ~3 digits of the stages, so the
+    # 1e-15 stage differences show up amplified in err; the controller uses
+    # err**(-1/5), i.e. <= 1e-10 relative on h (north_star bar: 1e-9).
+    assert abs(out.errs[0] - err_ref) <= 1e-9 * err_ref
+    assert rel(out.y_new, o.y_new) <= 1e-13
+
+
+TRAJ = load_golden("trajectories")
+
+
+def _check_records(res, gold, tol=1e-9):
+    rec = np.array([[r.t, r.h, r.e_kin, r.eps, r.rhs_evals, r.rejections] for r in res.records])
+    assert rec.shape == gold["rec"].shape
+    assert np.array_equal(rec[:, 4:], gold["rec"][:, 4:])
+    np.testing.assert_allclose(rec[:, :4], gold["rec"][:, :4], rtol=tol, atol=0)
+
+
+def _cfg(shape, kind, re, integ, mode, t_end, h=None, tol=None, seed=None, a=9.5, energy=1.0, lengths=None):
+    spec = srk.ProblemSpec(kind=kind, params=srk.PhysParams(re), seed=seed, a=a, energy=energy)
+    c = srk.RunConfig(grid_shape=shape, problem=spec, integrator=integ, mode=mode, t_end=t_end, h=h,
+                      lengths=lengths)
+    if tol is not None:
+        c.tol_abs = c.tol_rel = tol
+    return c
+
+
+def test_c1_rk4_100_steps_vs_reference():
+    res = srk.run_simulation(_cfg((32, 32, 32), "taylor_green", 1600.0, "rk4", "fixed", 1.0, h=0.01))
+    _check_records(res, TRAJ["c1_rk4"])
+    assert rel(res.state.fields, TRAJ["c1_rk4"]["y"]) <= 1e-10
+
+
+def test_c1_bs5_adaptive_vs_reference():
+    res = srk.run_simulation(_cfg((32, 32, 32), "taylor_green", 1600.0, "bs5", "adaptive", 1.0, tol=1e-6))
+    _check_records(res, TRAJ["c1_bs5"])
+    assert rel(res.state.fields, TRAJ["c1_bs5"]["y"]) <= 1e-10
+    # enstrophy history vs the oracle restatement (D2)
+    og = O.OGrid((32, 32, 32))
+    _, recs, _ = O.run_adaptive(O.OracleRHS(og, 1600.0), O.taylor_green(og), og, O.tableau("bs5"), O.Ctrl(),
+                                1e-3, 1.0)
+    z = np.array([r.enstrophy for r in res.records])
+    z_ref = np.array([r.ens for r in recs])
+    np.testing.assert_allclose(z, z_ref, rtol=1e-9, atol=0)
+
+
+def test_bs5_rejections_vs_reference():
+    c = _cfg((16, 16, 16), "hit", 1000.0, "bs5", "adaptive", 0.2, tol=1e-6, seed=3, a=4.0, energy=0.5)
+    c.h0 = 0.5
+    res = srk.run_simulation(c)
+    assert res.rejections > 0
+    _check_records(res, TRAJ["hit16_bs5_rej"])
+    assert rel(res.state.fields, TRAJ["hit16_bs5_rej"]["y"]) <= 1e-10
+
+
+def test_forced_hit_vs_reference():
+    c = _cfg((16, 16, 16), "hit", 2000.0, "bs5", "adaptive", 0.05, tol=1e-6, seed=5, a=4.0, energy=0.5)
+    c.forcing = True
+    c.k_f = 2.0
+    res = srk.run_simulation(c)
+    _check_records(res, TRAJ["hit16_forced"])
+    assert rel(res.state.fields, TRAJ["hit16_forced"]["y"]) <= 1e-10
+
+
+def test_rt2d_rk4_vs_reference():
+    spec = srk.ProblemSpec(kind="rayleigh_taylor", params=srk.PhysParams(1600.0))
+    c = srk.RunConfig(grid_shape=(16, 64), problem=spec, integrator="rk4", mode="fixed", t_end=0.2, h=0.01,
+                      lengths=srk.default_lengths("rayleigh_taylor", (16, 64)))
+    res = srk.run_simulation(c)
+    _check_records(res, TRAJ["rt2d_rk4"])
+    assert rel(res.state.fields, TRAJ["rt2d_rk4"]["y"]) <= 1e-10
+
+
+def test_initial_conditions_vs_reference():
+    ic = load_golden("ics")
+    g = srk.Grid((16, 16, 16))
+    assert rel(srk.hit_init(g, srk.ProblemSpec("hit", a=4.0, energy=0.5, seed=42)).fields, ic["hit16_a4_s42"]) <= 1e-14
+    assert rel(srk.taylor_green_init(g).fields, ic["tg16"]) <= 1e-14
+    shape = (16, 64)
+    g2 = srk.Grid(shape, srk.default_lengths("rayleigh_taylor", shape))
+    assert rel(srk.rayleigh_taylor_init(g2, srk.ProblemSpec("rayleigh_taylor")).fields, ic["rt16x64"]) <= 1e-14
+
+
+def test_hit_256_one_rhs_vs_oracle():
+    """Config-3 geometry: one RHS at 256^3 (M = 384) against the oracle (~15 s CPU)."""
+    og = O.OGrid((256, 256, 256))
+    y = O.hit(og, a=4.0, energy=0.5, seed=42)
+    f_ref = O.OracleRHS(og, 1000.0)(0.0, y)
+    f = srk.FlowRHS(srk.Grid((256,) * 3), srk.PhysParams(1000.0))(0.0, dev(y))
+    assert rel(f, f_ref) <= 1e-12
+
+
+def test_nonfinite_state_is_rejected():
+    g = srk.Grid((16, 16, 16))
+    y = torch.zeros((3,) + g.kshape, dtype=torch.complex128, device="cuda")
+    y[0, 1, 1, 1] = float("nan")
+    st = srk.ControllerState(h=1e-2)
+    rhs = srk.FlowRHS(g, srk.PhysParams(100.0))
+    with pytest.raises(srk.StepSizeUnderflowError):
+        cfg = srk.ControllerConfig(h_min=1e-3)
+        srk.adaptive_advance(y, 0.0, srk.make_bs5(), st, cfg, rhs, grid=g)
+    assert st.rejections >= 1
