@@ -294,6 +294,12 @@ def test_nonfinite_state_is_rejected():
     st = srk.ControllerState(h=1e-2)
     rhs = srk.FlowRHS(g, srk.PhysParams(100.0))
     with pytest.raises(srk.StepSizeUnderflowError):
-        cfg = srk.ControllerConfig(h_min=1e-3)
-        srk.adaptive_advance(y, 0.0, srk.make_bs5(), st, cfg, rhs, grid=g)
-    assert st.rejections >= 1
+        srk.adaptive_advance(y, 0.0, srk.make_bs5(), st, srk.ControllerConfig(h_min=1e-7), rhs, grid=g)
+    # same tallies as the reference controller on the same NaN state
+    og = O.OGrid((16, 16, 16))
+    ost = O.CtrlState(h=1e-2)
+    with pytest.raises(O.Underflow):
+        with np.errstate(all="ignore"):
+            O.adaptive_advance(y.cpu().numpy(), 0.0, O.tableau("bs5"), ost, O.Ctrl(h_min=1e-7),
+                               O.OracleRHS(og, 100.0))
+    assert (st.rejections, st.prev_rejected, st.h) == (ost.rejections, ost.prev_rejected, ost.h) == (2, True, 1e-6)

@@ -1,0 +1,116 @@
+"""Host-side logic of the drop-in API vs the oracle restatement (CPU-only)."""
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1810_10197_b200 as srk
+from paper_1810_10197_b200.simulation import _fixed_step_times
+
+
+@pytest.mark.parametrize("name", ["rk4", "dp5", "bs5", "kcl5"])
+def test_tableaux_match_oracle(name):
+    a, b = srk.make_pair(name), O.tableau(name)
+    assert np.array_equal(a.A, b.A) and np.array_equal(a.b, b.b) and np.array_equal(a.c, b.c)
+    assert (a.b_hat is None) == (b.b_hat is None)
+    if a.b_hat is not None:
+        assert np.array_equal(a.b_hat, b.b_hat)
+    assert a.fsal == b.fsal
+
+
+def test_fsal_flags():
+    assert srk.make_bs5().fsal and srk.make_dp5().fsal
+    assert not srk.make_rk4().fsal and not srk.make_kcl5().fsal
+
+
+def test_bs5_stage_sparsity():
+    # non-zeros per A row [0,1,2,3,4,5,6,6]; b has 6; b - b_hat has 7
+    p = srk.make_bs5()
+    assert [int(np.count_nonzero(r)) for r in p.A] == [0, 1, 2, 3, 4, 5, 6, 6]
+    assert np.count_nonzero(p.b) == 6 and np.count_nonzero(p.b - p.b_hat) == 7
+
+
+@pytest.mark.parametrize("err", [0.0, 1e-12, 0.3, 0.999999, 1.0, 1.0000001, 7.0, 1e9, np.inf, np.nan])
+@pytest.mark.parametrize("prev", [False, True])
+def test_propose_step_matches_oracle(err, prev):
+    s1 = srk.ControllerState(h=0.2, prev_rejected=prev)
+    s2 = O.CtrlState(h=0.2, prev_rejected=prev)
+    assert srk.propose_step(err, s1, srk.ControllerConfig()) == O.propose_step(err, s2, O.Ctrl())
+    assert (s1.prev_rejected, s1.rejections, s1.acceptances) == (s2.prev_rejected, s2.rejections, s2.acceptances)
+
+
+def test_propose_step_underflow():
+    st = srk.ControllerState(h=1e-3)
+    with pytest.raises(srk.StepSizeUnderflowError):
+        srk.propose_step(np.inf, st, srk.ControllerConfig(h_min=1e-4))
+
+
+def test_controller_exact_values():
+    # test_acceptance.py:174-195 style: err=0.5 -> 0.8 * 0.5**-0.2; err=32 -> shrink 0.4
+    st = srk.ControllerState(h=0.2)
+    h, ok = srk.propose_step(0.5, st, srk.ControllerConfig())
+    assert ok and h == 0.2 * min(2.0, 0.8 * 0.5 ** (-0.2))
+    st = srk.ControllerState(h=0.2)
+    h, ok = srk.propose_step(32.0, st, srk.ControllerConfig())
+    assert not ok and h == 0.2 * 0.4
+
+
+@pytest.mark.parametrize("shape,lengths", [((8, 6, 4), None), ((16, 64), (2 * np.pi, 8 * np.pi)),
+                                           ((12, 10, 8), (1.0, 2.0, 3.0))])
+def test_grid_geometry_matches_oracle(shape, lengths):
+    g, og = srk.Grid(shape, lengths), O.OGrid(shape, lengths)
+    assert g.kshape == og.kshape and g.mode_count == og.mode_count and g.points == og.points
+    assert g.padded_shape == og.pshape
+    for a, b in zip(g.k, og.k):
+        assert np.array_equal(a, b)
+    assert np.array_equal(g.k2, og.k2) and np.array_equal(g.inv_k2, og.inv_k2)
+    assert np.array_equal(np.broadcast_to(g.hermitian_weights, g.kshape), np.broadcast_to(og.w, og.kshape))
+
+
+@pytest.mark.parametrize("bad", [(7, 8, 8), (2, 8), (8,), (8, 8, 8, 8)])
+def test_grid_rejects_bad_shapes(bad):
+    with pytest.raises(ValueError):
+        srk.Grid(bad)
+
+
+def _cfg(**kw):
+    base = dict(grid_shape=(16, 16), problem=srk.ProblemSpec("taylor_green"), integrator="rk4", mode="fixed",
+                t_end=1.0, h=0.1)
+    base.update(kw)
+    return srk.RunConfig(**base)
+
+
+@pytest.mark.parametrize("kw", [dict(integrator="euler"), dict(mode="sometimes"), dict(mode="adaptive"),
+                                dict(h=None), dict(t_end=0.0),
+                                dict(problem=srk.ProblemSpec("hit")),
+                                dict(forcing=True)])
+def test_config_validation(kw):
+    with pytest.raises(srk.ConfigError):
+        _cfg(**kw).validate()
+
+
+class _D:
+    def __init__(self, t, steps):
+        self.t, self.steps = t, steps
+
+
+def test_fixed_step_times_lattice_and_tail():
+    total, n_full, h_last, time_at = _fixed_step_times(_D(0.0, 0), 0.3, 1.0)
+    assert (total, n_full) == (4, 3) and abs(h_last - 0.1) < 1e-12
+    assert [time_at(i) for i in range(4)] == [0.3, 0.6, 0.8999999999999999, 1.0]
+    total, n_full, h_last, time_at = _fixed_step_times(_D(0.0, 0), 0.1, 1.0)
+    assert total == 10 and h_last == 0.0 and [time_at(i) for i in range(10)] == [(i + 1) * 0.1 for i in range(10)]
+
+
+def test_default_lengths():
+    assert srk.default_lengths("rayleigh_taylor", (16, 64))[1] == 2 * np.pi * 4
+    assert srk.default_lengths("hit", (8, 8, 8)) == (2 * np.pi,) * 3
+
+
+def test_compute_without_cuda_fails_loudly():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    with pytest.raises(RuntimeError, match="CUDA"):
+        srk.FlowRHS(srk.Grid((8, 8, 8)), srk.PhysParams(10.0))
