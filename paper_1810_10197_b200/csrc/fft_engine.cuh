@@ -33,8 +33,20 @@
 template <int M_, int C_>
 struct RowTile {
   static constexpr int M = M_, C = C_;
-  static constexpr int SIZE = M_ * C_;  // in cplx
-  SRK_DEV static int idx(int row, int col) { return row * C_ + col; }
+  // C >= 8: a row spans all 32 banks -> conflict free as is.
+  // C == 4: a row is half a bank cycle; one pad row after every 8 rows puts
+  // rows 8j+q and 8(j+1)+q in opposite halves, so the stride-R stores of the
+  // first Stockham stage and the consecutive-row accesses of later stages
+  // both split 4/4 over the halves (conflict free).
+  static constexpr int SIZE = (C_ >= 8) ? M_ * C_ : (M_ + M_ / 8 + 1) * C_;  // in cplx
+  __device__ __forceinline__ static int idx(int row, int col) {
+    if constexpr (C_ >= 8) {
+      return row * C_ + col;
+    } else {
+      static_assert(C_ == 4, "RowTile supports C = 4 or C >= 8");
+      return (row + (row >> 3)) * 4 + col;
+    }
+  }
   SRK_DEV static int col_of(int tid, int) { return tid % C_; }
   SRK_DEV static int tj_of(int tid, int) { return tid / C_; }
 };
@@ -44,7 +56,7 @@ struct ColTile {
   static constexpr int M = M_, C = C_;
   static constexpr int PITCH = M_ + (M_ + 7) / 8 + 1;
   static constexpr int SIZE = PITCH * C_;
-  SRK_DEV static int idx(int row, int col) { return col * PITCH + row + (row >> 3); }
+  __device__ __forceinline__ static int idx(int row, int col) { return col * PITCH + row + (row >> 3); }
   SRK_DEV static int col_of(int tid, int tpc) { return tid / tpc; }
   SRK_DEV static int tj_of(int tid, int tpc) { return tid % tpc; }
 };
@@ -88,19 +100,19 @@ struct FastStage {
     if (act) {
 #pragma unroll
       for (int b = 0; b < NB; ++b) {
-        const int j = tj + b * TPC;
-        const int k = j % Ls;
+        const unsigned j = (unsigned)tj + (unsigned)(b * TPC);
+        const unsigned k = j % (unsigned)Ls;
         if constexpr (Ls > 1) {
           constexpr int TS = M / (Ls * R);
 #pragma unroll
           for (int t = 1; t < R; ++t) {
-            cplx w = __ldg(&tw[t * k * TS]);
+            cplx w = __ldg(&tw[(unsigned)t * k * (unsigned)TS]);
             if (SIGN > 0) w.y = -w.y;
             v[b][t] = cmul(v[b][t], w);
           }
         }
         DFT<R, SIGN>::run(v[b]);
-        const int base = (j - k) * R + k;
+        const int base = (int)((j - k) * (unsigned)R + k);
 #pragma unroll
         for (int q = 0; q < R; ++q) {
           const int row = base + q * Ls;
@@ -134,6 +146,7 @@ struct FastFFT {
     const int col = L::col_of(tid, TPC);
     const int tj = L::tj_of(tid, TPC);
     const bool act = (tid < NT) && (col < ncols);
+    __builtin_assume(tj >= 0 && tj < TPC);
     FastStage<M_, E_, L, SIGN, LD_SMEM, ST_SMEM, 1, Rs...>::go(sm, tw, col, tj, act, ld, st);
   }
 };

@@ -16,10 +16,10 @@ void srk_reg_generic(KEntry* t) {
   using E3 = GenericFFT<Z3>;
   using E6 = GenericFFT<Z6>;
   using E7 = GenericFFT<Z7>;
-  t[KK_Z_C2R] = SRK_ENTRY((k_zpass<E4, Z4, ZOP_C2R>), E4, Z4::SIZE * 16);
+  t[KK_Z_C2R] = SRK_ENTRY((k_zpass<E4, Z4, ZOP_C2R>), E4, Z4::SIZE * 16 + SRK_GEN_STG(4));
   t[KK_Z_R2C] = SRK_ENTRY((k_zpass<E4, Z4, ZOP_R2C>), E4, Z4::SIZE * 16);
-  t[KK_Z_NS3] = SRK_ENTRY((k_zpass<E6, Z6, ZOP_NS3>), E6, Z6::SIZE * 16);
-  t[KK_Z_NS2] = SRK_ENTRY((k_zpass<E3, Z3, ZOP_NS2>), E3, Z3::SIZE * 16);
-  t[KK_Z_B3] = SRK_ENTRY((k_zpass<E7, Z7, ZOP_B3>), E7, Z7::SIZE * 16);
-  t[KK_Z_B2] = SRK_ENTRY((k_zpass<E4, Z4, ZOP_B2>), E4, Z4::SIZE * 16);
+  t[KK_Z_NS3] = SRK_ENTRY((k_zpass<E6, Z6, ZOP_NS3>), E6, Z6::SIZE * 16 + SRK_GEN_STG(6));
+  t[KK_Z_NS2] = SRK_ENTRY((k_zpass<E3, Z3, ZOP_NS2>), E3, Z3::SIZE * 16 + SRK_GEN_STG(3));
+  t[KK_Z_B3] = SRK_ENTRY((k_zpass<E7, Z7, ZOP_B3>), E7, Z7::SIZE * 16 + SRK_GEN_STG(7));
+  t[KK_Z_B2] = SRK_ENTRY((k_zpass<E4, Z4, ZOP_B2>), E4, Z4::SIZE * 16 + SRK_GEN_STG(4));
 }

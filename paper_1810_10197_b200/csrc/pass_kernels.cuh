@@ -49,8 +49,10 @@ struct PassArgs {
   long long comp_stride;  // between state components
 };
 
+// Loaders are branch-free (selects, clamped addresses) so the compiler can
+// issue all E loads of a thread back to back before the first use.
 template <class Eng, int KIND, int SIGN>
-__global__ void __launch_bounds__(Eng::NT) k_colpass(const PassArgs a) {
+__global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(const PassArgs a) {
   extern __shared__ __align__(16) cplx sm[];
   const int bid = blockIdx.x;
   int plane, wt;
@@ -63,17 +65,21 @@ __global__ void __launch_bounds__(Eng::NT) k_colpass(const PassArgs a) {
   }
   const int w0 = wt * Eng::C;
   const int ncols = min(Eng::C, a.Qp - w0);
-  const long long rs = a.row_stride;
+  const unsigned rs = (unsigned)a.row_stride;  // intra-plane offsets fit in 32 bits
   const cplx* __restrict__ inp = a.in + plane * a.in_plane_stride + w0;
   cplx* __restrict__ outp = a.out + plane * a.out_plane_stride + w0;
+  const int n = a.n, M = a.M;
 
   if constexpr (KIND == PK_INV) {
+    const double sc = a.scale;
     auto ld = [&](int row, int col) -> cplx {
-      const int cr = pad_src(row, a.n, a.M);
-      if (cr < 0) return cmk(0.0, 0.0);
-      return cscale(inp[cr * rs + col], a.scale);
+      const int cr = pad_src(row, n, M);
+      const bool ok = cr >= 0;
+      cplx v = inp[(unsigned)(ok ? cr : 0) * rs + (unsigned)col];
+      const double f = ok ? sc : 0.0;
+      return cmk(v.x * f, v.y * f);
     };
-    auto st = [&](int row, int col, cplx v) { outp[row * rs + col] = v; };
+    auto st = [&](int row, int col, cplx v) { outp[(unsigned)row * rs + (unsigned)col] = v; };
     Eng::template run<SIGN, false, false>(a.gp, sm, a.tw, ncols, ld, st);
   } else if constexpr (KIND == PK_INV_RHS) {
     // plane = signal s: [u_0..u_{d-1}, w (3 comps in 3D, 1 in 2D), rho]
@@ -81,64 +87,64 @@ __global__ void __launch_bounds__(Eng::NT) k_colpass(const PassArgs a) {
     const int wc = (d == 3) ? 3 : 1;
     const int s = plane;
     const cplx* __restrict__ base = a.in + w0;  // component 0
-    auto ld = [&](int row, int col) -> cplx {
-      const int cr = pad_src(row, a.n, a.M);
-      if (cr < 0) return cmk(0.0, 0.0);
-      const long long off = cr * rs + col;
-      cplx v;
-      if (s < d) {
-        v = base[s * a.comp_stride + off];
-      } else if (s < d + wc) {
-        // spectral.py:47-65: w = i k x u (k_a = mode_a * 2pi/L_a, grid.py:75-93)
-        const int q = w0 + col;
-        const double kx = mode_full(cr, a.n) * a.ck0;
-        if (d == 3) {
-          const int y = q / a.K, kzi = q - (q / a.K) * a.K;
-          const double ky = mode_full(y, a.n1) * a.ck1;
-          const double kz = (double)kzi * a.ck2;
-          cplx p, m;
-          if (s == 3) {  // i(ky u2 - kz u1)
-            cplx u2 = base[2 * a.comp_stride + off], u1 = base[1 * a.comp_stride + off];
-            p = cscale(u2, ky);
-            m = cscale(u1, kz);
-          } else if (s == 4) {  // i(kz u0 - kx u2)
-            cplx u0 = base[off], u2 = base[2 * a.comp_stride + off];
-            p = cscale(u0, kz);
-            m = cscale(u2, kx);
-          } else {  // i(kx u1 - ky u0)
-            cplx u1 = base[1 * a.comp_stride + off], u0 = base[off];
-            p = cscale(u1, kx);
-            m = cscale(u0, ky);
-          }
-          cplx df = csub(p, m);
-          v = cmk(-df.y, df.x);
-        } else {
-          const double kz = (double)q * a.ck2;
-          cplx u1 = base[1 * a.comp_stride + off], u0 = base[off];
-          cplx df = csub(cscale(u1, kx), cscale(u0, kz));
-          v = cmk(-df.y, df.x);
-        }
+    // per-thread column constants (the column of a thread never changes)
+    const int mycol = Eng::col_of(threadIdx.x);
+    const int q = w0 + mycol;
+    double ky = 0.0, kz = 0.0;
+    if (d == 3) {
+      const int y = q / a.K, kzi = q - y * a.K;
+      ky = mode_full(y, a.n1) * a.ck1;
+      kz = (double)kzi * a.ck2;
+    } else {
+      kz = (double)q * a.ck2;
+    }
+    // w = i (fa * u_ca - fb * u_cb), fa/fb = kx (row dependent) where flagged.
+    int ca = s, cb = s;
+    double sa = 1.0, sb = 0.0;
+    int kxa = 0, kxb = 0;
+    const bool is_curl = (s >= d && s < d + wc);
+    if (is_curl) {
+      if (d == 3) {
+        if (s == 3) { ca = 2; sa = ky; cb = 1; sb = kz; }
+        else if (s == 4) { ca = 0; sa = kz; cb = 2; kxb = 1; }
+        else { ca = 1; kxa = 1; cb = 0; sb = ky; }
       } else {
-        v = base[d * a.comp_stride + off];  // density
+        ca = 1; kxa = 1; cb = 0; sb = kz;
       }
-      return cscale(v, a.scale);
+    } else if (s == d + wc) {
+      ca = cb = d;  // density
+    }
+    const cplx* __restrict__ pa = base + ca * a.comp_stride;
+    const cplx* __restrict__ pb = base + cb * a.comp_stride;
+    const double sc = a.scale;
+    auto ld = [&](int row, int col) -> cplx {
+      const int cr = pad_src(row, n, M);
+      const bool ok = cr >= 0;
+      const unsigned off = (unsigned)(ok ? cr : 0) * rs + (unsigned)col;
+      const cplx ua = pa[off];
+      const cplx ub = pb[off];
+      // spectral.py:47-65: w = i k x u (k_a = mode_a * 2pi/L_a, grid.py:75-93)
+      const double kx = mode_full(ok ? cr : 0, n) * a.ck0;
+      const double fa = kxa ? kx : sa, fb = kxb ? kx : sb;
+      const cplx df = csub(cscale(ua, fa), cscale(ub, fb));
+      cplx v = is_curl ? cmk(-df.y, df.x) : ua;
+      const double f = ok ? sc : 0.0;
+      return cmk(v.x * f, v.y * f);
     };
-    auto st = [&](int row, int col, cplx v) { outp[row * rs + col] = v; };
+    auto st = [&](int row, int col, cplx v) { outp[(unsigned)row * rs + (unsigned)col] = v; };
     Eng::template run<SIGN, false, false>(a.gp, sm, a.tw, ncols, ld, st);
   } else {  // PK_FWD: forward C2C + truncation (+ scale, Nyquist / DC-imag zeroing)
     const bool zn = a.zero_nyq != 0;
     const bool zdc = (a.zero_dc_imag != 0) && (w0 == 0);
-    auto ld = [&](int row, int col) -> cplx { return inp[row * rs + col]; };
+    const double sc = a.scale;
+    auto ld = [&](int row, int col) -> cplx { return inp[(unsigned)row * rs + (unsigned)col]; };
     auto st = [&](int row, int col, cplx v) {
-      const int c = trunc_dst(row, a.n, a.M, zn);
+      const int c = trunc_dst(row, n, M, zn);
       if (c == -1) return;
-      if (c == -2) {
-        outp[(a.n >> 1) * rs + col] = cmk(0.0, 0.0);
-        return;
-      }
-      cplx o = cscale(v, a.scale);
+      cplx o = cmk(v.x * sc, v.y * sc);
+      if (c == -2) o = cmk(0.0, 0.0);
       if (zdc && c == 0 && col == 0) o.y = 0.0;
-      outp[c * rs + col] = o;
+      outp[(unsigned)(c == -2 ? (n >> 1) : c) * rs + (unsigned)col] = o;
     };
     Eng::template run<SIGN, false, false>(a.gp, sm, a.tw, ncols, ld, st);
   }
@@ -196,31 +202,62 @@ SRK_DEV void zphys(const double* r, double* o) {
 }
 
 template <class Eng, class L, int OP>
-__global__ void __launch_bounds__(Eng::NT) k_zpass(const ZArgs a, int S_rt, int So_rt) {
+__global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 224 ? 2 : 1)) k_zpass(const ZArgs a, int S_rt, int So_rt) {
   extern __shared__ __align__(16) cplx sm[];
   const int p0 = 2 * blockIdx.x;
   const int S = (OP >= ZOP_NS3) ? ZSig<OP>::S : S_rt;
   const int So = (OP >= ZOP_NS3) ? ZSig<OP>::So : So_rt;
   const int M = a.M, K = a.K;
-  // spectral value of real signal g (= pp*S + s) at padded mode k, Hermitian-extended
-  auto herm = [&](int g, int k) -> cplx {
-    const int pp = g / S, s = g - (g / S) * S;
-    const int pen = p0 + pp;
-    if (pen >= a.P) return cmk(0.0, 0.0);
-    const cplx* __restrict__ src = a.in + s * a.in_sig_stride + (long long)pen * K;
-    if (k < K) {
-      cplx X = src[k];
-      if (k == 0 || 2 * k == M) X.y = 0.0;  // irfft ignores Im of DC / Nyquist
-      return X;
-    }
-    if (k >= M - (K - 1)) return cconj(src[M - k]);
-    return cmk(0.0, 0.0);
-  };
-
   if constexpr (OP != ZOP_R2C) {
+    // ---- stage the 2*S input rows (K contiguous modes each) in smem.  Fast
+    // path: one elected thread issues 1D TMA bulk copies (cp.async.bulk) that
+    // complete on an mbarrier; the engine's tile aliases the staging area (its
+    // first stage loads everything before its first barrier-protected store).
+    cplx* stg = Eng::kFast ? sm : sm + L::SIZE;
+    __shared__ __align__(8) unsigned long long mbar;
+    const bool bulk = Eng::kFast && ((K * 16) % 16 == 0);
+    if (bulk) {
+      if (threadIdx.x == 0) {
+        mbar_init(&mbar, 1);
+        fence_mbar_init();
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        unsigned bytes = 0;
+        for (int g = 0; g < 2 * S; ++g) bytes += (p0 + g / S < a.P) ? (unsigned)(K * 16) : 0u;
+        mbar_expect_tx(&mbar, bytes);
+        for (int g = 0; g < 2 * S; ++g) {
+          const int pp = g / S, s = g - pp * S, pen = p0 + pp;
+          if (pen < a.P)
+            bulk_g2s(stg + g * K, a.in + s * a.in_sig_stride + (long long)pen * K, (unsigned)(K * 16), &mbar);
+        }
+      }
+      // rows of a missing second pencil (odd P) are zero
+      if (p0 + 1 >= a.P)
+        for (int i = threadIdx.x; i < S * K; i += blockDim.x) stg[S * K + i] = cmk(0.0, 0.0);
+      mbar_wait(&mbar, 0);
+      __syncthreads();
+    } else {
+      for (int g = 0; g < 2 * S; ++g) {
+        const int pp = g / S, s = g - pp * S, pen = p0 + pp;
+        const cplx* __restrict__ src = a.in + s * a.in_sig_stride + (long long)pen * K;
+        for (int k = threadIdx.x; k < K; k += blockDim.x) stg[g * K + k] = (pen < a.P) ? src[k] : cmk(0.0, 0.0);
+      }
+      __syncthreads();
+    }
+    // Hermitian extension of stored modes onto the padded z axis (branch free)
+    auto hs = [&](int g, int k) -> cplx {
+      const bool head = k < K;
+      const bool tail = k >= M - (K - 1);
+      const int kk = head ? k : (tail ? M - k : 0);
+      cplx X = stg[g * K + kk];
+      X.y = tail ? -X.y : X.y;
+      if (k == 0 || 2 * k == M) X.y = 0.0;  // irfft ignores Im of DC / Nyquist
+      return (head || tail) ? X : cmk(0.0, 0.0);
+    };
     // ---- inverse: S complex columns, column c carries real signals 2c, 2c+1 ----
     auto ld = [&](int k, int c) -> cplx {
-      cplx A = herm(2 * c, k), B = herm(2 * c + 1, k);
+      cplx A = hs(2 * c, k), B = hs(2 * c + 1, k);
       return cmk(A.x - B.y, A.y + B.x);
     };
     if constexpr (OP == ZOP_C2R) {
@@ -235,11 +272,11 @@ __global__ void __launch_bounds__(Eng::NT) k_zpass(const ZArgs a, int S_rt, int 
           if (pen < a.P) a.out_real[s * a.out_sig_stride + (long long)pen * M + n] = v.y;
         }
       };
-      Eng::template run<+1, false, false>(a.gp, sm, a.tw, S, ld, st);
+      Eng::template run<+1, true, false>(a.gp, sm, a.tw, S, ld, st);
       return;
     } else {
       auto st = [&](int n, int c, cplx v) { sm[L::idx(n, c)] = v; };
-      Eng::template run<+1, false, true>(a.gp, sm, a.tw, S, ld, st);
+      Eng::template run<+1, true, true>(a.gp, sm, a.tw, S, ld, st);
       __syncthreads();
       // ---- physical space: per row n, both pencils ----
       for (int n = threadIdx.x; n < M; n += blockDim.x) {

@@ -27,6 +27,8 @@ struct KEntry {
 
 // plain z ops process up to this many real signals per pencil per launch
 #define SRK_Z_PLAIN_C 4
+// generic z kernels stage their inputs after the tile: 2 * C * (MAXM/2+1) complex
+#define SRK_GEN_STG(C) (2 * (C) * (SRK_GEN_MAXM / 2 + 1) * 16)
 
 typedef void (*srk_reg_fn)(KEntry* tab);
 

