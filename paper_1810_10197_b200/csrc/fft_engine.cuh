@@ -39,6 +39,10 @@ struct RowTile {
   // first Stockham stage and the consecutive-row accesses of later stages
   // both split 4/4 over the halves (conflict free).
   static constexpr int SIZE = (C_ >= 8) ? M_ * C_ : (M_ + M_ / 8 + 1) * C_;  // in cplx
+  // idx(row + 8m) = idx(row) + m*STEP8; within an aligned group of 8 rows
+  // idx(row + 1) = idx(row) + ROWSTEP  (lets the stages hoist index math)
+  static constexpr int STEP8 = (C_ >= 8) ? 8 * C_ : 36;
+  static constexpr int ROWSTEP = (C_ >= 8) ? C_ : 4;
   __device__ __forceinline__ static int idx(int row, int col) {
     if constexpr (C_ >= 8) {
       return row * C_ + col;
@@ -56,6 +60,8 @@ struct ColTile {
   static constexpr int M = M_, C = C_;
   static constexpr int PITCH = M_ + (M_ + 7) / 8 + 1;
   static constexpr int SIZE = PITCH * C_;
+  static constexpr int STEP8 = 9;
+  static constexpr int ROWSTEP = 1;
   __device__ __forceinline__ static int idx(int row, int col) { return col * PITCH + row + (row >> 3); }
   SRK_DEV static int col_of(int tid, int tpc) { return tid / tpc; }
   SRK_DEV static int tj_of(int tid, int tpc) { return tid % tpc; }
@@ -86,13 +92,16 @@ struct FastStage {
 #pragma unroll
       for (int b = 0; b < NB; ++b) {
         const int j = tj + b * TPC;
+        if constexpr (FIRST) {
 #pragma unroll
-        for (int t = 0; t < R; ++t) {
-          const int row = j + t * STRIDE;
-          if constexpr (FIRST)
-            v[b][t] = ld(row, col);
-          else
-            v[b][t] = sm[L::idx(row, col)];
+          for (int t = 0; t < R; ++t) v[b][t] = ld(j + t * STRIDE, col);
+        } else if constexpr (STRIDE % 8 == 0) {
+          const int a0 = L::idx(j, col);
+#pragma unroll
+          for (int t = 0; t < R; ++t) v[b][t] = sm[a0 + t * (STRIDE / 8) * L::STEP8];
+        } else {
+#pragma unroll
+          for (int t = 0; t < R; ++t) v[b][t] = sm[L::idx(j + t * STRIDE, col)];
         }
       }
     }
@@ -104,22 +113,30 @@ struct FastStage {
         const unsigned k = j % (unsigned)Ls;
         if constexpr (Ls > 1) {
           constexpr int TS = M / (Ls * R);
+          const unsigned kts = k * (unsigned)TS;
 #pragma unroll
           for (int t = 1; t < R; ++t) {
-            cplx w = __ldg(&tw[(unsigned)t * k * (unsigned)TS]);
+            cplx w = __ldg(&tw[(unsigned)t * kts]);
             if (SIGN > 0) w.y = -w.y;
             v[b][t] = cmul(v[b][t], w);
           }
         }
         DFT<R, SIGN>::run(v[b]);
         const int base = (int)((j - k) * (unsigned)R + k);
+        if constexpr (LAST) {
 #pragma unroll
-        for (int q = 0; q < R; ++q) {
-          const int row = base + q * Ls;
-          if constexpr (LAST)
-            st(row, col, v[b][q]);
-          else
-            sm[L::idx(row, col)] = v[b][q];
+          for (int q = 0; q < R; ++q) st(base + q * Ls, col, v[b][q]);
+        } else if constexpr (Ls % 8 == 0) {
+          const int a0 = L::idx(base, col);
+#pragma unroll
+          for (int q = 0; q < R; ++q) sm[a0 + q * (Ls / 8) * L::STEP8] = v[b][q];
+        } else if constexpr (Ls == 1 && (8 % R == 0)) {
+          const int a0 = L::idx(base, col);  // base = j*R: the R rows share one 8-row group
+#pragma unroll
+          for (int q = 0; q < R; ++q) sm[a0 + q * L::ROWSTEP] = v[b][q];
+        } else {
+#pragma unroll
+          for (int q = 0; q < R; ++q) sm[L::idx(base + q * Ls, col)] = v[b][q];
         }
       }
     }
@@ -174,6 +191,7 @@ __device__ __forceinline__ void gen_dft(int R, cplx* v) {
 template <class L>
 struct GenericFFT {
   static constexpr bool kFast = false;
+  static constexpr int M = 0;  // runtime
   static constexpr int C = L::C;
   static constexpr int NT = L::C;
   SRK_DEV static int col_of(int tid) { return tid; }

@@ -1,3 +1,3 @@
 // Fast compile-time FFT plan instantiations (see registry.cuh).
 #include "registry.cuh"
-SRK_DEFINE_SIZE(srk_reg_384, 384, 24, 8, 8, 8, 6)
+SRK_DEFINE_SIZE_F(srk_reg_384, 384, 24, 8, 12, (4, 4, 4, 6), 8, 8, 6)

@@ -1,3 +1,3 @@
 // Fast compile-time FFT plan instantiations (see registry.cuh).
 #include "registry.cuh"
-SRK_DEFINE_SIZE(srk_reg_96, 96, 24, 32, 8, 4, 3)
+SRK_DEFINE_SIZE_F(srk_reg_96, 96, 24, 32, 12, (4, 4, 6), 8, 4, 3)

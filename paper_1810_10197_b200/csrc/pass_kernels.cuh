@@ -49,11 +49,26 @@ struct PassArgs {
   long long comp_stride;  // between state components
 };
 
-// Loaders are branch-free (selects, clamped addresses) so the compiler can
-// issue all E loads of a thread back to back before the first use.
+// Fast path: the input rows of the tile are first copied to shared memory with
+// cp.async (16 B per request, no register staging, all requests in flight at
+// once); the engine's first stage then reads them from smem.  The staging
+// area aliases the FFT tile (the first stage loads everything before its
+// first barrier-protected store).  Loaders are branch-free (selects, clamped
+// addresses).  Generic path: loaders read global memory directly.
+template <int C>
+__device__ __forceinline__ void stage_rows(cplx* dst, const cplx* __restrict__ src, int rows, unsigned rs,
+                                           int ncols) {
+  const int tot = rows * C;
+  for (int i = threadIdx.x; i < tot; i += blockDim.x) {
+    const int r = i / C, c = i - (i / C) * C;
+    if (c < ncols) cp_async16(dst + i, src + (unsigned)r * rs + (unsigned)c);
+  }
+}
+
 template <class Eng, int KIND, int SIGN>
 __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(const PassArgs a) {
   extern __shared__ __align__(16) cplx sm[];
+  constexpr int C = Eng::C;
   const int bid = blockIdx.x;
   int plane, wt;
   if (a.sig_minor) {
@@ -63,8 +78,8 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
     plane = bid / a.tpp;
     wt = bid % a.tpp;
   }
-  const int w0 = wt * Eng::C;
-  const int ncols = min(Eng::C, a.Qp - w0);
+  const int w0 = wt * C;
+  const int ncols = min(C, a.Qp - w0);
   const unsigned rs = (unsigned)a.row_stride;  // intra-plane offsets fit in 32 bits
   const cplx* __restrict__ inp = a.in + plane * a.in_plane_stride + w0;
   cplx* __restrict__ outp = a.out + plane * a.out_plane_stride + w0;
@@ -72,15 +87,21 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
 
   if constexpr (KIND == PK_INV) {
     const double sc = a.scale;
+    if constexpr (Eng::kFast) {
+      stage_rows<C>(sm, inp, n, rs, ncols);
+      cp_async_wait_all();
+      __syncthreads();
+    }
     auto ld = [&](int row, int col) -> cplx {
       const int cr = pad_src(row, n, M);
       const bool ok = cr >= 0;
-      cplx v = inp[(unsigned)(ok ? cr : 0) * rs + (unsigned)col];
+      const int r = ok ? cr : 0;
+      cplx v = Eng::kFast ? sm[r * C + col] : inp[(unsigned)r * rs + (unsigned)col];
       const double f = ok ? sc : 0.0;
       return cmk(v.x * f, v.y * f);
     };
     auto st = [&](int row, int col, cplx v) { outp[(unsigned)row * rs + (unsigned)col] = v; };
-    Eng::template run<SIGN, false, false>(a.gp, sm, a.tw, ncols, ld, st);
+    Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, a.tw, ncols, ld, st);
   } else if constexpr (KIND == PK_INV_RHS) {
     // plane = signal s: [u_0..u_{d-1}, w (3 comps in 3D, 1 in 2D), rho]
     const int d = a.dims;
@@ -117,14 +138,22 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
     const cplx* __restrict__ pa = base + ca * a.comp_stride;
     const cplx* __restrict__ pb = base + cb * a.comp_stride;
     const double sc = a.scale;
+    cplx* sb_ = sm + (is_curl ? n * C : 0);
+    if constexpr (Eng::kFast) {
+      stage_rows<C>(sm, pa, n, rs, ncols);
+      if (is_curl) stage_rows<C>(sm + n * C, pb, n, rs, ncols);
+      cp_async_wait_all();
+      __syncthreads();
+    }
     auto ld = [&](int row, int col) -> cplx {
       const int cr = pad_src(row, n, M);
       const bool ok = cr >= 0;
-      const unsigned off = (unsigned)(ok ? cr : 0) * rs + (unsigned)col;
-      const cplx ua = pa[off];
-      const cplx ub = pb[off];
+      const int r = ok ? cr : 0;
+      const unsigned off = (unsigned)r * rs + (unsigned)col;
+      const cplx ua = Eng::kFast ? sm[r * C + col] : pa[off];
+      const cplx ub = Eng::kFast ? sb_[r * C + col] : pb[off];
       // spectral.py:47-65: w = i k x u (k_a = mode_a * 2pi/L_a, grid.py:75-93)
-      const double kx = mode_full(ok ? cr : 0, n) * a.ck0;
+      const double kx = mode_full(r, n) * a.ck0;
       const double fa = kxa ? kx : sa, fb = kxb ? kx : sb;
       const cplx df = csub(cscale(ua, fa), cscale(ub, fb));
       cplx v = is_curl ? cmk(-df.y, df.x) : ua;
@@ -132,12 +161,19 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
       return cmk(v.x * f, v.y * f);
     };
     auto st = [&](int row, int col, cplx v) { outp[(unsigned)row * rs + (unsigned)col] = v; };
-    Eng::template run<SIGN, false, false>(a.gp, sm, a.tw, ncols, ld, st);
+    Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, a.tw, ncols, ld, st);
   } else {  // PK_FWD: forward C2C + truncation (+ scale, Nyquist / DC-imag zeroing)
     const bool zn = a.zero_nyq != 0;
     const bool zdc = (a.zero_dc_imag != 0) && (w0 == 0);
     const double sc = a.scale;
-    auto ld = [&](int row, int col) -> cplx { return inp[(unsigned)row * rs + (unsigned)col]; };
+    if constexpr (Eng::kFast) {
+      stage_rows<C>(sm, inp, M, rs, ncols);
+      cp_async_wait_all();
+      __syncthreads();
+    }
+    auto ld = [&](int row, int col) -> cplx {
+      return Eng::kFast ? sm[row * C + col] : inp[(unsigned)row * rs + (unsigned)col];
+    };
     auto st = [&](int row, int col, cplx v) {
       const int c = trunc_dst(row, n, M, zn);
       if (c == -1) return;
@@ -146,7 +182,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
       if (zdc && c == 0 && col == 0) o.y = 0.0;
       outp[(unsigned)(c == -2 ? (n >> 1) : c) * rs + (unsigned)col] = o;
     };
-    Eng::template run<SIGN, false, false>(a.gp, sm, a.tw, ncols, ld, st);
+    Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, a.tw, ncols, ld, st);
   }
 }
 
@@ -201,13 +237,20 @@ SRK_DEV void zphys(const double* r, double* o) {
   }
 }
 
-template <class Eng, class L, int OP>
+// Eng runs the inverse transforms (S complex columns); EngF the forward ones
+// (So columns) -- a different plan when So < S so all threads stay busy.
+template <class Eng, class L, int OP, class EngF = Eng>
 __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 224 ? 2 : 1)) k_zpass(const ZArgs a, int S_rt, int So_rt) {
   extern __shared__ __align__(16) cplx sm[];
   const int p0 = 2 * blockIdx.x;
   const int S = (OP >= ZOP_NS3) ? ZSig<OP>::S : S_rt;
   const int So = (OP >= ZOP_NS3) ? ZSig<OP>::So : So_rt;
-  const int M = a.M, K = a.K;
+  // physics ops always run on the 3/2-padded axis: M = 3n/2, K = n/2 + 1 = M/3 + 1,
+  // known at compile time for the fast plans (lets the compiler resolve the
+  // Hermitian / zero-band selects and prune dead outputs statically)
+  constexpr bool kCT = Eng::kFast && OP >= ZOP_NS3;
+  const int M = kCT ? Eng::M : a.M;
+  const int K = kCT ? Eng::M / 3 + 1 : a.K;
   if constexpr (OP != ZOP_R2C) {
     // ---- stage the 2*S input rows (K contiguous modes each) in smem.  Fast
     // path: one elected thread issues 1D TMA bulk copies (cp.async.bulk) that
@@ -312,16 +355,20 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 224 ? 2 : 1)) k_zpass(con
     Eng::template run<-1, false, true>(a.gp, sm, a.tw, So, ld, st);
   } else {
     auto ld = [&](int n, int c) -> cplx { return sm[L::idx(n, c)]; };
-    auto st = [&](int n, int c, cplx v) { sm[L::idx(n, c)] = v; };
-    Eng::template run<-1, true, true>(a.gp, sm, a.tw, So, ld, st);
+    // only rows [0, K-1) and (M-K+1, M) feed the kept modes (kz = n/2 is zeroed)
+    auto st = [&](int n, int c, cplx v) {
+      if (n < K - 1 || n > M - K + 1) sm[L::idx(n, c)] = v;
+    };
+    EngF::template run<-1, true, true>(a.gp, sm, a.tw, So, ld, st);
   }
   __syncthreads();
   // ---- extraction: two real spectra from each complex column, keep K modes ----
   const bool zn = a.zero_nyq != 0;
   for (int i = threadIdx.x; i < So * K; i += blockDim.x) {
     const int c = i / K, k = i - (i / K) * K;
-    const cplx Zk = sm[L::idx(k, c)];
-    const cplx Zm = sm[L::idx(k == 0 ? 0 : M - k, c)];
+    const bool live = !(zn && k == K - 1);
+    const cplx Zk = live ? sm[L::idx(k, c)] : cmk(0.0, 0.0);
+    const cplx Zm = live ? sm[L::idx(k == 0 ? 0 : M - k, c)] : cmk(0.0, 0.0);
     cplx A = cmk(0.5 * (Zk.x + Zm.x), 0.5 * (Zk.y - Zm.y));
     cplx B = cmk(0.5 * (Zk.y + Zm.y), -0.5 * (Zk.x - Zm.x));
     if (zn && k == K - 1) {

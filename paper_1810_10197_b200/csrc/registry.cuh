@@ -41,12 +41,17 @@ struct GenCols {
 #define SRK_ENTRY(KFN, ENG, SMB) KEntry{(const void*)(KFN), ENG::NT, ENG::C, (int)(SMB)}
 
 // Instantiate every kernel kind for one fast FFT length.
-#define SRK_DEFINE_SIZE(NAME, M, E, CS, ...)                                                       \
+#define SRK_DEFINE_SIZE(NAME, M, E, CS, ...) SRK_DEFINE_SIZE_F(NAME, M, E, CS, E, (__VA_ARGS__), __VA_ARGS__)
+#define SRK_UNPAREN(...) __VA_ARGS__
+// EF / FR: elements-per-thread and radices of the forward transform of the NS3
+// z-pass (3 forward columns vs 6 inverse ones: E = 12 keeps every thread busy).
+#define SRK_DEFINE_SIZE_F(NAME, M, E, CS, EF, FR, ...)                                             \
   void NAME(KEntry* t) {                                                                           \
     using SL = RowTile<M, CS>;                                                                     \
     using SE = FastFFT<M, E, SL, __VA_ARGS__>;                                                     \
     t[KK_INV] = SRK_ENTRY((k_colpass<SE, PK_INV, +1>), SE, SL::SIZE * 16);                         \
-    t[KK_INV_RHS] = SRK_ENTRY((k_colpass<SE, PK_INV_RHS, +1>), SE, SL::SIZE * 16);                 \
+    t[KK_INV_RHS] = SRK_ENTRY((k_colpass<SE, PK_INV_RHS, +1>), SE,                                 \
+                              (SL::SIZE > 2 * (2 * M / 3) * CS ? SL::SIZE : 2 * (2 * M / 3) * CS) * 16); \
     t[KK_FWD] = SRK_ENTRY((k_colpass<SE, PK_FWD, -1>), SE, SL::SIZE * 16);                         \
     using Z4 = ColTile<M, 4>;                                                                      \
     using Z3 = ColTile<M, 3>;                                                                      \
@@ -56,9 +61,10 @@ struct GenCols {
     using E3 = FastFFT<M, E, Z3, __VA_ARGS__>;                                                     \
     using E6 = FastFFT<M, E, Z6, __VA_ARGS__>;                                                     \
     using E7 = FastFFT<M, E, Z7, __VA_ARGS__>;                                                     \
+    using E6F = FastFFT<M, EF, Z6, SRK_UNPAREN FR>;                                                \
     t[KK_Z_C2R] = SRK_ENTRY((k_zpass<E4, Z4, ZOP_C2R>), E4, Z4::SIZE * 16);                        \
     t[KK_Z_R2C] = SRK_ENTRY((k_zpass<E4, Z4, ZOP_R2C>), E4, Z4::SIZE * 16);                        \
-    t[KK_Z_NS3] = SRK_ENTRY((k_zpass<E6, Z6, ZOP_NS3>), E6, Z6::SIZE * 16);                        \
+    t[KK_Z_NS3] = SRK_ENTRY((k_zpass<E6, Z6, ZOP_NS3, E6F>), E6, Z6::SIZE * 16);                   \
     t[KK_Z_NS2] = SRK_ENTRY((k_zpass<E3, Z3, ZOP_NS2>), E3, Z3::SIZE * 16);                        \
     t[KK_Z_B3] = SRK_ENTRY((k_zpass<E7, Z7, ZOP_B3>), E7, Z7::SIZE * 16);                          \
     t[KK_Z_B2] = SRK_ENTRY((k_zpass<E4, Z4, ZOP_B2>), E4, Z4::SIZE * 16);                          \

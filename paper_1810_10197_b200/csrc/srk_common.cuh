@@ -243,3 +243,11 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
       "r"(phase)
       : "memory");
 }
+
+// cp.async (16 B, L2-only caching) global -> shared
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
