@@ -9,7 +9,9 @@ invalidated by the forcing, simulation.py:165-182).  The metric is RK stages
 
     python bench.py                       # N=1, 512^3, K=10, W=3
     python bench.py --impl reference      # CPU oracle port (the reference's algorithm)
-    torchrun --nproc-per-node N bench.py --gpus N   # N independent replicas
+    torchrun --nproc-per-node N bench.py --gpus N   # y-slab decomposed N^3 over N GPUs (strong scaling)
+    python bench.py --mode slab --grid 256  # the slab path on one GPU (NCCL world of 1)
+    torchrun ... bench.py --mode replicas # N independent replicas (weak scaling)
 """
 
 from __future__ import annotations
@@ -37,9 +39,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--grid", dest="n", type=int, default=512, help="N of the N^3 grid")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--mode", default="auto", choices=["auto", "single", "slab", "replicas"],
+                    help="auto: single GPU at N=1, slab decomposition (strong scaling) for N>1")
     return ap.parse_args()
 
 
@@ -333,6 +337,121 @@ def run_native(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def run_slab(args, rank, world, local_rank):
+    """N^3 grid y-slab decomposed over all ranks; strong scaling."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1810_10197_b200 as srk
+    from paper_1810_10197_b200 import _native
+    from paper_1810_10197_b200.diagnostics import diag_from_sums, reduce_sums
+    from paper_1810_10197_b200.slab import SlabFlowRHS, dist_sum_in_rank_order, hit_slab, slab_geometry
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    n = args.n
+    g = srk.Grid((n, n, n))
+    params = srk.PhysParams(reynolds=2000.0)
+    energy, k_f = 0.5, 2.0
+    red = dist_sum_in_rank_order()
+    rhs = SlabFlowRHS(g, params, rank, world)
+    plan = rhs.backend.h
+    y0 = hit_slab(g, rank, world, a=4.0, energy=energy, seed=42, allreduce=red)
+    pair = srk.make_bs5()
+    cfg = srk.ControllerConfig(tol_abs=1e-6, tol_rel=1e-6)
+
+    def new_state():
+        y = y0.clone()
+        return dict(y=y, t=0.0, f=rhs(0.0, y), ctrl=srk.ControllerState(h=1e-3))
+
+    def step(s):
+        out = srk.adaptive_advance(s["y"], s["t"], pair, s["ctrl"], cfg, rhs, first_stage=s["f"], grid=g,
+                                   allreduce=red, plan=plan)
+        y = out.y_new
+        srk.apply_forcing(y, g, energy, k_f, plan=plan, allreduce=red, slab=(rank, world))
+        f = rhs(out.t_new, y)
+        q = red(reduce_sums(g, y, fl=f, flags=2, ncomp=3, plan=plan))
+        s.update(y=y, t=out.t_new, f=f)
+        return out.rhs_evals + 1, diag_from_sums(q, g)
+
+    s = new_state()
+    for _ in range(args.warmup):
+        step(s)
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evals = 0
+    l0 = _native.LAUNCHES
+    with ClockSampler(local_rank) as clk:
+        e0.record(st)
+        for _ in range(args.steps):
+            ev, _ = step(s)
+            evals += ev
+        e1.record(st)
+        torch.cuda.synchronize()
+    launches = _native.LAUNCHES - l0
+    dist.barrier()
+    t_sec = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device=dev)
+    dist.all_reduce(t_sec, op=dist.ReduceOp.MAX)
+    T = t_sec.item()
+    value = evals / T  # every rank works on the same global stages
+
+    # phase timing of one RHS: 3 kernel groups + 2 exchanges (max over ranks)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+    yk = s["y"]
+    fk = torch.empty_like(yk)
+    b = rhs.backend
+    ev[0].record(st)
+    b.forward(yk, rhs.send1)
+    ev[1].record(st)
+    rhs.exchange(rhs.recv1, rhs.send1)
+    ev[2].record(st)
+    b.middle(rhs.recv1, rhs.send2)
+    ev[3].record(st)
+    rhs.exchange(rhs.recv2, rhs.send2)
+    ev[4].record(st)
+    b.finish(rhs.recv2, yk, fk)
+    ev[5].record(st)
+    torch.cuda.synchronize()
+    ph = torch.tensor([ev[i].elapsed_time(ev[i + 1]) for i in range(5)], dtype=torch.float64, device=dev)
+    dist.all_reduce(ph, op=dist.ReduceOp.MAX)
+    ph = ph.cpu().numpy()
+    geo = slab_geometry(g, world)
+    mb = model_bytes(n)["per_kernel"]
+    kb = list(mb.values())
+    grp_bytes = [kb[0] / world, (kb[1] + kb[2] + kb[3]) / world, (kb[4] + kb[5]) / world]
+    grp_ms = [ph[0], ph[2], ph[4]]
+    dom = int(np.argmax(grp_ms))
+    peak, peak_src = peaks()
+    achieved = grp_bytes[dom] / (grp_ms[dom] * 1e-3) / 1e9
+    a2a_bytes = (geo["send1"] + geo["send2"]) * 16 * (world - 1) / world
+    a2a_ms = ph[1] + ph[3]
+    if rank != 0:
+        return
+    names = ["K1 (forward)", "K2-K4 (middle)", "K5-K6 (finish)"]
+    line = {
+        "metric": METRIC, "value": value, "unit": "stages/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": T * 1e3 / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (device-side seeded HIT-spectrum slabs, E=0.5)",
+        "config": {"workload": f"forced_hit_bs5_{n}^3", "n": n, "nu": 5e-4, "tol": 1e-6, "k_f": 2.0,
+                   "parallelism": f"y-slab x{world}, NCCL all-to-all", "l2": "inputs larger than L2"},
+        "gpts_stage_per_s": value * n ** 3 / 1e9,
+        "rhs_evals": evals,
+        "stage_hbm_frac": model_bytes(n)["b_stage_bs5"] * value / world / (peak * 1e9),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "kernel": names[dom], "peak_source": peak_src,
+                     "phase_ms": {"forward": ph[0], "a2a1": ph[1], "middle": ph[2], "a2a2": ph[3],
+                                  "finish": ph[4]}},
+        "nvlink": {"bytes_per_rhs_per_gpu": a2a_bytes, "achieved_GBps": a2a_bytes / (a2a_ms * 1e-3) / 1e9
+                   if world > 1 else None, "peak_GBps": 770.0, "peak_source": "B200_PROFILING.md peer copy"},
+        "cpu_baseline": None, "e2e": None, "gpu_launches": launches, "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -341,14 +460,25 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    if world > 1:
+    mode = args.mode
+    if mode == "auto":
+        mode = "single" if world == 1 else "slab"
+    if world > 1 or mode == "slab":
         import torch
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29531")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl")
-    run_native(args, rank, world, local_rank)
-    if world > 1:
+    if mode == "slab":
+        run_slab(args, rank, world, local_rank)
+    else:
+        run_native(args, rank, world, local_rank)
+    if world > 1 or mode == "slab":
         import torch.distributed as dist
 
         dist.destroy_process_group()

@@ -126,6 +126,24 @@ int srk_band_scale(srk_plan* plan, void* u, int ncomp, const int64_t* idx_dev, i
 int srk_rhs_timed(srk_plan* plan, const void* y, void* f, double nu, double ri, double re_pr, void* stream,
                   float* ms_out, int max_kernels);
 
+/* ---- slab decomposition over y (multi-GPU, one plan per rank) ----
+ * The state on rank r is the y-slab (ncomp, n0, n1/nranks, n2/2+1) holding
+ * global rows y in [r*n1/nranks, (r+1)*n1/nranks).  One RHS is
+ *   srk_slab_forward (K1)  -> all-to-all(send1 -> recv1, equal splits)
+ *   srk_slab_middle (K2-K4) -> all-to-all(send2 -> recv2, equal splits)
+ *   srk_slab_finish (K5-K6)
+ * with the exchanges done by the caller (NCCL).  The kernels write the send
+ * layouts and read the receive layouts directly (no pack / unpack passes).
+ * Requires dims = 3, nranks | n1 and nranks | 3*n0/2. */
+int srk_plan_create_slab(srk_plan** out, const int64_t* shape, const double* lengths, int density, int nranks,
+                         int rank);
+/* complex128 element counts of the send (== receive) buffers */
+int srk_slab_sizes(const srk_plan* plan, int64_t* send1, int64_t* send2);
+int srk_slab_forward(srk_plan* plan, const void* y, void* send1, void* stream);
+int srk_slab_middle(srk_plan* plan, const void* recv1, void* send2, void* stream);
+int srk_slab_finish(srk_plan* plan, const void* recv2, const void* y, void* f, double nu, double ri, double re_pr,
+                    void* stream);
+
 /* Number of kernel launches the last srk_rhs issued (launch accounting for
  * the bench's gpu_launches claim). */
 int srk_rhs_launch_count(const srk_plan* plan);

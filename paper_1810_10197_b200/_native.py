@@ -25,7 +25,8 @@ EXPORTS = (
     "srk_plan_workspace_bytes", "srk_plan_set_workspace", "srk_rhs", "srk_widen",
     "srk_narrow", "srk_forward_transform", "srk_inverse_transform", "srk_curl",
     "srk_leray_project", "srk_combine", "srk_step_reduce", "srk_band_energy",
-    "srk_band_scale", "srk_rhs_launch_count", "srk_rhs_timed",
+    "srk_band_scale", "srk_rhs_launch_count", "srk_rhs_timed", "srk_plan_create_slab", "srk_slab_sizes",
+    "srk_slab_forward", "srk_slab_middle", "srk_slab_finish",
 )
 
 _lib = None
@@ -76,6 +77,11 @@ def load():
         "srk_band_scale": (c_int, [vp, vp, c_int, vp, c_int, c_dbl, vp]),
         "srk_rhs_launch_count": (c_int, [vp]),
         "srk_rhs_timed": (c_int, [vp, vp, vp, c_dbl, c_dbl, c_dbl, vp, P(ctypes.c_float), c_int]),
+        "srk_plan_create_slab": (c_int, [P(vp), P(i64), P(c_dbl), c_int, c_int, c_int]),
+        "srk_slab_sizes": (c_int, [vp, P(i64), P(i64)]),
+        "srk_slab_forward": (c_int, [vp, vp, vp, vp]),
+        "srk_slab_middle": (c_int, [vp, vp, vp, vp]),
+        "srk_slab_finish": (c_int, [vp, vp, vp, vp, c_dbl, c_dbl, c_dbl, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -47,7 +47,20 @@ struct PassArgs {
   int K;   // r2c extent n_last/2+1
   double ck0, ck1, ck2;  // 2*pi/L per axis (x, y, z) -- 2D uses ck0, ck2
   long long comp_stride;  // between state components
+  // slab decomposition: rows are grouped in blocks of *_rpb rows
+  // that sit *_bstride elements apart (all-to-all send / receive layouts);
+  // rpb == 0 means plain rows.  y0 / n1g: global y of the slab's first row and
+  // the global y extent (wavenumber labels in the curl).
+  int in_rpb, out_rpb;
+  long long in_bstride, out_bstride;
+  int y0, n1g;
 };
+
+SRK_DEV unsigned row_off(int row, unsigned rs, int rpb, long long bstride) {
+  if (rpb <= 0) return (unsigned)row * rs;
+  const int blk = row / rpb;
+  return (unsigned)blk * (unsigned)bstride + (unsigned)(row - blk * rpb) * rs;
+}
 
 // Fast path: the input rows of the tile are first copied to shared memory with
 // cp.async (16 B per request, no register staging, all requests in flight at
@@ -57,11 +70,11 @@ struct PassArgs {
 // addresses).  Generic path: loaders read global memory directly.
 template <int C>
 __device__ __forceinline__ void stage_rows(cplx* dst, const cplx* __restrict__ src, int rows, unsigned rs,
-                                           int ncols) {
+                                           int ncols, int rpb, long long bstride) {
   const int tot = rows * C;
   for (int i = threadIdx.x; i < tot; i += blockDim.x) {
     const int r = i / C, c = i - (i / C) * C;
-    if (c < ncols) cp_async16(dst + i, src + (unsigned)r * rs + (unsigned)c);
+    if (c < ncols) cp_async16(dst + i, src + row_off(r, rs, rpb, bstride) + (unsigned)c);
   }
 }
 
@@ -88,7 +101,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
   if constexpr (KIND == PK_INV) {
     const double sc = a.scale;
     if constexpr (Eng::kFast) {
-      stage_rows<C>(sm, inp, n, rs, ncols);
+      stage_rows<C>(sm, inp, n, rs, ncols, a.in_rpb, a.in_bstride);
       cp_async_wait_all();
       __syncthreads();
     }
@@ -96,11 +109,11 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
       const int cr = pad_src(row, n, M);
       const bool ok = cr >= 0;
       const int r = ok ? cr : 0;
-      cplx v = Eng::kFast ? sm[r * C + col] : inp[(unsigned)r * rs + (unsigned)col];
+      cplx v = Eng::kFast ? sm[r * C + col] : inp[row_off(r, rs, a.in_rpb, a.in_bstride) + (unsigned)col];
       const double f = ok ? sc : 0.0;
       return cmk(v.x * f, v.y * f);
     };
-    auto st = [&](int row, int col, cplx v) { outp[(unsigned)row * rs + (unsigned)col] = v; };
+    auto st = [&](int row, int col, cplx v) { outp[row_off(row, rs, a.out_rpb, a.out_bstride) + (unsigned)col] = v; };
     Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, a.tw, ncols, ld, st);
   } else if constexpr (KIND == PK_INV_RHS) {
     // plane = signal s: [u_0..u_{d-1}, w (3 comps in 3D, 1 in 2D), rho]
@@ -114,7 +127,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
     double ky = 0.0, kz = 0.0;
     if (d == 3) {
       const int y = q / a.K, kzi = q - y * a.K;
-      ky = mode_full(y, a.n1) * a.ck1;
+      ky = mode_full(a.y0 + y, a.n1g) * a.ck1;
       kz = (double)kzi * a.ck2;
     } else {
       kz = (double)q * a.ck2;
@@ -140,8 +153,8 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
     const double sc = a.scale;
     cplx* sb_ = sm + (is_curl ? n * C : 0);
     if constexpr (Eng::kFast) {
-      stage_rows<C>(sm, pa, n, rs, ncols);
-      if (is_curl) stage_rows<C>(sm + n * C, pb, n, rs, ncols);
+      stage_rows<C>(sm, pa, n, rs, ncols, a.in_rpb, a.in_bstride);
+      if (is_curl) stage_rows<C>(sm + n * C, pb, n, rs, ncols, a.in_rpb, a.in_bstride);
       cp_async_wait_all();
       __syncthreads();
     }
@@ -149,7 +162,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
       const int cr = pad_src(row, n, M);
       const bool ok = cr >= 0;
       const int r = ok ? cr : 0;
-      const unsigned off = (unsigned)r * rs + (unsigned)col;
+      const unsigned off = row_off(r, rs, a.in_rpb, a.in_bstride) + (unsigned)col;
       const cplx ua = Eng::kFast ? sm[r * C + col] : pa[off];
       const cplx ub = Eng::kFast ? sb_[r * C + col] : pb[off];
       // spectral.py:47-65: w = i k x u (k_a = mode_a * 2pi/L_a, grid.py:75-93)
@@ -160,19 +173,19 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
       const double f = ok ? sc : 0.0;
       return cmk(v.x * f, v.y * f);
     };
-    auto st = [&](int row, int col, cplx v) { outp[(unsigned)row * rs + (unsigned)col] = v; };
+    auto st = [&](int row, int col, cplx v) { outp[row_off(row, rs, a.out_rpb, a.out_bstride) + (unsigned)col] = v; };
     Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, a.tw, ncols, ld, st);
   } else {  // PK_FWD: forward C2C + truncation (+ scale, Nyquist / DC-imag zeroing)
     const bool zn = a.zero_nyq != 0;
-    const bool zdc = (a.zero_dc_imag != 0) && (w0 == 0);
+    const bool zdc = (a.zero_dc_imag != 0) && (w0 == 0) && (a.y0 == 0);
     const double sc = a.scale;
     if constexpr (Eng::kFast) {
-      stage_rows<C>(sm, inp, M, rs, ncols);
+      stage_rows<C>(sm, inp, M, rs, ncols, a.in_rpb, a.in_bstride);
       cp_async_wait_all();
       __syncthreads();
     }
     auto ld = [&](int row, int col) -> cplx {
-      return Eng::kFast ? sm[row * C + col] : inp[(unsigned)row * rs + (unsigned)col];
+      return Eng::kFast ? sm[row * C + col] : inp[row_off(row, rs, a.in_rpb, a.in_bstride) + (unsigned)col];
     };
     auto st = [&](int row, int col, cplx v) {
       const int c = trunc_dst(row, n, M, zn);
@@ -180,7 +193,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
       cplx o = cmk(v.x * sc, v.y * sc);
       if (c == -2) o = cmk(0.0, 0.0);
       if (zdc && c == 0 && col == 0) o.y = 0.0;
-      outp[(unsigned)(c == -2 ? (n >> 1) : c) * rs + (unsigned)col] = o;
+      outp[row_off(c == -2 ? (n >> 1) : c, rs, a.out_rpb, a.out_bstride) + (unsigned)col] = o;
     };
     Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, a.tw, ncols, ld, st);
   }

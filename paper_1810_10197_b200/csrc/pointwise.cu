@@ -28,7 +28,7 @@ __device__ __forceinline__ KVec kvec(long long idx, const GeomArgs& g) {
   if (g.dims == 3) {
     const int y = (int)(xy % g.n1), x = (int)(xy / g.n1);
     r.k[0] = DMUL(mode_full(x, g.n0), g.ck0);
-    r.k[1] = DMUL(mode_full(y, g.n1), g.ck1);
+    r.k[1] = DMUL(mode_full(g.y0 + y, g.n1g), g.ck1);
     r.k[2] = DMUL((double)kz, g.ck2);
     r.k2 = DADD(DADD(DMUL(r.k[0], r.k[0]), DMUL(r.k[1], r.k[1])), DMUL(r.k[2], r.k[2]));
   } else {

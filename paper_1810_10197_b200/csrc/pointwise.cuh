@@ -9,8 +9,9 @@
 
 struct GeomArgs {
   int dims;
-  int n0, n1, K;  // 2D: n1 = 1, K = n_last/2+1
+  int n0, n1, K;  // 2D: n1 = 1, K = n_last/2+1; slab: n1 = local y rows
   double ck0, ck1, ck2;  // 2*pi/L per axis; 2D uses ck0 (x) and ck2 (last)
+  int y0, n1g;    // slab: global y of local row 0, global y extent (n1g = n1, y0 = 0 unsplit)
 };
 
 struct ProjArgs {

@@ -133,6 +133,8 @@ struct srk_plan {
   double ck0, ck1, ck2;
   long long modes;  // n0*n1*K per component
   int S, So;        // rhs signal counts (widened, products)
+  int nranks = 1, rank = 0;  // slab decomposition over y (3D only)
+  int n1g = 0, y0 = 0, Mx = 0;
   std::map<int, cplx*> tw;
   long long A_elems = 0, B_elems = 0;
   char* ws = nullptr;
@@ -222,6 +224,8 @@ GeomArgs geom(const srk_plan* p) {
   g.ck0 = p->ck0;
   g.ck1 = p->ck1;
   g.ck2 = p->ck2;
+  g.y0 = p->y0;
+  g.n1g = p->n1g;
   return g;
 }
 
@@ -374,6 +378,7 @@ int srk_plan_create(srk_plan** out, int dims, const int64_t* shape, const double
     p->ck2 = two_pi / lengths[1];
   }
   p->K = p->n2 / 2 + 1;
+  p->n1g = p->n1;
   p->m0 = 3 * p->n0 / 2;
   p->m1 = dims == 3 ? 3 * p->n1 / 2 : 1;
   p->m2 = 3 * p->n2 / 2;
@@ -479,6 +484,8 @@ int srk_rhs(srk_plan* p, const void* y_, void* f_, double nu, double ri, double 
   a.ck1 = p->ck1;
   a.ck2 = p->ck2;
   a.comp_stride = p->modes;
+  a.y0 = p->y0;
+  a.n1g = p->n1g;
   if ((rc = launch_col(p, KK_INV_RHS, a, st))) return rc;
   const cplx* zin = p->A;
   cplx* zout = p->B;
@@ -659,6 +666,148 @@ int srk_band_scale(srk_plan* p, void* u, int ncomp, const int64_t* idx, int nb, 
   if (!p) return fail(SRK_ERR_INVALID, "null plan");
   srk_launch_band_scale((cplx*)u, (const long long*)idx, nb, ncomp, p->modes, gamma, (cudaStream_t)stream);
   return check_launch("k_band_scale");
+}
+
+// ---------------------------------------------------------------------------
+// Slab decomposition over y: rank r owns y-slab [r*Ny, (r+1)*Ny)
+// of the spectral state.  srk_slab_forward (K1) writes the x-padded signals
+// straight into the all-to-all #1 send layout [dest][s][x_loc][y_loc][kz];
+// srk_slab_middle (K2-K4) reads the receive layout [src][s][x_loc][y_loc][kz]
+// of its x-slab and writes the all-to-all #2 send layout
+// [dest][o][x_loc][y_loc][kz]; srk_slab_finish (K5-K6) reads the receive
+// layout [src][o][x_loc][y_loc][kz] and writes the tendency y-slab.
+// ---------------------------------------------------------------------------
+int srk_plan_create_slab(srk_plan** out, const int64_t* shape, const double* lengths, int density, int nranks,
+                         int rank) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(SRK_ERR_INVALID, "bad rank / nranks");
+  if (shape[1] % nranks || (3 * shape[0] / 2) % nranks)
+    return fail(SRK_ERR_INVALID, "slab decomposition needs nranks | n1 and nranks | 3*n0/2");
+  int64_t loc[3] = {shape[0], shape[1] / nranks, shape[2]};
+  if (loc[1] < 1) return fail(SRK_ERR_INVALID, "too many ranks for n1");
+  // create with the local y extent (workspace sizing is redone below)
+  int64_t tmp[3] = {shape[0], shape[1], shape[2]};
+  int rc = srk_plan_create(out, 3, tmp, lengths, density, 0);
+  if (rc) return rc;
+  srk_plan* p = *out;
+  p->nranks = nranks;
+  p->rank = rank;
+  p->n1g = (int)shape[1];
+  p->n1 = (int)loc[1];
+  p->y0 = rank * p->n1;
+  p->Mx = p->m0 / nranks;
+  p->modes = (long long)p->n0 * p->n1 * p->K;
+  const long long K = p->K, Ny = p->n1, Mx = p->Mx, m1 = p->m1, n0 = p->n0;
+  long long A = std::max<long long>(p->So * Mx * m1 * K, p->So * n0 * Ny * K);
+  long long B = p->S * Mx * m1 * K;
+  p->A_elems = A;
+  p->B_elems = B;
+  p->need_bytes = align256(A * 16) + align256(std::max<long long>(B, 1) * 16);
+  return SRK_OK;
+}
+
+int srk_slab_sizes(const srk_plan* p, int64_t* send1, int64_t* send2) {
+  if (!p) return fail(SRK_ERR_INVALID, "null plan");
+  *send1 = (int64_t)p->S * p->m0 * p->n1 * p->K;
+  *send2 = (int64_t)p->So * p->Mx * p->n1g * p->K;
+  return SRK_OK;
+}
+
+int srk_slab_forward(srk_plan* p, const void* y, void* send1, void* stream) {
+  if (!p || !p->Mx) return fail(SRK_ERR_INVALID, "not a slab plan");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int d = p->dims;
+  const long long blk = (long long)p->S * p->Mx * p->n1 * p->K;
+  PassArgs a = x_pass(p, (const cplx*)y, (cplx*)send1, p->S, p->n0, p->m0, p->m0, p->n0);
+  a.out_plane_stride = (long long)p->Mx * p->n1 * p->K;
+  a.out_rpb = p->Mx;
+  a.out_bstride = blk;
+  a.scale = std::pow(1.5, d) / ((double)p->m0 * p->m1 * p->m2);
+  a.dims = d;
+  a.n1 = p->n1;
+  a.K = p->K;
+  a.ck0 = p->ck0;
+  a.ck1 = p->ck1;
+  a.ck2 = p->ck2;
+  a.comp_stride = p->modes;
+  a.y0 = p->y0;
+  a.n1g = p->n1g;
+  return launch_col(p, KK_INV_RHS, a, st);
+}
+
+int srk_slab_middle(srk_plan* p, const void* recv1, void* send2, void* stream) {
+  if (!p || !p->Mx) return fail(SRK_ERR_INVALID, "not a slab plan");
+  int rc = need_ws(p);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long K = p->K, Ny = p->n1, Mx = p->Mx, m1 = p->m1;
+  // K2: y pad + inverse y from the receive layout
+  PassArgs b = base_pass();
+  b.in = (const cplx*)recv1;
+  b.out = p->B;
+  b.M = p->m1;
+  b.n = p->n1g;
+  b.planes = p->S * p->Mx;
+  b.Qp = p->K;
+  b.row_stride = K;
+  b.in_plane_stride = Ny * K;
+  b.out_plane_stride = m1 * K;
+  b.in_rpb = (int)Ny;
+  b.in_bstride = (long long)p->S * Mx * Ny * K;
+  if ((rc = launch_col(p, KK_INV, b, st))) return rc;
+  // K3: z pencils of the x-slab
+  const int P = (int)(Mx * m1);
+  ZArgs z = z_args(p, p->m2, p->n2, P);
+  z.in = p->B;
+  z.out = p->A;
+  z.in_sig_stride = (long long)P * K;
+  z.out_sig_stride = (long long)P * K;
+  z.zero_nyq = 1;
+  if ((rc = launch_z(p, p->density ? KK_Z_B3 : KK_Z_NS3, z, 0, 0, st))) return rc;
+  // K4: forward y + truncation into the all-to-all #2 send layout
+  PassArgs c = base_pass();
+  c.in = p->A;
+  c.out = (cplx*)send2;
+  c.M = p->m1;
+  c.n = p->n1g;
+  c.planes = p->So * p->Mx;
+  c.Qp = p->K;
+  c.row_stride = K;
+  c.in_plane_stride = m1 * K;
+  c.out_plane_stride = Ny * K;
+  c.out_rpb = (int)Ny;
+  c.out_bstride = (long long)p->So * Mx * Ny * K;
+  c.zero_nyq = 1;
+  return launch_col(p, KK_FWD, c, st);
+}
+
+int srk_slab_finish(srk_plan* p, const void* recv2, const void* y, void* f, double nu, double ri, double re_pr,
+                    void* stream) {
+  if (!p || !p->Mx) return fail(SRK_ERR_INVALID, "not a slab plan");
+  int rc = need_ws(p);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long K = p->K, Ny = p->n1, Mx = p->Mx;
+  PassArgs c5 = x_pass(p, (const cplx*)recv2, p->A, p->So, p->m0, p->n0, p->m0, p->n0);
+  c5.in_plane_stride = Mx * Ny * K;
+  c5.in_rpb = p->Mx;
+  c5.in_bstride = (long long)p->So * Mx * Ny * K;
+  c5.scale = std::pow(1.0 / 1.5, p->dims);
+  c5.zero_nyq = 1;
+  c5.zero_dc_imag = 1;
+  c5.y0 = p->y0;
+  if ((rc = launch_col(p, KK_FWD, c5, st))) return rc;
+  ProjArgs pa;
+  pa.g = geom(p);
+  pa.G = p->A;
+  pa.y = (const cplx*)y;
+  pa.f = (cplx*)f;
+  pa.modes = p->modes;
+  pa.density = p->density;
+  pa.nu = nu;
+  pa.ri = ri;
+  pa.re_pr = re_pr;
+  srk_launch_project(pa, st);
+  return check_launch("k_project");
 }
 
 }  // extern "C"

@@ -32,15 +32,19 @@ class DiagnosticsRecord:
 
 
 def reduce_sums(grid: Grid, y1, fl=None, y0=None, terms=(), tol_abs=0.0, tol_rel=0.0, flags=2, ncomp=None,
-                stream=None):
-    """Launch srk_step_reduce; returns the 9 device sums as a CUDA float64 tensor (no sync)."""
-    p = get_plan(grid)
+                stream=None, plan=None):
+    """Launch srk_step_reduce; returns the 9 device sums as a CUDA float64 tensor (no sync).
+
+    ``plan``: a slab plan handle (paper_1810_10197_b200.slab) when y1 is a y-slab;
+    the sums are then this rank's partials."""
+    lib = _native.load()
+    h = get_plan(grid).h if plan is None else plan
     ncomp = y1.shape[0] if ncomp is None else ncomp
     out = torch.empty(9, dtype=torch.float64, device=y1.device)
     Fs = [t for _, t in terms]
     cs = [c for c, _ in terms]
-    _native.check(p.lib.srk_step_reduce(
-        p.h, _native.ptr(y0), _native.ptr(y1), len(Fs), _native.ptr_array(Fs), _native.dbl_array(cs),
+    _native.check(lib.srk_step_reduce(
+        h, _native.ptr(y0), _native.ptr(y1), len(Fs), _native.ptr_array(Fs), _native.dbl_array(cs),
         _native.ptr(fl if fl is not None else y1), ncomp, float(tol_abs), float(tol_rel), int(flags),
         _native.ptr(out), _native.stream_ptr(stream)), "srk_step_reduce")
     _native.count(2)

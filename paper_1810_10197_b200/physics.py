@@ -113,23 +113,50 @@ def forcing_band(grid: Grid, k_f, device):
     return _BANDS[key]
 
 
-def apply_forcing(u_hat, grid: Grid, target_energy, k_f):
-    """Rescale 0<|k|<=k_f in place to restore ``target_energy`` (physics.py:209-239)."""
+def forcing_band_slab(grid: Grid, k_f, device, rank, nranks):
+    """Band modes of one y-slab (flat indices within the slab component)."""
+    key = (grid.shape, grid.lengths, float(k_f), str(device), rank, nranks)
+    if key not in _BANDS:
+        ny = grid.shape[1] // nranks
+        k2 = grid.k2[:, rank * ny:(rank + 1) * ny]
+        band = (k2 > 0.0) & (k2 <= k_f * k_f * (1.0 + 1e-12))
+        idx = np.flatnonzero(band.ravel()).astype(np.int64)
+        w = np.broadcast_to(grid.hermitian_weights, k2.shape).ravel()[idx].astype(np.float64)
+        _BANDS[key] = (torch.from_numpy(idx).to(device), torch.from_numpy(np.ascontiguousarray(w)).to(device),
+                       len(idx))
+    return _BANDS[key]
+
+
+def apply_forcing(u_hat, grid: Grid, target_energy, k_f, plan=None, allreduce=None, slab=None):
+    """Rescale 0<|k|<=k_f in place to restore ``target_energy`` (physics.py:209-239).
+
+    Slab runs pass the slab ``plan``, ``slab=(rank, nranks)`` and the rank-order
+    ``allreduce``; E_total and E_band are then global sums."""
     from .diagnostics import reduce_sums
 
     u = u_hat
     if not (isinstance(u, torch.Tensor) and u.is_cuda and u.is_contiguous()):
         raise TypeError("apply_forcing works in place on a contiguous CUDA tensor")
-    idx, w, nb = forcing_band(grid, k_f, u.device)
-    p = get_plan(grid)
+    if slab is None:
+        idx, w, nb = forcing_band(grid, k_f, u.device)
+        ph = get_plan(grid).h
+    else:
+        idx, w, nb = forcing_band_slab(grid, k_f, u.device, slab[0], slab[1])
+        ph = plan
+    lib = _native.load()
     ncomp = u.shape[0]
     pts2 = 2.0 * float(grid.points) ** 2
-    q = reduce_sums(grid, u, flags=2, ncomp=ncomp)
-    eb = torch.empty(1, dtype=torch.float64, device=u.device)
-    _native.check(p.lib.srk_band_energy(p.h, _native.ptr(u), ncomp, _native.ptr(idx), _native.ptr(w), nb,
-                                        _native.ptr(eb), _native.stream_ptr()))
-    e_total = q[4].item() / pts2
-    e_band = eb.item() / pts2
+    q = reduce_sums(grid, u, flags=2, ncomp=ncomp, plan=plan)
+    eb = torch.zeros(1, dtype=torch.float64, device=u.device)
+    if nb > 0:
+        _native.check(lib.srk_band_energy(ph, _native.ptr(u), ncomp, _native.ptr(idx), _native.ptr(w), nb,
+                                          _native.ptr(eb), _native.stream_ptr()))
+    if allreduce is not None:
+        s = allreduce([q[4].item(), eb.item()])
+        e_total, e_band = s[0] / pts2, s[1] / pts2
+    else:
+        e_total = q[4].item() / pts2
+        e_band = eb.item() / pts2
     e_rest = e_total - e_band
     if e_band <= 0.0:
         raise ForcingError("forcing band carries no energy")
@@ -137,7 +164,8 @@ def apply_forcing(u_hat, grid: Grid, target_energy, k_f):
     if radicand < 0.0:
         raise ForcingError(f"energy outside the band ({e_rest:.6e}) exceeds target ({target_energy:.6e})")
     gamma = float(np.sqrt(radicand))
-    _native.check(p.lib.srk_band_scale(p.h, _native.ptr(u), ncomp, _native.ptr(idx), nb, gamma,
-                                       _native.stream_ptr()))
+    if nb > 0:
+        _native.check(lib.srk_band_scale(ph, _native.ptr(u), ncomp, _native.ptr(idx), nb, gamma,
+                                         _native.stream_ptr()))
     _native.count(2)
     return gamma

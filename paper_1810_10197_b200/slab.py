@@ -1,0 +1,210 @@
+"""Slab-decomposed multi-GPU RHS: one process per GPU, NCCL all-to-all.
+
+Rank r of P owns the y-slab ``(ncomp, n0, n1/P, n2/2+1)`` of the spectral
+state (global rows y in [r*n1/P, (r+1)*n1/P)).  One RHS evaluation:
+
+    K1 (x-inverse + curl, local)        -> send1 [dest][s][x_loc][y_loc][kz]
+    all-to-all #1 (equal splits)         -> recv1 [src][s][x_loc][y_loc][kz]  (x-slab)
+    K2 + K3 + K4 (y, z, y passes, local) -> send2 [dest][o][x_loc][y_loc][kz]
+    all-to-all #2                        -> recv2 [src][o][x_loc][y_loc][kz]  (y-slab)
+    K5 + K6 (x-forward + projection)     -> f (y-slab)
+
+The exchange happens after the x padding and before the y padding, so it moves
+9*S_x complex values per RHS instead of 9*S_xy.  The kernels write
+the send layouts and read the receive layouts directly; there is no pack or
+unpack pass.  Reductions (error norm, E_kin, eps, Z, forcing band energy) are
+per-slab device sums, all-gathered and added in rank order so every rank takes
+the same accept/reject decision bit for bit.
+
+The stage functions are pluggable (``backend``) so the CPU test-suite can run
+the same orchestration on gloo with a numpy restatement of the three kernel
+groups (tests/slab_numpy_backend.py).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native
+from .grid import Grid
+from .physics import PhysParams
+
+
+def slab_geometry(grid: Grid, nranks: int, density=False):
+    """Buffer sizes (complex elements) and local extents of the decomposition."""
+    if grid.dims != 3:
+        raise ValueError("slab decomposition is 3D only (2D configs run as replicas)")
+    n0, n1, n2 = grid.shape
+    m0 = 3 * n0 // 2
+    if n1 % nranks or m0 % nranks:
+        raise ValueError(f"need nranks | n1 ({n1}) and nranks | 3*n0/2 ({m0})")
+    K = n2 // 2 + 1
+    S = 3 + 3 + (1 if density else 0)
+    So = 6 if density else 3
+    ny, mx = n1 // nranks, m0 // nranks
+    return dict(n0=n0, n1=n1, n2=n2, K=K, m0=m0, m1=3 * n1 // 2, m2=3 * n2 // 2, ny=ny, mx=mx, S=S, So=So,
+                send1=S * m0 * ny * K, send2=So * mx * n1 * K)
+
+
+def scatter_slab(y_full, rank, nranks):
+    """(c, n0, n1, K) -> this rank's y-slab (contiguous copy)."""
+    ny = y_full.shape[2] // nranks
+    return y_full[:, :, rank * ny:(rank + 1) * ny].contiguous() if isinstance(y_full, torch.Tensor) else \
+        np.ascontiguousarray(y_full[:, :, rank * ny:(rank + 1) * ny])
+
+
+class CudaSlabBackend:
+    """The three libsrk kernel groups of one rank (srk_slab_forward / _middle / _finish)."""
+
+    def __init__(self, grid: Grid, params: PhysParams, rank: int, nranks: int, density=False):
+        self.lib = _native.load()
+        self.params = params
+        shape = (ctypes.c_int64 * 3)(*grid.shape)
+        lengths = (ctypes.c_double * 3)(*grid.lengths)
+        h = ctypes.c_void_p()
+        _native.check(self.lib.srk_plan_create_slab(ctypes.byref(h), shape, lengths, int(density), nranks, rank),
+                      "srk_plan_create_slab")
+        self.h = h
+        nb = ctypes.c_int64()
+        _native.check(self.lib.srk_plan_workspace_bytes(h, ctypes.byref(nb)))
+        self.ws = torch.empty(max(nb.value, 256), dtype=torch.uint8, device="cuda")
+        _native.check(self.lib.srk_plan_set_workspace(h, ctypes.c_void_p(self.ws.data_ptr()), self.ws.numel()))
+        self.device = torch.device("cuda", torch.cuda.current_device())
+
+    def empty(self, n):
+        return torch.empty(n, dtype=torch.complex128, device=self.device)
+
+    def forward(self, y, send1):
+        _native.check(self.lib.srk_slab_forward(self.h, _native.ptr(y), _native.ptr(send1), _native.stream_ptr()))
+        _native.count(1)
+
+    def middle(self, recv1, send2):
+        _native.check(self.lib.srk_slab_middle(self.h, _native.ptr(recv1), _native.ptr(send2),
+                                               _native.stream_ptr()))
+        _native.count(3)
+
+    def finish(self, recv2, y, f):
+        p = self.params
+        _native.check(self.lib.srk_slab_finish(self.h, _native.ptr(recv2), _native.ptr(y), _native.ptr(f),
+                                               1.0 / p.reynolds, float(p.richardson),
+                                               float(p.reynolds) * float(p.prandtl), _native.stream_ptr()))
+        _native.count(2)
+
+    def __del__(self):
+        try:
+            self.lib.srk_plan_destroy(self.h)
+        except Exception:
+            pass
+
+
+def dist_all_to_all(group=None):
+    """Equal-split all-to-all over torch.distributed (NCCL on GPUs, gloo on CPU)."""
+    import torch.distributed as dist
+
+    def exchange(recv, send):
+        if recv.is_complex():  # NCCL / gloo move the (re, im) float64 pairs
+            recv, send = torch.view_as_real(recv), torch.view_as_real(send)
+        dist.all_to_all_single(recv, send, group=group)
+
+    return exchange
+
+
+def dist_sum_in_rank_order(group=None):
+    """Deterministic all-reduce of a small vector: all-gather, then add in rank order."""
+    import torch.distributed as dist
+
+    def reduce(q):
+        q = torch.as_tensor(q, dtype=torch.float64)
+        t = q.to(dist_device(group))
+        parts = [torch.empty_like(t) for _ in range(dist.get_world_size(group))]
+        dist.all_gather(parts, t, group=group)
+        acc = parts[0].clone()
+        for p in parts[1:]:
+            acc += p
+        return acc.cpu().tolist()
+
+    return reduce
+
+
+def dist_device(group=None):
+    import torch.distributed as dist
+
+    return torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else \
+        torch.device("cpu")
+
+
+class SlabFlowRHS:
+    """``f(t, y_slab)`` for one rank of a slab-decomposed grid (drop-in for FlowRHS)."""
+
+    def __init__(self, grid: Grid, params: PhysParams, rank: int, nranks: int, density=False, backend=None,
+                 exchange=None):
+        self.grid, self.params, self.rank, self.nranks = grid, params, rank, nranks
+        self.density = bool(density)
+        self.geo = slab_geometry(grid, nranks, density)
+        self.backend = backend if backend is not None else CudaSlabBackend(grid, params, rank, nranks, density)
+        self.exchange = exchange if exchange is not None else dist_all_to_all()
+        g = self.geo
+        self.send1, self.recv1 = self.backend.empty(g["send1"]), self.backend.empty(g["send1"])
+        self.send2, self.recv2 = self.backend.empty(g["send2"]), self.backend.empty(g["send2"])
+        self.calls = 0
+
+    @property
+    def local_kshape(self):
+        g = self.geo
+        return (g["n0"], g["ny"], g["K"])
+
+    def __call__(self, t, y, out=None):
+        f = out if out is not None else (torch.empty_like(y) if isinstance(y, torch.Tensor) else np.empty_like(y))
+        self.backend.forward(y, self.send1)
+        self.exchange(self.recv1, self.send1)
+        self.backend.middle(self.recv1, self.send2)
+        self.exchange(self.recv2, self.send2)
+        self.backend.finish(self.recv2, y, f)
+        self.calls += 1
+        return f
+
+
+def hit_slab(grid: Grid, rank: int, nranks: int, a=4.0, energy=0.5, seed=42, allreduce=None):
+    """Device-side synthetic HIT y-slab for throughput runs (FFT cost is
+    data independent): modulus |k| exp(-|k|^2/a^2), uniform random phases from a
+    per-rank torch generator, Leray projection, energy scaled to ``energy``.
+    Unlike hit_init the kz=0 / n/2 planes are not symmetrised (that couples
+    slabs); parity runs use hit_init instead."""
+    from .physics import leray_project  # noqa: F401  (slab-local projection below)
+
+    n0, n1, n2 = grid.shape
+    ny, K = n1 // nranks, n2 // 2 + 1
+    dev = torch.device("cuda", torch.cuda.current_device())
+    L = grid.lengths
+
+    def modes(n):
+        m = torch.arange(n, dtype=torch.float64, device=dev)
+        return torch.where(m > n // 2, m - n, m)
+
+    kx = (modes(n0) * (2 * np.pi / L[0]))[:, None, None]
+    ky = (modes(n1)[rank * ny:(rank + 1) * ny] * (2 * np.pi / L[1]))[None, :, None]
+    kz = (torch.arange(K, dtype=torch.float64, device=dev) * (2 * np.pi / L[2]))[None, None, :]
+    k2 = kx * kx + ky * ky + kz * kz
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(int(seed) * 7919 + rank)
+    u = torch.empty((3, n0, ny, K), dtype=torch.complex128, device=dev)
+    for j in range(3):
+        ph = torch.rand((n0, ny, K), dtype=torch.float64, device=dev, generator=gen) * (2 * np.pi)
+        u[j] = torch.polar(torch.sqrt(k2) * torch.exp(-k2 / a ** 2), ph)
+    inv = torch.where(k2 == 0, torch.zeros_like(k2), 1.0 / torch.where(k2 == 0, torch.ones_like(k2), k2))
+    kd = (kx * u[0] + ky * u[1] + kz * u[2]) * inv
+    u[0] -= kx * kd
+    u[1] -= ky * kd
+    u[2] -= kz * kd
+    u[:, n0 // 2] = 0
+    u[..., K - 1] = 0
+    w = torch.full((K,), 2.0, dtype=torch.float64, device=dev)
+    w[0] = w[-1] = 1.0
+    e = float((w * (u.real ** 2 + u.imag ** 2)).sum()) / (2.0 * float(grid.points) ** 2)
+    if allreduce is not None:
+        e = allreduce([e])[0]
+    u *= float(np.sqrt(energy / e))
+    return u

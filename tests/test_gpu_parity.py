@@ -304,3 +304,54 @@ def test_nonfinite_state_is_rejected():
                                O.OracleRHS(og, 100.0))
     assert (st.rejections, st.prev_rejected, st.h) == (ost.rejections, ost.prev_rejected, ost.h)
     assert st.rejections == 2
+
+
+@pytest.mark.parametrize("P,shape", [(2, (32, 32, 32)), (4, (64, 64, 64)), (3, (32, 48, 16))])
+def test_slab_kernels_emulated_ranks_match_single_gpu(P, shape):
+    """SURVEY §8e kernels on one GPU: P virtual ranks, the all-to-alls emulated by
+    block copies (all_to_all semantics), compared with the unsplit RHS."""
+    from paper_1810_10197_b200.slab import CudaSlabBackend, scatter_slab, slab_geometry
+
+    og = O.OGrid(shape)
+    y = dev(O.hit(og, a=4.0, energy=0.5, seed=8))
+    g = srk.Grid(shape)
+    params = srk.PhysParams(321.0)
+    f_ref = srk.FlowRHS(g, params)(0.0, y)
+    geo = slab_geometry(g, P)
+    backs = [CudaSlabBackend(g, params, r, P) for r in range(P)]
+    ys = [scatter_slab(y, r, P) for r in range(P)]
+
+    def a2a(sends):
+        blk = sends[0].numel() // P
+        return [torch.cat([sends[q][r * blk:(r + 1) * blk] for q in range(P)]) for r in range(P)]
+
+    s1 = [b.empty(geo["send1"]) for b in backs]
+    for r in range(P):
+        backs[r].forward(ys[r], s1[r])
+    r1 = a2a(s1)
+    s2 = [b.empty(geo["send2"]) for b in backs]
+    for r in range(P):
+        backs[r].middle(r1[r], s2[r])
+    r2 = a2a(s2)
+    fs = [torch.empty_like(ys[r]) for r in range(P)]
+    for r in range(P):
+        backs[r].finish(r2[r], ys[r], fs[r])
+    f = torch.cat(fs, dim=2)
+    assert rel(f, f_ref) <= 1e-14
+
+
+def test_slab_reduction_partials_sum_to_global():
+    from paper_1810_10197_b200.diagnostics import reduce_sums
+    from paper_1810_10197_b200.slab import CudaSlabBackend, scatter_slab
+
+    shape = (32, 32, 32)
+    og = O.OGrid(shape)
+    y = dev(O.hit(og, a=4.0, energy=0.5, seed=8))
+    g = srk.Grid(shape)
+    P = 4
+    tot = np.zeros(9)
+    for r in range(P):
+        b = CudaSlabBackend(g, srk.PhysParams(100.0), r, P)
+        tot += np.array(reduce_sums(g, scatter_slab(y, r, P), flags=2, ncomp=3, plan=b.h).tolist())
+    full = np.array(reduce_sums(g, y, flags=2, ncomp=3).tolist())
+    np.testing.assert_allclose(tot[[4, 8]], full[[4, 8]], rtol=1e-13)
