@@ -153,7 +153,10 @@ struct FastFFT {
   static constexpr int C = L::C;
   static constexpr int NT = C * TPC;
   static constexpr bool kFast = true;
-  static_assert((1 * ... * Rs) == M_, "radices must multiply to M");
+  static constexpr int RPROD = (1 * ... * Rs);
+  // RPROD < M: a prefix of a longer plan (the remaining stages are run by the
+  // caller, e.g. the fused middle stage of the NS3 z-pass)
+  static_assert(M_ % RPROD == 0, "radices must divide M");
   SRK_DEV static int col_of(int tid) { return L::col_of(tid, TPC); }
   // ncols: columns of the tile that carry data (<= C); idle threads still hit barriers.
   template <int SIGN, bool LD_SMEM, bool ST_SMEM, class LD, class ST>

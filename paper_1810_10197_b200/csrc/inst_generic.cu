@@ -5,9 +5,15 @@
 
 void srk_reg_generic(KEntry* t) {
   using SE = GenericFFT<GenCols<32>>;
-  t[KK_INV] = SRK_ENTRY((k_colpass<SE, PK_INV, +1>), SE, 0);
-  t[KK_INV_RHS] = SRK_ENTRY((k_colpass<SE, PK_INV_RHS, +1>), SE, 0);
-  t[KK_FWD] = SRK_ENTRY((k_colpass<SE, PK_FWD, -1>), SE, 0);
+  t[KK_INV] = SRK_ENTRY((k_colpass<SE, PK_INV, +1, 0>), SE, 0);
+  t[KK_FWD] = SRK_ENTRY((k_colpass<SE, PK_FWD, -1, 0>), SE, 0);
+  t[KK_INV_P] = t[KK_INV];
+  t[KK_FWD_P] = t[KK_FWD];
+  t[KK_INV_RHS] = SRK_ENTRY((k_colpass<SE, PK_INV_RHS, +1, 0>), SE, 0);
+  t[KK_INV_RHS_SLAB] = SRK_ENTRY((k_colpass<SE, PK_INV_RHS, +1, PF_BOUT>), SE, 0);
+  t[KK_INV_P_SLAB] = SRK_ENTRY((k_colpass<SE, PK_INV, +1, PF_BIN>), SE, 0);
+  t[KK_FWD_P_SLABO] = SRK_ENTRY((k_colpass<SE, PK_FWD, -1, PF_BOUT>), SE, 0);
+  t[KK_FWD_P_SLABI] = SRK_ENTRY((k_colpass<SE, PK_FWD, -1, PF_BIN>), SE, 0);
   using Z4 = ColTile<SRK_GEN_MAXM, 4>;
   using Z3 = ColTile<SRK_GEN_MAXM, 3>;
   using Z6 = ColTile<SRK_GEN_MAXM, 6>;

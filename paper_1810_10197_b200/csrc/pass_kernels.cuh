@@ -78,10 +78,16 @@ __device__ __forceinline__ void stage_rows(cplx* dst, const cplx* __restrict__ s
   }
 }
 
-template <class Eng, int KIND, int SIGN>
-__global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(const PassArgs a) {
+// FL bits: PF_CTN -- padded pass with n = 2M/3 known at compile time (lets the
+// pad / truncate maps resolve statically); PF_BIN / PF_BOUT -- blocked input /
+// output rows (slab all-to-all layouts).
+enum PassFlags { PF_CTN = 1, PF_BIN = 2, PF_BOUT = 4 };
+
+template <class Eng, int KIND, int SIGN, int FL = 0>
+__global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : (Eng::NT <= 256 ? 2 : 1))) k_colpass(const PassArgs a) {
   extern __shared__ __align__(16) cplx sm[];
   constexpr int C = Eng::C;
+  constexpr bool CTN = (FL & PF_CTN) && Eng::kFast;
   const int bid = blockIdx.x;
   int plane, wt;
   if (a.sig_minor) {
@@ -96,12 +102,15 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
   const unsigned rs = (unsigned)a.row_stride;  // intra-plane offsets fit in 32 bits
   const cplx* __restrict__ inp = a.in + plane * a.in_plane_stride + w0;
   cplx* __restrict__ outp = a.out + plane * a.out_plane_stride + w0;
-  const int n = a.n, M = a.M;
+  const int M = CTN ? Eng::M : a.M;
+  const int n = CTN ? 2 * Eng::M / 3 : a.n;
+  const int in_rpb = (FL & PF_BIN) ? a.in_rpb : 0;
+  const int out_rpb = (FL & PF_BOUT) ? a.out_rpb : 0;
 
   if constexpr (KIND == PK_INV) {
     const double sc = a.scale;
     if constexpr (Eng::kFast) {
-      stage_rows<C>(sm, inp, n, rs, ncols, a.in_rpb, a.in_bstride);
+      stage_rows<C>(sm, inp, n, rs, ncols, in_rpb, a.in_bstride);
       cp_async_wait_all();
       __syncthreads();
     }
@@ -109,11 +118,11 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
       const int cr = pad_src(row, n, M);
       const bool ok = cr >= 0;
       const int r = ok ? cr : 0;
-      cplx v = Eng::kFast ? sm[r * C + col] : inp[row_off(r, rs, a.in_rpb, a.in_bstride) + (unsigned)col];
+      cplx v = Eng::kFast ? sm[r * C + col] : inp[row_off(r, rs, in_rpb, a.in_bstride) + (unsigned)col];
       const double f = ok ? sc : 0.0;
       return cmk(v.x * f, v.y * f);
     };
-    auto st = [&](int row, int col, cplx v) { outp[row_off(row, rs, a.out_rpb, a.out_bstride) + (unsigned)col] = v; };
+    auto st = [&](int row, int col, cplx v) { outp[row_off(row, rs, out_rpb, a.out_bstride) + (unsigned)col] = v; };
     Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, a.tw, ncols, ld, st);
   } else if constexpr (KIND == PK_INV_RHS) {
     // plane = signal s: [u_0..u_{d-1}, w (3 comps in 3D, 1 in 2D), rho]
@@ -153,8 +162,8 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
     const double sc = a.scale;
     cplx* sb_ = sm + (is_curl ? n * C : 0);
     if constexpr (Eng::kFast) {
-      stage_rows<C>(sm, pa, n, rs, ncols, a.in_rpb, a.in_bstride);
-      if (is_curl) stage_rows<C>(sm + n * C, pb, n, rs, ncols, a.in_rpb, a.in_bstride);
+      stage_rows<C>(sm, pa, n, rs, ncols, in_rpb, a.in_bstride);
+      if (is_curl) stage_rows<C>(sm + n * C, pb, n, rs, ncols, in_rpb, a.in_bstride);
       cp_async_wait_all();
       __syncthreads();
     }
@@ -162,7 +171,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
       const int cr = pad_src(row, n, M);
       const bool ok = cr >= 0;
       const int r = ok ? cr : 0;
-      const unsigned off = row_off(r, rs, a.in_rpb, a.in_bstride) + (unsigned)col;
+      const unsigned off = row_off(r, rs, in_rpb, a.in_bstride) + (unsigned)col;
       const cplx ua = Eng::kFast ? sm[r * C + col] : pa[off];
       const cplx ub = Eng::kFast ? sb_[r * C + col] : pb[off];
       // spectral.py:47-65: w = i k x u (k_a = mode_a * 2pi/L_a, grid.py:75-93)
@@ -173,19 +182,19 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
       const double f = ok ? sc : 0.0;
       return cmk(v.x * f, v.y * f);
     };
-    auto st = [&](int row, int col, cplx v) { outp[row_off(row, rs, a.out_rpb, a.out_bstride) + (unsigned)col] = v; };
+    auto st = [&](int row, int col, cplx v) { outp[row_off(row, rs, out_rpb, a.out_bstride) + (unsigned)col] = v; };
     Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, a.tw, ncols, ld, st);
   } else {  // PK_FWD: forward C2C + truncation (+ scale, Nyquist / DC-imag zeroing)
     const bool zn = a.zero_nyq != 0;
     const bool zdc = (a.zero_dc_imag != 0) && (w0 == 0) && (a.y0 == 0);
     const double sc = a.scale;
     if constexpr (Eng::kFast) {
-      stage_rows<C>(sm, inp, M, rs, ncols, a.in_rpb, a.in_bstride);
+      stage_rows<C>(sm, inp, M, rs, ncols, in_rpb, a.in_bstride);
       cp_async_wait_all();
       __syncthreads();
     }
     auto ld = [&](int row, int col) -> cplx {
-      return Eng::kFast ? sm[row * C + col] : inp[row_off(row, rs, a.in_rpb, a.in_bstride) + (unsigned)col];
+      return Eng::kFast ? sm[row * C + col] : inp[row_off(row, rs, in_rpb, a.in_bstride) + (unsigned)col];
     };
     auto st = [&](int row, int col, cplx v) {
       const int c = trunc_dst(row, n, M, zn);
@@ -193,7 +202,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
       cplx o = cmk(v.x * sc, v.y * sc);
       if (c == -2) o = cmk(0.0, 0.0);
       if (zdc && c == 0 && col == 0) o.y = 0.0;
-      outp[row_off(c == -2 ? (n >> 1) : c, rs, a.out_rpb, a.out_bstride) + (unsigned)col] = o;
+      outp[row_off(c == -2 ? (n >> 1) : c, rs, out_rpb, a.out_bstride) + (unsigned)col] = o;
     };
     Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, a.tw, ncols, ld, st);
   }
@@ -392,6 +401,146 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 224 ? 2 : 1)) k_zpass(con
     for (int h = 0; h < 2; ++h) {
       const int g = 2 * c + h;
       if (g >= 2 * So) break;
+      const int pp = g / So, s = g - pp * So, pen = p0 + pp;
+      if (pen < a.P) a.out[s * a.out_sig_stride + (long long)pen * K + k] = h ? B : A;
+    }
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// NS3 z-pass with a fused middle stage (fast plans only).  Inverse plan
+// (IR..., 4), forward plan (4, FR...), E = 24, M/4 threads (= 6 columns x
+// M/24).  Thread j runs the last inverse radix-4 butterfly of all 6 complex
+// columns (both pencils) on rows j + M/4*q, forms u x w for both pencils on
+// those 4 rows in registers, packs the 6 real products into the 3 forward
+// columns and runs the first forward radix-4 butterfly (same rows) before
+// writing back -- no physical-space pass through shared memory.  The final
+// forward stage only stores the rows the extraction reads (dead outputs of the
+// last butterfly are removed at compile time).
+// ---------------------------------------------------------------------------
+template <int M, class L, class EngI, int EF, int... FR>
+__global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(const ZArgs a, int, int) {
+  extern __shared__ __align__(16) cplx sm[];
+  constexpr int S = 6, So = 3, NT = M / 4, K = M / 3 + 1, Q = M / 4;
+  static_assert(EngI::NT == NT, "inverse prefix must use M/4 threads");
+  const int p0 = 2 * blockIdx.x;
+  const int tid = threadIdx.x;
+  // ---- staging: 12 real-signal rows of K modes via 1D TMA bulk copies ----
+  cplx* stg = sm;
+  __shared__ __align__(8) unsigned long long mbar;
+  if (tid == 0) {
+    mbar_init(&mbar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    unsigned bytes = 0;
+    for (int g = 0; g < 2 * S; ++g) bytes += (p0 + g / S < a.P) ? (unsigned)(K * 16) : 0u;
+    mbar_expect_tx(&mbar, bytes);
+    for (int g = 0; g < 2 * S; ++g) {
+      const int pp = g / S, s = g - pp * S, pen = p0 + pp;
+      if (pen < a.P) bulk_g2s(stg + g * K, a.in + s * a.in_sig_stride + (long long)pen * K, (unsigned)(K * 16), &mbar);
+    }
+  }
+  if (p0 + 1 >= a.P)
+    for (int i = tid; i < S * K; i += NT) stg[S * K + i] = cmk(0.0, 0.0);
+  mbar_wait(&mbar, 0);
+  __syncthreads();
+  auto hs = [&](int g, int k) -> cplx {
+    const bool head = k < K;
+    const bool tail = k >= M - (K - 1);
+    const int kk = head ? k : (tail ? M - k : 0);
+    cplx X = stg[g * K + kk];
+    X.y = tail ? -X.y : X.y;
+    if (k == 0) X.y = 0.0;  // irfft ignores Im of DC (2k == M cannot occur in the padded band)
+    return (head || tail) ? X : cmk(0.0, 0.0);
+  };
+  // ---- inverse prefix stages (Stockham, in place) ----
+  {
+    auto ld = [&](int k, int c) -> cplx {
+      cplx A = hs(2 * c, k), B = hs(2 * c + 1, k);
+      return cmk(A.x - B.y, A.y + B.x);
+    };
+    auto st = [&](int n, int c, cplx v) { sm[L::idx(n, c)] = v; };
+    EngI::template run<+1, true, true>(a.gp, sm, a.tw, S, ld, st);
+  }
+  __syncthreads();
+  // ---- fused: last inverse radix-4 (Ls = M/4) | u x w | first forward radix-4 ----
+  {
+    const int j = tid;
+    cplx v[S][4];
+#pragma unroll
+    for (int c = 0; c < S; ++c) {
+      if constexpr (Q % 8 == 0) {
+        const int a0 = L::idx(j, c);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) v[c][t] = sm[a0 + t * (Q / 8) * L::STEP8];
+      } else {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) v[c][t] = sm[L::idx(j + t * Q, c)];
+      }
+    }
+    cplx w[4];
+#pragma unroll
+    for (int t = 1; t < 4; ++t) {
+      w[t] = __ldg(&a.tw[t * j]);
+      w[t].y = -w[t].y;  // inverse sign
+    }
+    __syncthreads();
+    double o[4][6];
+#pragma unroll
+    for (int c = 0; c < S; ++c) {
+#pragma unroll
+      for (int t = 1; t < 4; ++t) v[c][t] = cmul(v[c][t], w[t]);
+      DFT<4, +1>::run(v[c]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+#pragma unroll
+      for (int pp = 0; pp < 2; ++pp) {
+        double r[6] = {v[3 * pp][q].x, v[3 * pp][q].y, v[3 * pp + 1][q].x,
+                       v[3 * pp + 1][q].y, v[3 * pp + 2][q].x, v[3 * pp + 2][q].y};
+        zphys<ZOP_NS3>(r, &o[q][3 * pp]);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < So; ++c) {
+      cplx F[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) F[q] = cmk(o[q][2 * c], o[q][2 * c + 1]);
+      DFT<4, -1>::run(F);
+      const int a0 = L::idx(4 * j, c);  // Stockham stage-1 outputs: rows 4j + q
+#pragma unroll
+      for (int q = 0; q < 4; ++q) sm[a0 + q * L::ROWSTEP] = F[q];
+    }
+  }
+  __syncthreads();
+  // ---- forward suffix stages (Ls = 4 ...) on the 3 packed columns ----
+  {
+    // EF elements per thread: 12 puts all M/4 threads on the 3 forward columns
+    constexpr int TPC = M / EF;
+    const int col = tid / TPC, tj = tid - (tid / TPC) * TPC;
+    const bool act = col < So;
+    __builtin_assume(tj >= 0 && tj < TPC);
+    auto ld = [&](int, int) -> cplx { return cmk(0.0, 0.0); };
+    auto st = [&](int n, int c, cplx v) {
+      if (n < K - 1 || n > M - K + 1) sm[L::idx(n, c)] = v;
+    };
+    FastStage<M, EF, L, -1, true, true, 4, FR...>::go(sm, a.tw, col, tj, act, ld, st);
+  }
+  __syncthreads();
+  // ---- extraction: two real spectra per complex column, K modes, kz = n/2 zeroed ----
+  for (int i = tid; i < So * K; i += NT) {
+    const int c = i / K, k = i - (i / K) * K;
+    const bool live = k != K - 1;
+    const cplx Zk = live ? sm[L::idx(k, c)] : cmk(0.0, 0.0);
+    const cplx Zm = live ? sm[L::idx(k == 0 ? 0 : M - k, c)] : cmk(0.0, 0.0);
+    const cplx A = cmk(0.5 * (Zk.x + Zm.x), 0.5 * (Zk.y - Zm.y));
+    const cplx B = cmk(0.5 * (Zk.y + Zm.y), -0.5 * (Zk.x - Zm.x));
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int g = 2 * c + h;
       const int pp = g / So, s = g - pp * So, pen = p0 + pp;
       if (pen < a.P) a.out[s * a.out_sig_stride + (long long)pen * K + k] = h ? B : A;
     }

@@ -6,16 +6,22 @@
 #include "pass_kernels.cuh"
 
 enum KernelKind {
-  KK_INV = 0,      // strided inverse C2C (+ pad)             K1 plain / K2
-  KK_INV_RHS = 1,  // strided inverse C2C with curl on load   K1
-  KK_FWD = 2,      // strided forward C2C (+ truncation)      K4 / K5
+  KK_INV = 0,      // strided inverse C2C, runtime n (unpadded transforms)
+  KK_INV_RHS = 1,  // strided inverse C2C with curl on load, padded      K1
+  KK_FWD = 2,      // strided forward C2C, runtime n
   KK_Z_C2R = 3,
   KK_Z_R2C = 4,
   KK_Z_NS3 = 5,
   KK_Z_NS2 = 6,
   KK_Z_B3 = 7,
   KK_Z_B2 = 8,
-  KK_COUNT = 9
+  KK_INV_P = 9,          // padded inverse (n = 2M/3 compile time)        K2
+  KK_FWD_P = 10,         // padded forward + truncation                   K4, K5
+  KK_INV_RHS_SLAB = 11,  // K1, blocked output rows (all-to-all #1 send)
+  KK_INV_P_SLAB = 12,    // K2, blocked input rows (all-to-all #1 receive)
+  KK_FWD_P_SLABO = 13,   // K4, blocked output rows (all-to-all #2 send)
+  KK_FWD_P_SLABI = 14,   // K5, blocked input rows (all-to-all #2 receive)
+  KK_COUNT = 15
 };
 
 struct KEntry {
@@ -40,6 +46,20 @@ struct GenCols {
 
 #define SRK_ENTRY(KFN, ENG, SMB) KEntry{(const void*)(KFN), ENG::NT, ENG::C, (int)(SMB)}
 
+// Strided kinds of one fast length (SE / SL in scope).
+#define SRK_RHS_SMEM(M, CS) ((SL::SIZE > 2 * (2 * M / 3) * CS ? SL::SIZE : 2 * (2 * M / 3) * CS) * 16)
+#define SRK_STRIDED_KINDS(M, CS)                                                                   \
+    t[KK_INV] = SRK_ENTRY((k_colpass<SE, PK_INV, +1, 0>), SE, SL::SIZE * 16);                      \
+    t[KK_FWD] = SRK_ENTRY((k_colpass<SE, PK_FWD, -1, 0>), SE, SL::SIZE * 16);                      \
+    t[KK_INV_P] = SRK_ENTRY((k_colpass<SE, PK_INV, +1, PF_CTN>), SE, SL::SIZE * 16);               \
+    t[KK_FWD_P] = SRK_ENTRY((k_colpass<SE, PK_FWD, -1, PF_CTN>), SE, SL::SIZE * 16);               \
+    t[KK_INV_RHS] = SRK_ENTRY((k_colpass<SE, PK_INV_RHS, +1, PF_CTN>), SE, SRK_RHS_SMEM(M, CS));   \
+    t[KK_INV_RHS_SLAB] = SRK_ENTRY((k_colpass<SE, PK_INV_RHS, +1, PF_CTN | PF_BOUT>), SE,          \
+                                   SRK_RHS_SMEM(M, CS));                                           \
+    t[KK_INV_P_SLAB] = SRK_ENTRY((k_colpass<SE, PK_INV, +1, PF_CTN | PF_BIN>), SE, SL::SIZE * 16); \
+    t[KK_FWD_P_SLABO] = SRK_ENTRY((k_colpass<SE, PK_FWD, -1, PF_CTN | PF_BOUT>), SE, SL::SIZE * 16); \
+    t[KK_FWD_P_SLABI] = SRK_ENTRY((k_colpass<SE, PK_FWD, -1, PF_CTN | PF_BIN>), SE, SL::SIZE * 16);
+
 // Instantiate every kernel kind for one fast FFT length.
 #define SRK_DEFINE_SIZE(NAME, M, E, CS, ...) SRK_DEFINE_SIZE_F(NAME, M, E, CS, E, (__VA_ARGS__), __VA_ARGS__)
 #define SRK_UNPAREN(...) __VA_ARGS__
@@ -49,10 +69,7 @@ struct GenCols {
   void NAME(KEntry* t) {                                                                           \
     using SL = RowTile<M, CS>;                                                                     \
     using SE = FastFFT<M, E, SL, __VA_ARGS__>;                                                     \
-    t[KK_INV] = SRK_ENTRY((k_colpass<SE, PK_INV, +1>), SE, SL::SIZE * 16);                         \
-    t[KK_INV_RHS] = SRK_ENTRY((k_colpass<SE, PK_INV_RHS, +1>), SE,                                 \
-                              (SL::SIZE > 2 * (2 * M / 3) * CS ? SL::SIZE : 2 * (2 * M / 3) * CS) * 16); \
-    t[KK_FWD] = SRK_ENTRY((k_colpass<SE, PK_FWD, -1>), SE, SL::SIZE * 16);                         \
+    SRK_STRIDED_KINDS(M, CS)                                                                       \
     using Z4 = ColTile<M, 4>;                                                                      \
     using Z3 = ColTile<M, 3>;                                                                      \
     using Z6 = ColTile<M, 6>;                                                                      \
@@ -70,6 +87,29 @@ struct GenCols {
     t[KK_Z_B2] = SRK_ENTRY((k_zpass<E4, Z4, ZOP_B2>), E4, Z4::SIZE * 16);                          \
   }
 
+// Separate strided-pass plan (ES elements/thread, CSS columns, radices SR) and
+// z-pass plan (E, CS, radices ...).
+#define SRK_DEFINE_SIZE_S(NAME, M, ES, CSS, SR, E, ...)                                             \
+  void NAME(KEntry* t) {                                                                           \
+    using SL = RowTile<M, CSS>;                                                                    \
+    using SE = FastFFT<M, ES, SL, SRK_UNPAREN SR>;                                                 \
+    SRK_STRIDED_KINDS(M, CSS)                                                                      \
+    using Z4 = ColTile<M, 4>;                                                                      \
+    using Z3 = ColTile<M, 3>;                                                                      \
+    using Z6 = ColTile<M, 6>;                                                                      \
+    using Z7 = ColTile<M, 7>;                                                                      \
+    using E4 = FastFFT<M, E, Z4, __VA_ARGS__>;                                                     \
+    using E3 = FastFFT<M, E, Z3, __VA_ARGS__>;                                                     \
+    using E6 = FastFFT<M, E, Z6, __VA_ARGS__>;                                                     \
+    using E7 = FastFFT<M, E, Z7, __VA_ARGS__>;                                                     \
+    t[KK_Z_C2R] = SRK_ENTRY((k_zpass<E4, Z4, ZOP_C2R>), E4, Z4::SIZE * 16);                        \
+    t[KK_Z_R2C] = SRK_ENTRY((k_zpass<E4, Z4, ZOP_R2C>), E4, Z4::SIZE * 16);                        \
+    t[KK_Z_NS3] = SRK_ENTRY((k_zpass<E6, Z6, ZOP_NS3>), E6, Z6::SIZE * 16);                        \
+    t[KK_Z_NS2] = SRK_ENTRY((k_zpass<E3, Z3, ZOP_NS2>), E3, Z3::SIZE * 16);                        \
+    t[KK_Z_B3] = SRK_ENTRY((k_zpass<E7, Z7, ZOP_B3>), E7, Z7::SIZE * 16);                          \
+    t[KK_Z_B2] = SRK_ENTRY((k_zpass<E4, Z4, ZOP_B2>), E4, Z4::SIZE * 16);                          \
+  }
+
 // Unpadded power-of-two lengths only need the plain kinds.
 #define SRK_DEFINE_SIZE_PLAIN(NAME, M, E, CS, ...)                                                 \
   void NAME(KEntry* t) {                                                                           \
@@ -81,4 +121,14 @@ struct GenCols {
     using E4 = FastFFT<M, E, Z4, __VA_ARGS__>;                                                     \
     t[KK_Z_C2R] = SRK_ENTRY((k_zpass<E4, Z4, ZOP_C2R>), E4, Z4::SIZE * 16);                        \
     t[KK_Z_R2C] = SRK_ENTRY((k_zpass<E4, Z4, ZOP_R2C>), E4, Z4::SIZE * 16);                        \
+  }
+
+// NS3 z-pass with the fused middle stage: inverse prefix (IR..., product M/4),
+// forward suffix (FR..., product M/4), E = 24.
+#define SRK_NS3F(M, IR, EF, FR)                                                                     \
+  {                                                                                                \
+    using ZL = ColTile<M, 6>;                                                                      \
+    using EI = FastFFT<M, 24, ZL, SRK_UNPAREN IR>;                                                 \
+    t[KK_Z_NS3] = KEntry{(const void*)(k_zpass_ns3f<M, ZL, EI, EF, SRK_UNPAREN FR>), M / 4, 6,      \
+                         (int)(ZL::SIZE * 16)};                                                    \
   }

@@ -183,6 +183,8 @@ int need_ws(srk_plan* p) {
 
 // ---- strided pass launch -------------------------------------------------
 int launch_col(srk_plan* p, int kind, PassArgs a, cudaStream_t st) {
+  const bool padded_kind = kind == KK_INV_P || kind == KK_FWD_P || kind == KK_INV_RHS || kind >= KK_INV_RHS_SLAB;
+  if (padded_kind && 3 * a.n != 2 * a.M) return fail(SRK_ERR_INVALID, "padded pass needs M = 3n/2");
   KEntry e;
   int rc = get_entry(kind, a.M, e, a.gp);
   if (rc) return rc;
@@ -287,12 +289,12 @@ int inverse_chain(srk_plan* p, const cplx* spec, int c, double* phys, bool pad, 
   const double scale = (pad ? std::pow(1.5, p->dims) : 1.0) / ((double)M0 * M1 * M2);
   PassArgs a = x_pass(p, spec, p->A, c, p->n0, M0, M0, p->n0);
   a.scale = scale;
-  int rc = launch_col(p, KK_INV, a, st);
+  int rc = launch_col(p, pad ? KK_INV_P : KK_INV, a, st);
   if (rc) return rc;
   const cplx* zin = p->A;
   if (p->dims == 3) {
     PassArgs b = y_pass(p, p->A, p->B, c, M0, p->n1, M1, M1, p->n1);
-    if ((rc = launch_col(p, KK_INV, b, st))) return rc;
+    if ((rc = launch_col(p, pad ? KK_INV_P : KK_INV, b, st))) return rc;
     zin = p->B;
   }
   const int P = M0 * M1;
@@ -327,14 +329,14 @@ int forward_chain(srk_plan* p, const double* phys, int c, cplx* spec, bool trunc
   if (p->dims == 3) {
     PassArgs b = y_pass(p, p->A, p->B, c, M0, M1, p->n1, M1, p->n1);
     b.zero_nyq = trunc ? 1 : 0;
-    if ((rc = launch_col(p, KK_FWD, b, st))) return rc;
+    if ((rc = launch_col(p, trunc ? KK_FWD_P : KK_FWD, b, st))) return rc;
     xin = p->B;
   }
   PassArgs a = x_pass(p, xin, spec, c, M0, p->n0, M0, p->n0);
   a.scale = trunc ? std::pow(1.0 / 1.5, p->dims) : 1.0;
   a.zero_nyq = trunc ? 1 : 0;
   a.zero_dc_imag = trunc ? 1 : 0;
-  return launch_col(p, KK_FWD, a, st);
+  return launch_col(p, trunc ? KK_FWD_P : KK_FWD, a, st);
 }
 
 }  // namespace
@@ -492,7 +494,7 @@ int srk_rhs(srk_plan* p, const void* y_, void* f_, double nu, double ri, double 
   if (d == 3) {
     // K2: y pad + inverse y
     PassArgs b = y_pass(p, p->A, p->B, p->S, p->m0, p->n1, p->m1, p->m1, p->n1);
-    if ((rc = launch_col(p, KK_INV, b, st))) return rc;
+    if ((rc = launch_col(p, KK_INV_P, b, st))) return rc;
     zin = p->B;
     zout = p->A;
   }
@@ -512,7 +514,7 @@ int srk_rhs(srk_plan* p, const void* y_, void* f_, double nu, double ri, double 
     // K4: forward y + truncate
     PassArgs b = y_pass(p, p->A, p->B, p->So, p->m0, p->m1, p->n1, p->m1, p->n1);
     b.zero_nyq = 1;
-    if ((rc = launch_col(p, KK_FWD, b, st))) return rc;
+    if ((rc = launch_col(p, KK_FWD_P, b, st))) return rc;
     xin = p->B;
   }
   // K5: forward x + truncate + 1/1.5^d + Nyquist / DC-imag zeroing -> G
@@ -520,7 +522,7 @@ int srk_rhs(srk_plan* p, const void* y_, void* f_, double nu, double ri, double 
   c5.scale = std::pow(1.0 / 1.5, d);
   c5.zero_nyq = 1;
   c5.zero_dc_imag = 1;
-  if ((rc = launch_col(p, KK_FWD, c5, st))) return rc;
+  if ((rc = launch_col(p, KK_FWD_P, c5, st))) return rc;
   // K6: projection + viscous (+ Boussinesq terms)
   ProjArgs pa;
   pa.g = geom(p);
@@ -731,7 +733,7 @@ int srk_slab_forward(srk_plan* p, const void* y, void* send1, void* stream) {
   a.comp_stride = p->modes;
   a.y0 = p->y0;
   a.n1g = p->n1g;
-  return launch_col(p, KK_INV_RHS, a, st);
+  return launch_col(p, KK_INV_RHS_SLAB, a, st);
 }
 
 int srk_slab_middle(srk_plan* p, const void* recv1, void* send2, void* stream) {
@@ -753,7 +755,7 @@ int srk_slab_middle(srk_plan* p, const void* recv1, void* send2, void* stream) {
   b.out_plane_stride = m1 * K;
   b.in_rpb = (int)Ny;
   b.in_bstride = (long long)p->S * Mx * Ny * K;
-  if ((rc = launch_col(p, KK_INV, b, st))) return rc;
+  if ((rc = launch_col(p, KK_INV_P_SLAB, b, st))) return rc;
   // K3: z pencils of the x-slab
   const int P = (int)(Mx * m1);
   ZArgs z = z_args(p, p->m2, p->n2, P);
@@ -777,7 +779,7 @@ int srk_slab_middle(srk_plan* p, const void* recv1, void* send2, void* stream) {
   c.out_rpb = (int)Ny;
   c.out_bstride = (long long)p->So * Mx * Ny * K;
   c.zero_nyq = 1;
-  return launch_col(p, KK_FWD, c, st);
+  return launch_col(p, KK_FWD_P_SLABO, c, st);
 }
 
 int srk_slab_finish(srk_plan* p, const void* recv2, const void* y, void* f, double nu, double ri, double re_pr,
@@ -795,7 +797,7 @@ int srk_slab_finish(srk_plan* p, const void* recv2, const void* y, void* f, doub
   c5.zero_nyq = 1;
   c5.zero_dc_imag = 1;
   c5.y0 = p->y0;
-  if ((rc = launch_col(p, KK_FWD, c5, st))) return rc;
+  if ((rc = launch_col(p, KK_FWD_P_SLABI, c5, st))) return rc;
   ProjArgs pa;
   pa.g = geom(p);
   pa.G = p->A;
