@@ -141,6 +141,27 @@ def ics(srk):
     return out
 
 
+def io_cases(srk):
+    """SRKL checkpoint + diagnostics CSV written by the reference driver, and an
+    energy spectrum (simulation.py:371-516, diagnostics.py:73-91)."""
+    import tempfile
+
+    out = {}
+    with tempfile.TemporaryDirectory() as td:
+        spec = srk.ProblemSpec(kind="taylor_green", params=srk.PhysParams(reynolds=100.0), seed=7)
+        c = srk.RunConfig(grid_shape=(16, 16), problem=spec, integrator="dp5", mode="fixed", t_end=0.5, h=0.1,
+                          output_dir=td, checkpoint_interval=0.2)
+        srk.run_simulation(c)
+        for name in ("final.srkl", "checkpoint_t0.200000.srkl", "diagnostics.csv"):
+            with open(os.path.join(td, name), "rb") as fh:
+                out[name.replace(".", "_")] = np.frombuffer(fh.read(), dtype=np.uint8)
+    g = srk.Grid((16, 16, 16))
+    u = srk.hit_init(g, srk.ProblemSpec(kind="hit", a=4.0, energy=0.5, seed=42)).fields
+    sp = srk.energy_spectrum(u, g)
+    out["spectrum_hit16_E"] = sp.E
+    return out
+
+
 def _save(name, dct):
     flat = {}
     for case, vals in dct.items():
@@ -161,6 +182,7 @@ def main():
     _save("dealias_cases.npz", dealias_cases(srk))
     _save("ics.npz", ics(srk))
     _save("trajectories.npz", trajectories(srk))
+    _save("io_cases.npz", io_cases(srk))
     man = dict(reference="spectralrk " + srk.__version__, numpy=np.__version__,
                scipy=scipy.__version__, generator="oracle/make_golden.py")
     with open(os.path.join(OUT, "MANIFEST.json"), "w") as fh:

@@ -17,10 +17,14 @@ from .integrators import (ButcherPair, NonFiniteStateError, StepOutcome, ab2_com
                           make_kcl5, make_pair, make_rk4, rk_step)
 from .control import (AdvanceOutcome, ControllerConfig, ControllerState, StepSizeUnderflowError,
                       adaptive_advance, error_norm, error_norm_delta, propose_step, scale_vector)
-from .diagnostics import DiagnosticsRecord, dissipation_rate, enstrophy, kinetic_energy
+from .diagnostics import (DiagnosticsRecord, SpectrumRecord, compare_series, dissipation_rate, energy_spectrum,
+                          enstrophy, field_error_norms, kinetic_energy)
 from .problems import ProblemSpec, hit_init, rayleigh_taylor_init, taylor_green_init
 from .simulation import (ADAPTIVE_CAPABLE, INTEGRATORS, ConfigError, RunConfig, SimulationResult,
                          default_lengths, make_initial_state, run_simulation)
+from .checkpoint import (CheckpointData, CheckpointError, read_checkpoint, read_diagnostics_csv,
+                         write_checkpoint, write_diagnostics_csv)
+from .workprec import WorkPrecisionPoint, cell_config, work_precision, write_work_precision_csv
 from . import _native
 
 __version__ = "0.1.0"

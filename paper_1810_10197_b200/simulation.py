@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import warnings
 from dataclasses import dataclass, field
+from pathlib import Path
 
 import numpy as np
 import torch
@@ -23,6 +24,7 @@ from .integrators import NonFiniteStateError, make_pair, make_rk4, run_stages
 from .physics import FlowRHS, FlowState, apply_forcing
 from .problems import ProblemSpec, hit_init, rayleigh_taylor_init, taylor_green_init
 from .spectral import to_device
+from .checkpoint import CheckpointData, CheckpointError, write_checkpoint, write_diagnostics_csv
 
 __all__ = ["RunConfig", "ConfigError", "default_lengths", "make_initial_state", "SimulationResult",
            "run_simulation", "INTEGRATORS", "ADAPTIVE_CAPABLE"]
@@ -121,35 +123,94 @@ class SimulationResult:
     errs: list = field(default_factory=list)
 
 
-class _Driver:
-    """simulation.py:93-219 (device tensors; checkpointing out of scope)."""
+def _rng_state_tuple(rng):
+    st = rng.bit_generator.state["state"]
+    return (st["state"], st["inc"])
 
-    def __init__(self, config, initial_state=None):
+
+def _rng_from_tuple(tup):
+    rng = np.random.default_rng()
+    state = rng.bit_generator.state
+    state["state"]["state"], state["state"]["inc"] = tup
+    rng.bit_generator.state = state
+    return rng
+
+
+class _Driver:
+    """simulation.py:93-219 on device tensors (cached tendency, FSAL, accounting,
+    resume, periodic SRKL checkpoints)."""
+
+    def __init__(self, config, initial_state=None, resume=None):
         self.config = config
-        if initial_state is None:
-            st = make_initial_state(config)
-        elif callable(initial_state):
-            st = initial_state(config)
+        if resume is not None:
+            if tuple(resume.grid.shape) != tuple(config.grid_shape):
+                raise CheckpointError(f"checkpoint grid {resume.grid.shape} does not match configured grid "
+                                      f"{tuple(config.grid_shape)}")
+            if resume.has_density != config.has_density:
+                raise CheckpointError("checkpoint and configuration disagree on the presence of a density field")
+            self.grid = resume.grid
+            self.y = to_device(resume.fields, torch.complex128)[0].clone()
+            self.t = resume.time
+            self.evals = resume.rhs_evals
+            self.rejections = resume.rejections
+            self.steps = resume.steps
+            self.f_now = None if resume.f_now is None else to_device(resume.f_now, torch.complex128)[0].clone()
+            self.prev_rejected = resume.prev_rejected
+            self.h_ctrl = resume.h
+            self.rng = (_rng_from_tuple(resume.rng_state) if resume.rng_state is not None
+                        else np.random.default_rng(config.problem.seed))
         else:
-            st = initial_state
-        if isinstance(st, FlowState):
-            self.grid, y = st.grid, st.fields
-        else:
-            lengths = config.lengths or default_lengths(config.problem.kind, config.grid_shape)
-            self.grid, y = Grid(config.grid_shape, lengths), st
-        self.y = to_device(y, torch.complex128)[0].clone()
-        self.t = 0.0
-        self.evals = 0
-        self.rejections = 0
-        self.steps = 0
-        self.h_ctrl = config.h if config.mode == "fixed" else config.h0
-        self.prev_rejected = False
+            if initial_state is None:
+                st = make_initial_state(config)
+            elif callable(initial_state):
+                st = initial_state(config)
+            else:
+                st = initial_state
+            if isinstance(st, FlowState):
+                self.grid, y = st.grid, st.fields
+            else:
+                lengths = config.lengths or default_lengths(config.problem.kind, config.grid_shape)
+                self.grid, y = Grid(config.grid_shape, lengths), st
+            self.y = to_device(y, torch.complex128)[0].clone()
+            self.t = 0.0
+            self.evals = 0
+            self.rejections = 0
+            self.steps = 0
+            self.f_now = None
+            self.h_ctrl = config.h if config.mode == "fixed" else config.h0
+            self.prev_rejected = False
+            self.rng = np.random.default_rng(config.problem.seed)
         self.rhs = FlowRHS(self.grid, config.problem.params, density=config.has_density)
-        self.f_now = self.rhs(self.t, self.y)
-        self.evals += 1
+        if self.f_now is None:
+            self.f_now = self.rhs(self.t, self.y)
+            self.evals += 1
         self.records = []
         self.errs = []
-        self._pending = None  # device sums for the next record
+        out_dir = getattr(config, "output_dir", None)
+        self.out_dir = Path(out_dir) if out_dir else None
+        if self.out_dir is not None:
+            self.out_dir.mkdir(parents=True, exist_ok=True)
+        interval = getattr(config, "checkpoint_interval", None)
+        self._next_checkpoint = None
+        if interval is not None and self.out_dir is not None:
+            self._next_checkpoint = (int(np.floor(self.t / interval + 1e-9)) + 1) * interval
+
+    def maybe_checkpoint(self):
+        """simulation.py:184-191."""
+        if self._next_checkpoint is None:
+            return
+        if self.t + 1e-12 >= self._next_checkpoint:
+            write_checkpoint(self.out_dir / f"checkpoint_t{self.t:.6f}.srkl", self.snapshot())
+            while self._next_checkpoint <= self.t + 1e-12:
+                self._next_checkpoint += self.config.checkpoint_interval
+
+    def snapshot(self) -> CheckpointData:
+        cfg = self.config
+        return CheckpointData(grid=self.grid, fields=self.y, has_density=cfg.has_density, time=self.t,
+                              h=self.h_ctrl, prev_rejected=self.prev_rejected, rhs_evals=self.evals,
+                              rejections=self.rejections, steps=self.steps, f_now=self.f_now,
+                              rng_state=_rng_state_tuple(self.rng), forcing=cfg.forcing, k_f=cfg.k_f,
+                              forcing_energy=cfg.problem.energy)
 
     def record(self, h, sums=None):
         d = self.grid.dims
@@ -222,6 +283,7 @@ def _run_fixed(drv, max_steps=None):
         drv.t = time_at(i)
         drv.after_accept(stages[-1] if pair.fsal else None, fsal_ok=pair.fsal)
         drv.record(h_i)
+        drv.maybe_checkpoint()
 
 
 def _run_ab2(drv, h, t_end, max_steps=None):
@@ -241,6 +303,7 @@ def _run_ab2(drv, h, t_end, max_steps=None):
     drv.t = time_at(0)
     drv.after_accept(None, fsal_ok=False)
     drv.record(h0)
+    drv.maybe_checkpoint()
     for i in range(1, total):
         h_i = h if i < n_full else h_last
         if h_i != h:
@@ -253,6 +316,7 @@ def _run_ab2(drv, h, t_end, max_steps=None):
         drv.t = time_at(i)
         drv.after_accept(None, fsal_ok=False)
         drv.record(h_i)
+        drv.maybe_checkpoint()
 
 
 def _run_adaptive(drv, max_steps=None):
@@ -286,22 +350,26 @@ def _run_adaptive(drv, max_steps=None):
         drv.errs.append(out.errs)
         fsal_used = drv.after_accept(out.last_stage, fsal_ok=pair.fsal)
         drv.record(out.h_used, sums=out.diag_sums if fsal_used else None)
+        drv.maybe_checkpoint()
         n += 1
 
 
 def run_simulation(config, resume=None, initial_state=None, max_steps=None):
     """simulation.py:350-368 on the device.
 
+    ``resume``: CheckpointData (read_checkpoint) continuing a run bit-exactly.
     ``initial_state``: optional FlowState / array / callable(config) replacing
     make_initial_state (IC hook).  ``max_steps``: accepted-step cap
-    (SURVEY D6).  Checkpoint/resume and CSV output are out of scope this round.
+    (SURVEY D6).  With ``config.output_dir`` the diagnostics CSV, periodic and
+    final SRKL checkpoints are written like the reference.
     """
-    if resume is not None:
-        raise NotImplementedError("checkpoint resume is not part of the device path yet")
     config.validate()
-    drv = _Driver(config, initial_state)
+    drv = _Driver(config, initial_state, resume)
     if config.mode == "fixed":
         _run_fixed(drv, max_steps)
     else:
         _run_adaptive(drv, max_steps)
+    if drv.out_dir is not None:
+        write_diagnostics_csv(drv.records, drv.out_dir / "diagnostics.csv")
+        write_checkpoint(drv.out_dir / "final.srkl", drv.snapshot())
     return drv.result()

@@ -355,3 +355,65 @@ def test_slab_reduction_partials_sum_to_global():
         tot += np.array(reduce_sums(g, scatter_slab(y, r, P), flags=2, ncomp=3, plan=b.h).tolist())
     full = np.array(reduce_sums(g, y, flags=2, ncomp=3).tolist())
     np.testing.assert_allclose(tot[[4, 8]], full[[4, 8]], rtol=1e-13)
+
+
+def _tg2d(integ="rk4", mode="fixed", t_end=1.0, **kw):
+    spec = srk.ProblemSpec(kind="taylor_green", params=srk.PhysParams(100.0), seed=7)
+    c = srk.RunConfig(grid_shape=(16, 16), problem=spec, integrator=integ, mode=mode, t_end=t_end, **kw)
+    return c
+
+
+@pytest.mark.parametrize("integ,setting", [("rk4", dict(h=0.05)), ("dp5", dict(h=0.05))])
+def test_fixed_restart_bit_exact(integ, setting, tmp_path):
+    """test_simulation.py:312-326 on the device path."""
+    full = srk.run_simulation(_tg2d(integ, **setting))
+    srk.run_simulation(_tg2d(integ, t_end=0.5, output_dir=str(tmp_path / "leg1"), checkpoint_interval=0.5,
+                             **setting))
+    snap = srk.read_checkpoint(tmp_path / "leg1" / "final.srkl")
+    res = srk.run_simulation(_tg2d(integ, **setting), resume=snap)
+    assert torch.equal(full.state.fields, res.state.fields)
+    assert res.rhs_evals == full.rhs_evals and res.t == full.t
+    assert [r.t for r in res.records] == [r.t for r in full.records][10:]
+
+
+def test_adaptive_restart_bit_exact(tmp_path):
+    """test_simulation.py:327-348 on the device path."""
+    out = tmp_path / "run"
+    kw = dict(tol_abs=1e-7, tol_rel=1e-7, h0=0.01)
+    full = srk.run_simulation(_tg2d("bs5", "adaptive", output_dir=str(out), checkpoint_interval=0.25, **kw))
+    snap = srk.read_checkpoint(sorted(out.glob("checkpoint_*.srkl"))[0])
+    assert 0.25 <= snap.time < full.t
+    res = srk.run_simulation(_tg2d("bs5", "adaptive", **kw), resume=snap)
+    assert torch.equal(full.state.fields, res.state.fields)
+    assert res.rhs_evals == full.rhs_evals and res.rejections == full.rejections
+
+
+def test_resume_from_reference_checkpoint(tmp_path):
+    """A checkpoint written by the reference CPU driver resumes on the GPU path."""
+    io = load_golden("io_cases")
+    p = tmp_path / "ref.srkl"
+    p.write_bytes(io["final_srkl"].tobytes())
+    snap = srk.read_checkpoint(p)
+    mine = srk.run_simulation(_tg2d("dp5", h=0.1, t_end=0.5))
+    assert rel(mine.state.fields, snap.fields) <= 1e-12
+    a = srk.run_simulation(_tg2d("dp5", h=0.1, t_end=1.0), resume=snap)
+    b = srk.run_simulation(_tg2d("dp5", h=0.1, t_end=1.0))
+    assert rel(a.state.fields, b.state.fields) <= 1e-12 and a.rhs_evals == b.rhs_evals
+
+
+def test_energy_spectrum_vs_reference():
+    io = load_golden("io_cases")
+    g = srk.Grid((16, 16, 16))
+    u = srk.hit_init(g, srk.ProblemSpec("hit", a=4.0, energy=0.5, seed=42)).fields
+    sp = srk.energy_spectrum(u, g)
+    np.testing.assert_allclose(sp.E, io["spectrum_hit16_E"], rtol=1e-12, atol=1e-300)
+    assert abs(sp.E.sum() - 0.5) < 1e-13
+
+
+def test_work_precision_sweep_small():
+    base = _tg2d("rk4", h=0.01, t_end=0.2)
+    ref = _tg2d("rk4", h=0.001, t_end=0.2).validate()
+    cells = [srk.cell_config(base, "rk4", "fixed", 0.02), srk.cell_config(base, "bs5", "adaptive", 1e-6)]
+    pts, _ = srk.work_precision(cells, ref)
+    assert len(pts) == 4 and all(p.status == "ok" and np.isfinite(p.error) for p in pts)
+    assert {p.rhs_evals for p in pts if p.integrator == "rk4"} == {10 * 4 + 1}
