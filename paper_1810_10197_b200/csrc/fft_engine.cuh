@@ -55,10 +55,11 @@ struct RowTile {
   SRK_DEV static int tj_of(int tid, int) { return tid / C_; }
 };
 
-template <int M_, int C_>
+template <int M_, int C_, int MINPITCH = 0>
 struct ColTile {
   static constexpr int M = M_, C = C_;
-  static constexpr int PITCH = M_ + (M_ + 7) / 8 + 1;
+  static constexpr int PITCH0 = M_ + (M_ + 7) / 8 + 1;
+  static constexpr int PITCH = PITCH0 > MINPITCH ? PITCH0 : MINPITCH;
   static constexpr int SIZE = PITCH * C_;
   static constexpr int STEP8 = 9;
   static constexpr int ROWSTEP = 1;

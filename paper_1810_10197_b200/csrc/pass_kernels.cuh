@@ -84,7 +84,7 @@ __device__ __forceinline__ void stage_rows(cplx* dst, const cplx* __restrict__ s
 enum PassFlags { PF_CTN = 1, PF_BIN = 2, PF_BOUT = 4 };
 
 template <class Eng, int KIND, int SIGN, int FL = 0>
-__global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : (Eng::NT <= 256 ? 2 : 1))) k_colpass(const PassArgs a) {
+__global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(const PassArgs a) {
   extern __shared__ __align__(16) cplx sm[];
   constexpr int C = Eng::C;
   constexpr bool CTN = (FL & PF_CTN) && Eng::kFast;
@@ -229,6 +229,7 @@ struct ZArgs {
   int So; // output real signals per pencil
   long long in_sig_stride, out_sig_stride;  // complex elements (P*K) or real (P*M)
   int zero_nyq;  // R2C: zero the kz = n/2 plane (narrow)
+  int mode;      // NS3 fused z-pass experiment switch (0 = prefetch in the forward half)
 };
 
 template <int OP>
@@ -262,7 +263,7 @@ SRK_DEV void zphys(const double* r, double* o) {
 // Eng runs the inverse transforms (S complex columns); EngF the forward ones
 // (So columns) -- a different plan when So < S so all threads stay busy.
 template <class Eng, class L, int OP, class EngF = Eng>
-__global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 224 ? 2 : 1)) k_zpass(const ZArgs a, int S_rt, int So_rt) {
+__global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 192 ? 2 : 1)) k_zpass(const ZArgs a, int S_rt, int So_rt) {
   extern __shared__ __align__(16) cplx sm[];
   const int p0 = 2 * blockIdx.x;
   const int S = (OP >= ZOP_NS3) ? ZSig<OP>::S : S_rt;

@@ -181,7 +181,9 @@ __global__ void __launch_bounds__(256) k_reduce(const RedArgs a) {
         z = DADD(z, DMUL(DMUL(w, k2), DADD(DMUL(y1.x, y1.x), DMUL(y1.y, y1.y))));
       }
     }
-    if (c < 4) acc[c] = r2;
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc)
+      if (cc == c) acc[cc] = r2;  // static indices only (no local-memory array)
     acc[4] += e;
     acc[5] += ep;
     acc[6] += bad;

@@ -29,6 +29,7 @@ struct KEntry {
   int nt;    // threads per block
   int cols;  // columns per block (strided) / complex columns capacity (z)
   int smem;  // dynamic shared memory bytes
+  int persistent = 0;  // z pass: grid-stride over pencil pairs (grid = resident CTAs)
 };
 
 // plain z ops process up to this many real signals per pencil per launch
@@ -125,10 +126,11 @@ struct GenCols {
 
 // NS3 z-pass with the fused middle stage: inverse prefix (IR..., product M/4),
 // forward suffix (FR..., product M/4), E = 24.
+// Pitch >= 4K so that tile columns 3..5 hold the 12 staged rows of K modes.
 #define SRK_NS3F(M, IR, EF, FR)                                                                     \
   {                                                                                                \
-    using ZL = ColTile<M, 6>;                                                                      \
+    using ZL = ColTile<M, 6>;                                                                           \
     using EI = FastFFT<M, 24, ZL, SRK_UNPAREN IR>;                                                 \
     t[KK_Z_NS3] = KEntry{(const void*)(k_zpass_ns3f<M, ZL, EI, EF, SRK_UNPAREN FR>), M / 4, 6,      \
-                         (int)(ZL::SIZE * 16)};                                                    \
+                         (int)(ZL::SIZE * 16), 0};                                                 \
   }

@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -112,6 +113,7 @@ int ensure_smem(const KEntry& e) {
   if (it != g_smem_set.end()) return SRK_OK;
   cudaError_t err = cudaFuncSetAttribute(e.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, e.smem);
   if (err != cudaSuccess) return fail(SRK_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(err));
+
   g_smem_set[e.fn] = 1;
   return SRK_OK;
 }
@@ -208,7 +210,15 @@ int launch_z(srk_plan* p, int kind, ZArgs a, int S_rt, int So_rt, cudaStream_t s
   if (rc) return rc;
   if ((rc = get_tw(p, a.M, &a.tw))) return rc;
   if ((rc = ensure_smem(e))) return rc;
-  const int grid = (a.P + 1) / 2;
+  int grid = (a.P + 1) / 2;
+  if (e.persistent && !getenv("SRK_NOPERSIST")) {
+    int per_sm = 0, dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, e.fn, e.nt, e.smem);
+    if (getenv("SRK_DEBUG")) fprintf(stderr, "srk: persistent z-pass %d CTAs/SM x %d SMs\n", per_sm, nsm);
+    grid = std::min(grid, std::max(1, per_sm) * nsm);
+  }
   void* args[] = {&a, &S_rt, &So_rt};
   cudaError_t err = cudaLaunchKernel(e.fn, dim3(grid), dim3(e.nt), args, e.smem, st);
   if (err != cudaSuccess) return fail(SRK_ERR_CUDA, std::string("zpass launch: ") + cudaGetErrorString(err));
@@ -506,6 +516,7 @@ int srk_rhs(srk_plan* p, const void* y_, void* f_, double nu, double ri, double 
   z.in_sig_stride = (long long)P * p->K;
   z.out_sig_stride = (long long)P * p->K;
   z.zero_nyq = 1;
+  z.mode = getenv("SRK_ZMODE") ? atoi(getenv("SRK_ZMODE")) : 0;
   const int kind = d == 3 ? (p->density ? KK_Z_B3 : KK_Z_NS3) : (p->density ? KK_Z_B2 : KK_Z_NS2);
   if ((rc = launch_z(p, kind, z, 0, 0, st))) return rc;
   const cplx* xin = zout;
