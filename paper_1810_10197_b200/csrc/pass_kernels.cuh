@@ -18,7 +18,13 @@
 
 #include "fft_engine.cuh"
 
-enum PassKind { PK_INV = 0, PK_INV_RHS = 1, PK_FWD = 2 };
+enum PassKind {
+  PK_INV = 0,      // plain padded / unpadded inverse
+  PK_INV_RHS = 1,  // x inverse with the full curl on load (2D K1)
+  PK_FWD = 2,      // forward + truncation
+  PK_INV_KX = 3,   // 3D K1: x inverse of [u0, u1, u2, kx u1, kx u2, (rho)]
+  PK_INV_CURLY = 4 // 3D K2: y inverse of [u, w, (rho)], w = i k x u formed on load from the K1 signals
+};
 enum ZOp { ZOP_C2R = 0, ZOP_R2C = 1, ZOP_NS3 = 2, ZOP_NS2 = 3, ZOP_B3 = 4, ZOP_B2 = 5 };
 
 // Strided-axis pass.  Global column g within a plane (plane = signal for the
@@ -54,6 +60,7 @@ struct PassArgs {
   int in_rpb, out_rpb;
   long long in_bstride, out_bstride;
   int y0, n1g;
+  int xplanes;  // PK_INV_CURLY: x planes per signal (m0, or m0/P on a slab)
 };
 
 SRK_DEV unsigned row_off(int row, unsigned rs, int rpb, long long bstride) {
@@ -181,6 +188,73 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
       cplx v = is_curl ? cmk(-df.y, df.x) : ua;
       const double f = ok ? sc : 0.0;
       return cmk(v.x * f, v.y * f);
+    };
+    auto st = [&](int row, int col, cplx v) { outp[row_off(row, rs, out_rpb, a.out_bstride) + (unsigned)col] = v; };
+    Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, a.tw, ncols, ld, st);
+  } else if constexpr (KIND == PK_INV_KX) {
+    // 3D K1.  k_y and k_z are constant along x, so the x inverse commutes with
+    // them: only k_x u1 and k_x u2 need their own transforms; the curl is
+    // completed in K2 (PK_INV_CURLY).  plane = signal s of
+    // [u0, u1, u2, kx*u1, kx*u2, rho]; one component staged per CTA.
+    const int s = plane;
+    const int comp = (s < 3) ? s : (s == 3 ? 1 : (s == 4 ? 2 : 3));
+    const bool use_kx = (s == 3 || s == 4);
+    const cplx* __restrict__ pa = a.in + w0 + comp * a.comp_stride;
+    const double sc = a.scale;
+    if constexpr (Eng::kFast) {
+      stage_rows<C>(sm, pa, n, rs, ncols, in_rpb, a.in_bstride);
+      cp_async_wait_all();
+      __syncthreads();
+    }
+    auto ld = [&](int row, int col) -> cplx {
+      const int cr = pad_src(row, n, M);
+      const bool ok = cr >= 0;
+      const int r = ok ? cr : 0;
+      const cplx u = Eng::kFast ? sm[r * C + col] : pa[row_off(r, rs, in_rpb, a.in_bstride) + (unsigned)col];
+      const double kx = mode_full(r, n) * a.ck0;
+      const double f = ok ? (use_kx ? kx * sc : sc) : 0.0;
+      return cmk(u.x * f, u.y * f);
+    };
+    auto st = [&](int row, int col, cplx v) { outp[row_off(row, rs, out_rpb, a.out_bstride) + (unsigned)col] = v; };
+    Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, a.tw, ncols, ld, st);
+  } else if constexpr (KIND == PK_INV_CURLY) {
+    // 3D K2.  plane = (s, x), s over [u0, u1, u2, w0, w1, w2, (rho)]; the input
+    // planes are the K1 signals [U0, U1, U2, X1 = F(kx u1), X2 = F(kx u2), R]:
+    //   w0 = i (ky U2 - kz U1),  w1 = i (kz U0 - X2),  w2 = i (X1 - ky U0)
+    // (spectral.py:47-65 after the x transform; ky varies along this pass's
+    // rows, kz along its columns).
+    const int X = a.xplanes;
+    const int s = plane / X, x = plane - (plane / X) * X;
+    int ca = s, cb = s, fa_ky = 0, fa_kz = 0, fb_ky = 0, fb_kz = 0;
+    bool is_curl = false;
+    if (s == 3) { ca = 2; fa_ky = 1; cb = 1; fb_kz = 1; is_curl = true; }
+    else if (s == 4) { ca = 0; fa_kz = 1; cb = 4; is_curl = true; }
+    else if (s == 5) { ca = 3; cb = 0; fb_ky = 1; is_curl = true; }
+    else if (s == 6) { ca = cb = 5; }
+    const cplx* __restrict__ pa = a.in + (long long)(ca * X + x) * a.in_plane_stride + w0;
+    const cplx* __restrict__ pb = a.in + (long long)(cb * X + x) * a.in_plane_stride + w0;
+    const int mycol = Eng::col_of(threadIdx.x);
+    const double kz = (double)(w0 + mycol) * a.ck2;
+    cplx* sb_ = sm + (is_curl ? n * C : 0);
+    if constexpr (Eng::kFast) {
+      stage_rows<C>(sm, pa, n, rs, ncols, in_rpb, a.in_bstride);
+      if (is_curl) stage_rows<C>(sm + n * C, pb, n, rs, ncols, in_rpb, a.in_bstride);
+      cp_async_wait_all();
+      __syncthreads();
+    }
+    auto ld = [&](int row, int col) -> cplx {
+      const int cr = pad_src(row, n, M);
+      const bool ok = cr >= 0;
+      const int r = ok ? cr : 0;
+      const unsigned off = row_off(r, rs, in_rpb, a.in_bstride) + (unsigned)col;
+      const cplx A = Eng::kFast ? sm[r * C + col] : pa[off];
+      const cplx B = Eng::kFast ? sb_[r * C + col] : pb[off];
+      const double ky = mode_full(r, n) * a.ck1;
+      const double fa = fa_ky ? ky : (fa_kz ? kz : 1.0);
+      const double fb = fb_ky ? ky : (fb_kz ? kz : 1.0);
+      const cplx df = csub(cscale(A, fa), cscale(B, fb));
+      cplx v = is_curl ? cmk(-df.y, df.x) : A;
+      return ok ? v : cmk(0.0, 0.0);
     };
     auto st = [&](int row, int col, cplx v) { outp[row_off(row, rs, out_rpb, a.out_bstride) + (unsigned)col] = v; };
     Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, a.tw, ncols, ld, st);

@@ -21,7 +21,11 @@ enum KernelKind {
   KK_INV_P_SLAB = 12,    // K2, blocked input rows (all-to-all #1 receive)
   KK_FWD_P_SLABO = 13,   // K4, blocked output rows (all-to-all #2 send)
   KK_FWD_P_SLABI = 14,   // K5, blocked input rows (all-to-all #2 receive)
-  KK_COUNT = 15
+  KK_INV_KX = 15,        // 3D K1 (u, kx u signals)
+  KK_INV_KX_SLAB = 16,   // 3D K1, all-to-all #1 send layout
+  KK_INV_CURLY = 17,     // 3D K2 (curl completed on load)
+  KK_INV_CURLY_SLAB = 18,  // 3D K2 from the all-to-all #1 receive layout
+  KK_COUNT = 19
 };
 
 struct KEntry {
@@ -59,7 +63,12 @@ struct GenCols {
                                    SRK_RHS_SMEM(M, CS));                                           \
     t[KK_INV_P_SLAB] = SRK_ENTRY((k_colpass<SE, PK_INV, +1, PF_CTN | PF_BIN>), SE, SL::SIZE * 16); \
     t[KK_FWD_P_SLABO] = SRK_ENTRY((k_colpass<SE, PK_FWD, -1, PF_CTN | PF_BOUT>), SE, SL::SIZE * 16); \
-    t[KK_FWD_P_SLABI] = SRK_ENTRY((k_colpass<SE, PK_FWD, -1, PF_CTN | PF_BIN>), SE, SL::SIZE * 16);
+    t[KK_FWD_P_SLABI] = SRK_ENTRY((k_colpass<SE, PK_FWD, -1, PF_CTN | PF_BIN>), SE, SL::SIZE * 16); \
+    t[KK_INV_KX] = SRK_ENTRY((k_colpass<SE, PK_INV_KX, +1, PF_CTN>), SE, SL::SIZE * 16);           \
+    t[KK_INV_KX_SLAB] = SRK_ENTRY((k_colpass<SE, PK_INV_KX, +1, PF_CTN | PF_BOUT>), SE, SL::SIZE * 16); \
+    t[KK_INV_CURLY] = SRK_ENTRY((k_colpass<SE, PK_INV_CURLY, +1, PF_CTN>), SE, SRK_RHS_SMEM(M, CS)); \
+    t[KK_INV_CURLY_SLAB] = SRK_ENTRY((k_colpass<SE, PK_INV_CURLY, +1, PF_CTN | PF_BIN>), SE,       \
+                                     SRK_RHS_SMEM(M, CS));
 
 // Instantiate every kernel kind for one fast FFT length.
 #define SRK_DEFINE_SIZE(NAME, M, E, CS, ...) SRK_DEFINE_SIZE_F(NAME, M, E, CS, E, (__VA_ARGS__), __VA_ARGS__)

@@ -135,6 +135,7 @@ struct srk_plan {
   double ck0, ck1, ck2;
   long long modes;  // n0*n1*K per component
   int S, So;        // rhs signal counts (widened, products)
+  int S1;           // 3D: K1 output signals [u0,u1,u2,kx u1,kx u2,(rho)]; 2D: S
   int nranks = 1, rank = 0;  // slab decomposition over y (3D only)
   int n1g = 0, y0 = 0, Mx = 0;
   std::map<int, cplx*> tw;
@@ -398,6 +399,7 @@ int srk_plan_create(srk_plan** out, int dims, const int64_t* shape, const double
   const int d = dims, wc = dims == 3 ? 3 : 1;
   p->S = d + wc + p->density;
   p->So = p->density ? 2 * d : d;
+  p->S1 = dims == 3 ? 5 + p->density : p->S;
   const int nstate = d + p->density;
   p->max_comps = std::max(max_comps, nstate);
   // every padded length must have a kernel
@@ -421,7 +423,7 @@ int srk_plan_create(srk_plan** out, int dims, const int64_t* shape, const double
   auto upA = [&](long long v) { A = std::max(A, v); };
   auto upB = [&](long long v) { B = std::max(B, v); };
   if (dims == 3) {
-    upA(p->S * m0 * n1 * K);   // K1 out
+    upA(p->S1 * m0 * n1 * K);  // K1 out
     upB(p->S * m0 * m1 * K);   // K2 out
     upA(p->So * m0 * m1 * K);  // K3 out
     upB(p->So * m0 * n1 * K);  // K4 out
@@ -486,8 +488,9 @@ int srk_rhs(srk_plan* p, const void* y_, void* f_, double nu, double ri, double 
   cplx* f = (cplx*)f_;
   p->last_launches = 0;
   const int d = p->dims;
-  // K1: curl + x pad + inverse x
-  PassArgs a = x_pass(p, y, p->A, p->S, p->n0, p->m0, p->m0, p->n0);
+  // K1: x pad + inverse x (3D: [u, kx u1, kx u2] -- the curl is completed in K2;
+  // 2D: curl on load)
+  PassArgs a = x_pass(p, y, p->A, p->S1, p->n0, p->m0, p->m0, p->n0);
   a.scale = std::pow(1.5, d) / ((double)p->m0 * p->m1 * p->m2);
   a.dims = d;
   a.n1 = p->n1;
@@ -498,13 +501,16 @@ int srk_rhs(srk_plan* p, const void* y_, void* f_, double nu, double ri, double 
   a.comp_stride = p->modes;
   a.y0 = p->y0;
   a.n1g = p->n1g;
-  if ((rc = launch_col(p, KK_INV_RHS, a, st))) return rc;
+  if ((rc = launch_col(p, d == 3 ? KK_INV_KX : KK_INV_RHS, a, st))) return rc;
   const cplx* zin = p->A;
   cplx* zout = p->B;
   if (d == 3) {
-    // K2: y pad + inverse y
+    // K2: curl completion + y pad + inverse y
     PassArgs b = y_pass(p, p->A, p->B, p->S, p->m0, p->n1, p->m1, p->m1, p->n1);
-    if ((rc = launch_col(p, KK_INV_P, b, st))) return rc;
+    b.xplanes = p->m0;
+    b.ck1 = p->ck1;
+    b.ck2 = p->ck2;
+    if ((rc = launch_col(p, KK_INV_CURLY, b, st))) return rc;
     zin = p->B;
     zout = p->A;
   }
@@ -695,7 +701,7 @@ int srk_plan_create_slab(srk_plan** out, const int64_t* shape, const double* len
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(SRK_ERR_INVALID, "bad rank / nranks");
   if (shape[1] % nranks || (3 * shape[0] / 2) % nranks)
     return fail(SRK_ERR_INVALID, "slab decomposition needs nranks | n1 and nranks | 3*n0/2");
-  int64_t loc[3] = {shape[0], shape[1] / nranks, shape[2]};
+  int64_t loc[3] = {shape[0], shape[1] / nranks, shape[2]};  // local y extent
   if (loc[1] < 1) return fail(SRK_ERR_INVALID, "too many ranks for n1");
   // create with the local y extent (workspace sizing is redone below)
   int64_t tmp[3] = {shape[0], shape[1], shape[2]};
@@ -712,6 +718,7 @@ int srk_plan_create_slab(srk_plan** out, const int64_t* shape, const double* len
   const long long K = p->K, Ny = p->n1, Mx = p->Mx, m1 = p->m1, n0 = p->n0;
   long long A = std::max<long long>(p->So * Mx * m1 * K, p->So * n0 * Ny * K);
   long long B = p->S * Mx * m1 * K;
+  (void)loc;
   p->A_elems = A;
   p->B_elems = B;
   p->need_bytes = align256(A * 16) + align256(std::max<long long>(B, 1) * 16);
@@ -720,7 +727,7 @@ int srk_plan_create_slab(srk_plan** out, const int64_t* shape, const double* len
 
 int srk_slab_sizes(const srk_plan* p, int64_t* send1, int64_t* send2) {
   if (!p) return fail(SRK_ERR_INVALID, "null plan");
-  *send1 = (int64_t)p->S * p->m0 * p->n1 * p->K;
+  *send1 = (int64_t)p->S1 * p->m0 * p->n1 * p->K;
   *send2 = (int64_t)p->So * p->Mx * p->n1g * p->K;
   return SRK_OK;
 }
@@ -729,8 +736,8 @@ int srk_slab_forward(srk_plan* p, const void* y, void* send1, void* stream) {
   if (!p || !p->Mx) return fail(SRK_ERR_INVALID, "not a slab plan");
   cudaStream_t st = (cudaStream_t)stream;
   const int d = p->dims;
-  const long long blk = (long long)p->S * p->Mx * p->n1 * p->K;
-  PassArgs a = x_pass(p, (const cplx*)y, (cplx*)send1, p->S, p->n0, p->m0, p->m0, p->n0);
+  const long long blk = (long long)p->S1 * p->Mx * p->n1 * p->K;
+  PassArgs a = x_pass(p, (const cplx*)y, (cplx*)send1, p->S1, p->n0, p->m0, p->m0, p->n0);
   a.out_plane_stride = (long long)p->Mx * p->n1 * p->K;
   a.out_rpb = p->Mx;
   a.out_bstride = blk;
@@ -744,7 +751,7 @@ int srk_slab_forward(srk_plan* p, const void* y, void* send1, void* stream) {
   a.comp_stride = p->modes;
   a.y0 = p->y0;
   a.n1g = p->n1g;
-  return launch_col(p, KK_INV_RHS_SLAB, a, st);
+  return launch_col(p, KK_INV_KX_SLAB, a, st);
 }
 
 int srk_slab_middle(srk_plan* p, const void* recv1, void* send2, void* stream) {
@@ -765,8 +772,11 @@ int srk_slab_middle(srk_plan* p, const void* recv1, void* send2, void* stream) {
   b.in_plane_stride = Ny * K;
   b.out_plane_stride = m1 * K;
   b.in_rpb = (int)Ny;
-  b.in_bstride = (long long)p->S * Mx * Ny * K;
-  if ((rc = launch_col(p, KK_INV_P_SLAB, b, st))) return rc;
+  b.in_bstride = (long long)p->S1 * Mx * Ny * K;
+  b.xplanes = p->Mx;
+  b.ck1 = p->ck1;
+  b.ck2 = p->ck2;
+  if ((rc = launch_col(p, KK_INV_CURLY_SLAB, b, st))) return rc;
   // K3: z pencils of the x-slab
   const int P = (int)(Mx * m1);
   ZArgs z = z_args(p, p->m2, p->n2, P);

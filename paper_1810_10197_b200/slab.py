@@ -3,14 +3,15 @@
 Rank r of P owns the y-slab ``(ncomp, n0, n1/P, n2/2+1)`` of the spectral
 state (global rows y in [r*n1/P, (r+1)*n1/P)).  One RHS evaluation:
 
-    K1 (x-inverse + curl, local)        -> send1 [dest][s][x_loc][y_loc][kz]
+    K1 (x-inverse of u, kx u1, kx u2)   -> send1 [dest][s][x_loc][y_loc][kz]  (5 signals)
     all-to-all #1 (equal splits)         -> recv1 [src][s][x_loc][y_loc][kz]  (x-slab)
-    K2 + K3 + K4 (y, z, y passes, local) -> send2 [dest][o][x_loc][y_loc][kz]
+    K2 (curl completed on load) + K3 + K4 -> send2 [dest][o][x_loc][y_loc][kz]
     all-to-all #2                        -> recv2 [src][o][x_loc][y_loc][kz]  (y-slab)
     K5 + K6 (x-forward + projection)     -> f (y-slab)
 
 The exchange happens after the x padding and before the y padding, so it moves
-9*S_x complex values per RHS instead of 9*S_xy.  The kernels write
+8*S_x complex values per RHS (5 K1 signals + 3 products; SURVEY §8e counts 9
+with the curl finished before the exchange) instead of 9*S_xy.  The kernels write
 the send layouts and read the receive layouts directly; there is no pack or
 unpack pass.  Reductions (error norm, E_kin, eps, Z, forcing band energy) are
 per-slab device sums, all-gathered and added in rank order so every rank takes
@@ -43,10 +44,11 @@ def slab_geometry(grid: Grid, nranks: int, density=False):
         raise ValueError(f"need nranks | n1 ({n1}) and nranks | 3*n0/2 ({m0})")
     K = n2 // 2 + 1
     S = 3 + 3 + (1 if density else 0)
+    S1 = 5 + (1 if density else 0)  # K1 signals [u0, u1, u2, kx u1, kx u2, (rho)]
     So = 6 if density else 3
     ny, mx = n1 // nranks, m0 // nranks
-    return dict(n0=n0, n1=n1, n2=n2, K=K, m0=m0, m1=3 * n1 // 2, m2=3 * n2 // 2, ny=ny, mx=mx, S=S, So=So,
-                send1=S * m0 * ny * K, send2=So * mx * n1 * K)
+    return dict(n0=n0, n1=n1, n2=n2, K=K, m0=m0, m1=3 * n1 // 2, m2=3 * n2 // 2, ny=ny, mx=mx, S=S, S1=S1,
+                So=So, send1=S1 * m0 * ny * K, send2=So * mx * n1 * K)
 
 
 def scatter_slab(y_full, rank, nranks):

@@ -26,6 +26,7 @@ class NumpySlabBackend:
         g = self.g
         self.kx = (_modes_full(g["n0"]) * (2 * np.pi / L[0]))[:, None, None]
         ky_all = _modes_full(g["n1"]) * (2 * np.pi / L[1])
+        self.ky_full = ky_all
         self.ky = ky_all[rank * g["ny"]:(rank + 1) * g["ny"]][None, :, None]
         self.kz = (np.arange(g["K"], dtype=np.float64) * (2 * np.pi / L[2]))[None, None, :]
         self.scale_in = 1.5 ** 3 / (g["m0"] * g["m1"] * g["m2"])
@@ -66,11 +67,10 @@ class NumpySlabBackend:
     def forward(self, y, send1):
         g, u = self.g, y.numpy()
         kx, ky, kz = self.kx, self.ky, self.kz
-        sig = [u[0], u[1], u[2],
-               1j * (ky * u[2] - kz * u[1]), 1j * (kz * u[0] - kx * u[2]), 1j * (kx * u[1] - ky * u[0])]
+        sig = [u[0], u[1], u[2], kx * u[1], kx * u[2]]  # curl completed in middle()
         if self.density:
             sig.append(u[3])
-        out = send1.numpy().reshape(self.P, g["S"], g["mx"], g["ny"], g["K"])
+        out = send1.numpy().reshape(self.P, g["S1"], g["mx"], g["ny"], g["K"])
         for s, a in enumerate(sig):
             p = np.fft.ifft(self._pad(a * self.scale_in, 0, g["n0"], g["m0"]), axis=0) * g["m0"]
             for d in range(self.P):
@@ -78,8 +78,15 @@ class NumpySlabBackend:
 
     def middle(self, recv1, send2):
         g = self.g
-        r = recv1.numpy().reshape(self.P, g["S"], g["mx"], g["ny"], g["K"])
-        full = np.concatenate([r[q] for q in range(self.P)], axis=2)  # (S, mx, n1, K)
+        r = recv1.numpy().reshape(self.P, g["S1"], g["mx"], g["ny"], g["K"])
+        w1 = np.concatenate([r[q] for q in range(self.P)], axis=2)  # (S1, mx, n1, K)
+        kyf = (self.ky_full)[None, :, None]
+        kz = self.kz
+        U0, U1, U2, X1, X2 = w1[0], w1[1], w1[2], w1[3], w1[4]
+        sig = [U0, U1, U2, 1j * (kyf * U2 - kz * U1), 1j * (kz * U0 - X2), 1j * (X1 - kyf * U0)]
+        if self.density:
+            sig.append(w1[5])
+        full = np.stack(sig)
         a = np.fft.ifft(self._pad(full, 2, g["n1"], g["m1"]), axis=2) * g["m1"]
         ph = np.fft.irfft(a, n=g["m2"], axis=3) * g["m2"]
         u, w = ph[:3], ph[3:6]

@@ -86,9 +86,10 @@ def test_slab_geometry_rules():
 
     geo = slab_geometry(Grid((1024, 1024, 1024)), 8)
     assert geo["ny"] == 128 and geo["mx"] == 192
-    # bytes per GPU per RHS crossing the fabric (~12.7 GB at P=8)
+    # bytes per GPU per RHS crossing the fabric (~12.7 GB at P=8 with
+    # 6 exchanged signals; the curl is completed after the exchange here -> 5)
     sent = (geo["send1"] + geo["send2"]) * 16 * (7 / 8)
-    assert 11e9 < sent < 14e9
+    assert 10e9 < sent < 12e9
     with pytest.raises(ValueError):
         slab_geometry(Grid((16, 12, 8)), 5)
     with pytest.raises(ValueError):
