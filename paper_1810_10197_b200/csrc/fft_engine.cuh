@@ -77,6 +77,21 @@ struct GenPlan {
 // ---------------------------------------------------------------------------
 // Compile-time engine
 // ---------------------------------------------------------------------------
+// WS: column-private stages (a warp owns whole columns, TPC <= 32): the
+// barriers between stages only need to order the warp itself, except the
+// first stage's load->store barrier when its input (staging) aliases other
+// columns' tile space.
+template <bool WS, int TPC>
+__device__ __forceinline__ void stage_sync() {
+  if constexpr (WS && TPC <= 32)
+    __syncwarp();
+  else
+    __syncthreads();
+}
+
+template <int M, int E, class L, int SIGN, bool LD_SMEM, bool ST_SMEM, int Ls, int R, int... Rest>
+struct FastStageW;
+
 template <int M, int E, class L, int SIGN, bool LD_SMEM, bool ST_SMEM, int Ls, int R, int... Rest>
 struct FastStage {
   template <class LD, class ST>
@@ -148,6 +163,82 @@ struct FastStage {
   }
 };
 
+template <int M, int E, class L, int SIGN, bool LD_SMEM, bool ST_SMEM, int Ls, int R, int... Rest>
+struct FastStageW {
+  template <class LD, class ST>
+  __device__ __forceinline__ static void go(cplx* sm, const cplx* __restrict__ tw, int col, int tj,
+                                            bool act, LD& ld, ST& st) {
+    constexpr int TPC = M / E;
+    constexpr int NB = E / R;
+    constexpr int STRIDE = M / R;
+    constexpr bool FIRST = (Ls == 1);
+    constexpr bool LAST = (sizeof...(Rest) == 0);
+    static_assert(E % R == 0, "radix must divide elements-per-thread");
+    cplx v[NB][R];
+    if (act) {
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int j = tj + b * TPC;
+        if constexpr (FIRST) {
+#pragma unroll
+          for (int t = 0; t < R; ++t) v[b][t] = ld(j + t * STRIDE, col);
+        } else if constexpr (STRIDE % 8 == 0) {
+          const int a0 = L::idx(j, col);
+#pragma unroll
+          for (int t = 0; t < R; ++t) v[b][t] = sm[a0 + t * (STRIDE / 8) * L::STEP8];
+        } else {
+#pragma unroll
+          for (int t = 0; t < R; ++t) v[b][t] = sm[L::idx(j + t * STRIDE, col)];
+        }
+      }
+    }
+    if constexpr ((!FIRST || LD_SMEM) && (!LAST || ST_SMEM)) {
+      if constexpr (FIRST)
+        __syncthreads();  // staging may alias other columns
+      else
+        stage_sync<true, TPC>();
+    }
+    if (act) {
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const unsigned j = (unsigned)tj + (unsigned)(b * TPC);
+        const unsigned k = j % (unsigned)Ls;
+        if constexpr (Ls > 1) {
+          constexpr int TS = M / (Ls * R);
+          const unsigned kts = k * (unsigned)TS;
+#pragma unroll
+          for (int t = 1; t < R; ++t) {
+            cplx w = __ldg(&tw[(unsigned)t * kts]);
+            if (SIGN > 0) w.y = -w.y;
+            v[b][t] = cmul(v[b][t], w);
+          }
+        }
+        DFT<R, SIGN>::run(v[b]);
+        const int base = (int)((j - k) * (unsigned)R + k);
+        if constexpr (LAST) {
+#pragma unroll
+          for (int q = 0; q < R; ++q) st(base + q * Ls, col, v[b][q]);
+        } else if constexpr (Ls % 8 == 0) {
+          const int a0 = L::idx(base, col);
+#pragma unroll
+          for (int q = 0; q < R; ++q) sm[a0 + q * (Ls / 8) * L::STEP8] = v[b][q];
+        } else if constexpr (Ls == 1 && (8 % R == 0)) {
+          const int a0 = L::idx(base, col);  // base = j*R: the R rows share one 8-row group
+#pragma unroll
+          for (int q = 0; q < R; ++q) sm[a0 + q * L::ROWSTEP] = v[b][q];
+        } else {
+#pragma unroll
+          for (int q = 0; q < R; ++q) sm[L::idx(base + q * Ls, col)] = v[b][q];
+        }
+      }
+    }
+    if constexpr (!LAST) {
+      stage_sync<true, TPC>();
+      FastStageW<M, E, L, SIGN, LD_SMEM, ST_SMEM, Ls * R, Rest...>::go(sm, tw, col, tj, act, ld, st);
+    }
+  }
+};
+
 template <int M_, int E_, class L, int... Rs>
 struct FastFFT {
   static constexpr int M = M_, E = E_, TPC = M_ / E_;
@@ -169,6 +260,17 @@ struct FastFFT {
     const bool act = (tid < NT) && (col < ncols);
     __builtin_assume(tj >= 0 && tj < TPC);
     FastStage<M_, E_, L, SIGN, LD_SMEM, ST_SMEM, 1, Rs...>::go(sm, tw, col, tj, act, ld, st);
+  }
+  // column-private variant (ColTile: a warp owns whole columns when TPC <= 32)
+  template <int SIGN, bool LD_SMEM, bool ST_SMEM, class LD, class ST>
+  __device__ __forceinline__ static void run_ws(const GenPlan&, cplx* sm, const cplx* __restrict__ tw,
+                                                int ncols, LD& ld, ST& st) {
+    const int tid = threadIdx.x;
+    const int col = L::col_of(tid, TPC);
+    const int tj = L::tj_of(tid, TPC);
+    const bool act = (tid < NT) && (col < ncols);
+    __builtin_assume(tj >= 0 && tj < TPC);
+    FastStageW<M_, E_, L, SIGN, LD_SMEM, ST_SMEM, 1, Rs...>::go(sm, tw, col, tj, act, ld, st);
   }
 };
 

@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
       return cmk(A.x - B.y, A.y + B.x);
     };
     auto st = [&](int n, int c, cplx v) { sm[L::idx(n, c)] = v; };
-    EngI::template run<+1, true, true>(a.gp, sm, a.tw, S, ld, st);
+    EngI::template run_ws<+1, true, true>(a.gp, sm, a.tw, S, ld, st);
   }
   __syncthreads();
   // ---- fused: last inverse radix-4 (Ls = M/4) | u x w | first forward radix-4 ----
@@ -602,7 +602,7 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
     auto st = [&](int n, int c, cplx v) {
       if (n < K - 1 || n > M - K + 1) sm[L::idx(n, c)] = v;
     };
-    FastStage<M, EF, L, -1, true, true, 4, FR...>::go(sm, a.tw, col, tj, act, ld, st);
+    FastStageW<M, EF, L, -1, true, true, 4, FR...>::go(sm, a.tw, col, tj, act, ld, st);
   }
   __syncthreads();
   // ---- extraction: two real spectra per complex column, K modes, kz = n/2 zeroed ----
