@@ -61,6 +61,9 @@ struct PassArgs {
   long long in_bstride, out_bstride;
   int y0, n1g;
   int xplanes;  // PK_INV_CURLY: x planes per signal (m0, or m0/P on a slab)
+  int xblk;     // PK_INV_CURLY: x planes per block (divides xplanes)
+  int nsig;     // PK_INV_CURLY: output signals; block planes run signal-fastest
+                // (p = x*nsig + s) so the 6 signals of one x share L2-resident inputs
 };
 
 SRK_DEV unsigned row_off(int row, unsigned rs, int rpb, long long bstride) {
@@ -107,6 +110,15 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
   const int w0 = wt * C;
   const int ncols = min(C, a.Qp - w0);
   const unsigned rs = (unsigned)a.row_stride;  // intra-plane offsets fit in 32 bits
+  if constexpr (KIND == PK_INV_CURLY) {
+    // blocks of XB x-planes, signal-major inside a block: the 5 input planes of
+    // XB x values stay L2-resident while the 6 signals read them
+    const int XB = a.xblk;
+    const int span = a.nsig * XB;
+    const int xb = plane / span, r = plane - xb * span;
+    const int s_ = r / XB, x_ = xb * XB + (r - (r / XB) * XB);
+    plane = s_ * a.xplanes + x_;
+  }
   const cplx* __restrict__ inp = a.in + plane * a.in_plane_stride + w0;
   cplx* __restrict__ outp = a.out + plane * a.out_plane_stride + w0;
   const int M = CTN ? Eng::M : a.M;

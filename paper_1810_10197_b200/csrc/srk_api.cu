@@ -185,6 +185,14 @@ int need_ws(srk_plan* p) {
 }
 
 // ---- strided pass launch -------------------------------------------------
+int curly_xblk(int X) {
+  int want = 2;
+  if (const char* e = getenv("SRK_XBLK")) want = atoi(e);
+  for (int b = want; b > 1; --b)
+    if (X % b == 0) return b;
+  return 1;
+}
+
 int launch_col(srk_plan* p, int kind, PassArgs a, cudaStream_t st) {
   const bool padded_kind = kind == KK_INV_P || kind == KK_FWD_P || kind == KK_INV_RHS || kind >= KK_INV_RHS_SLAB;
   if (padded_kind && 3 * a.n != 2 * a.M) return fail(SRK_ERR_INVALID, "padded pass needs M = 3n/2");
@@ -508,6 +516,8 @@ int srk_rhs(srk_plan* p, const void* y_, void* f_, double nu, double ri, double 
     // K2: curl completion + y pad + inverse y
     PassArgs b = y_pass(p, p->A, p->B, p->S, p->m0, p->n1, p->m1, p->m1, p->n1);
     b.xplanes = p->m0;
+    b.xblk = curly_xblk(p->m0);
+    b.nsig = p->S;
     b.ck1 = p->ck1;
     b.ck2 = p->ck2;
     if ((rc = launch_col(p, KK_INV_CURLY, b, st))) return rc;
@@ -774,6 +784,8 @@ int srk_slab_middle(srk_plan* p, const void* recv1, void* send2, void* stream) {
   b.in_rpb = (int)Ny;
   b.in_bstride = (long long)p->S1 * Mx * Ny * K;
   b.xplanes = p->Mx;
+  b.xblk = curly_xblk(p->Mx);
+  b.nsig = p->S;
   b.ck1 = p->ck1;
   b.ck2 = p->ck2;
   if ((rc = launch_col(p, KK_INV_CURLY_SLAB, b, st))) return rc;
