@@ -25,7 +25,9 @@ enum KernelKind {
   KK_INV_KX_SLAB = 16,   // 3D K1, all-to-all #1 send layout
   KK_INV_CURLY = 17,     // 3D K2 (curl completed on load)
   KK_INV_CURLY_SLAB = 18,  // 3D K2 from the all-to-all #1 receive layout
-  KK_COUNT = 19
+  KK_FWD_PROJ = 19,        // K5 + K6 fused over a cluster of So CTAs (DSMEM)
+  KK_FWD_PROJ_SLAB = 20,   // same, reading the all-to-all #2 receive layout
+  KK_COUNT = 21
 };
 
 struct KEntry {
@@ -68,7 +70,9 @@ struct GenCols {
     t[KK_INV_KX_SLAB] = SRK_ENTRY((k_colpass<SE, PK_INV_KX, +1, PF_CTN | PF_BOUT>), SE, SL::SIZE * 16); \
     t[KK_INV_CURLY] = SRK_ENTRY((k_colpass<SE, PK_INV_CURLY, +1, PF_CTN>), SE, SRK_RHS_SMEM(M, CS)); \
     t[KK_INV_CURLY_SLAB] = SRK_ENTRY((k_colpass<SE, PK_INV_CURLY, +1, PF_CTN | PF_BIN>), SE,       \
-                                     SRK_RHS_SMEM(M, CS));
+                                     SRK_RHS_SMEM(M, CS));                                         \
+    t[KK_FWD_PROJ] = SRK_ENTRY((k_xfwd_proj<SE, PF_CTN>), SE, SL::SIZE * 16);                      \
+    t[KK_FWD_PROJ_SLAB] = SRK_ENTRY((k_xfwd_proj<SE, PF_CTN | PF_BIN>), SE, SL::SIZE * 16);
 
 // Instantiate every kernel kind for one fast FFT length.
 #define SRK_DEFINE_SIZE(NAME, M, E, CS, ...) SRK_DEFINE_SIZE_F(NAME, M, E, CS, E, (__VA_ARGS__), __VA_ARGS__)

@@ -212,6 +212,43 @@ int launch_col(srk_plan* p, int kind, PassArgs a, cudaStream_t st) {
   return SRK_OK;
 }
 
+// ---- fused x-forward + projection over clusters of So CTAs --------------------
+int launch_fwd_proj(srk_plan* p, int kind, PassArgs a, cudaStream_t st) {
+  KEntry e;
+  int rc = get_entry(kind, a.M, e, a.gp);
+  if (rc) return rc;
+  if (!e.fn || !g_fast->count(a.M)) return fail(SRK_ERR_UNSUPPORTED, "no fused projection kernel");
+  if ((rc = get_tw(p, a.M, &a.tw))) return rc;
+  if ((rc = ensure_smem(e))) return rc;
+  a.tpp = (a.Qp + e.cols - 1) / e.cols;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(a.planes * a.tpp));
+  cfg.blockDim = dim3(e.nt);
+  cfg.dynamicSmemBytes = e.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = a.planes;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  void* args[] = {&a};
+  cudaError_t err = cudaLaunchKernelExC(&cfg, e.fn, args);
+  if (err != cudaSuccess) return fail(SRK_ERR_CUDA, std::string("fused projection launch: ") + cudaGetErrorString(err));
+  p->last_launches++;
+  if (p->timing && p->nev < 16) cudaEventRecord(p->ev[p->nev++], st);
+  return SRK_OK;
+}
+
+// Opt-in (SRK_FUSEPROJ=1): measured slower than K5 + K6 on B200 at 512^3
+// (6.2 ms vs 2.3 + 2.0 ms; DSMEM reads of the peer tiles and cluster
+// co-scheduling cost more than the 6.5 GB of G traffic they save).
+bool use_fused_proj(const srk_plan* p) {
+  init_registry();
+  return getenv("SRK_FUSEPROJ") && g_fast->count(p->m0) && g_fast->at(p->m0).e[KK_FWD_PROJ].fn;
+}
+
 // ---- z pass launch (pairs of pencils) ---------------------------------------
 int launch_z(srk_plan* p, int kind, ZArgs a, int S_rt, int So_rt, cudaStream_t st) {
   KEntry e;
@@ -549,6 +586,23 @@ int srk_rhs(srk_plan* p, const void* y_, void* f_, double nu, double ri, double 
   c5.scale = std::pow(1.0 / 1.5, d);
   c5.zero_nyq = 1;
   c5.zero_dc_imag = 1;
+  if (use_fused_proj(p)) {  // K5 + K6 fused over a thread-block cluster (DSMEM)
+    c5.y = y;
+    c5.f = f;
+    c5.density = p->density;
+    c5.nu = nu;
+    c5.ri = ri;
+    c5.re_pr = re_pr;
+    c5.dims = d;
+    c5.K = p->K;
+    c5.n1g = p->n1g;
+    c5.y0 = p->y0;
+    c5.ck0 = p->ck0;
+    c5.ck1 = p->ck1;
+    c5.ck2 = p->ck2;
+    c5.comp_stride = p->modes;
+    return launch_fwd_proj(p, KK_FWD_PROJ, c5, st);
+  }
   if ((rc = launch_col(p, KK_FWD_P, c5, st))) return rc;
   // K6: projection + viscous (+ Boussinesq terms)
   ProjArgs pa;
@@ -830,6 +884,22 @@ int srk_slab_finish(srk_plan* p, const void* recv2, const void* y, void* f, doub
   c5.zero_nyq = 1;
   c5.zero_dc_imag = 1;
   c5.y0 = p->y0;
+  if (use_fused_proj(p)) {
+    c5.y = (const cplx*)y;
+    c5.f = (cplx*)f;
+    c5.density = p->density;
+    c5.nu = nu;
+    c5.ri = ri;
+    c5.re_pr = re_pr;
+    c5.dims = p->dims;
+    c5.K = p->K;
+    c5.n1g = p->n1g;
+    c5.ck0 = p->ck0;
+    c5.ck1 = p->ck1;
+    c5.ck2 = p->ck2;
+    c5.comp_stride = p->modes;
+    return launch_fwd_proj(p, KK_FWD_PROJ_SLAB, c5, st);
+  }
   if ((rc = launch_col(p, KK_FWD_P_SLABI, c5, st))) return rc;
   ProjArgs pa;
   pa.g = geom(p);

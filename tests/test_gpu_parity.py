@@ -417,3 +417,14 @@ def test_work_precision_sweep_small():
     pts, _ = srk.work_precision(cells, ref)
     assert len(pts) == 4 and all(p.status == "ok" and np.isfinite(p.error) for p in pts)
     assert {p.rhs_evals for p in pts if p.integrator == "rk4"} == {10 * 4 + 1}
+
+
+def test_fused_cluster_projection_matches(monkeypatch):
+    """Opt-in K5+K6 fusion over a thread-block cluster (DSMEM) gives the same RHS."""
+    og = O.OGrid((64, 64, 64))
+    y = dev(O.hit(og, a=4.0, energy=0.5, seed=2))
+    g = srk.Grid((64, 64, 64))
+    f0 = srk.FlowRHS(g, srk.PhysParams(500.0))(0.0, y)
+    monkeypatch.setenv("SRK_FUSEPROJ", "1")
+    f1 = srk.FlowRHS(g, srk.PhysParams(500.0))(0.0, y)
+    assert rel(f1, f0) <= 1e-15
