@@ -642,6 +642,7 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
 }
 
 
+
 // ---------------------------------------------------------------------------
 // K5 + K6 fused over a thread-block cluster (cluster = the So product signals
 // of one column tile; cluster rank = signal).  Each CTA runs the x-forward

@@ -570,7 +570,7 @@ int srk_rhs(srk_plan* p, const void* y_, void* f_, double nu, double ri, double 
   z.out_sig_stride = (long long)P * p->K;
   z.zero_nyq = 1;
   z.mode = getenv("SRK_ZMODE") ? atoi(getenv("SRK_ZMODE")) : 0;
-  const int kind = d == 3 ? (p->density ? KK_Z_B3 : KK_Z_NS3) : (p->density ? KK_Z_B2 : KK_Z_NS2);
+  int kind = d == 3 ? (p->density ? KK_Z_B3 : KK_Z_NS3) : (p->density ? KK_Z_B2 : KK_Z_NS2);
   if ((rc = launch_z(p, kind, z, 0, 0, st))) return rc;
   const cplx* xin = zout;
   cplx* gbuf = p->A;
