@@ -144,6 +144,12 @@ int srk_slab_middle(srk_plan* plan, const void* recv1, void* send2, void* stream
 int srk_slab_finish(srk_plan* plan, const void* recv2, const void* y, void* f, double nu, double ri, double re_pr,
                     void* stream);
 
+/* Diagnostics: when dev_buf (u64) is non-NULL, launch number launch_index of
+ * the next srk_rhs chain (0 = K1) records clock64() phase timestamps of every
+ * 97th CTA into it (3 per CTA for the axis passes, 6 for the NS3 z-pass;
+ * tools/phase_timing.py).  Not a compute entry point. */
+int srk_debug_phase_buffer(srk_plan* plan, void* dev_buf, int launch_index);
+
 /* Number of kernel launches the last srk_rhs issued (launch accounting for
  * the bench's gpu_launches claim). */
 int srk_rhs_launch_count(const srk_plan* plan);

@@ -11,7 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libsrk.so")
+LIB_PATH = os.environ.get("SRK_LIB") or os.path.join(_HERE, "_lib", "libsrk.so")  # SRK_LIB: experiment builds
 
 SRK_OK = 0
 SRK_ERR_INVALID = 1
@@ -26,7 +26,7 @@ EXPORTS = (
     "srk_narrow", "srk_forward_transform", "srk_inverse_transform", "srk_curl",
     "srk_leray_project", "srk_combine", "srk_step_reduce", "srk_band_energy",
     "srk_band_scale", "srk_rhs_launch_count", "srk_rhs_timed", "srk_plan_create_slab", "srk_slab_sizes",
-    "srk_slab_forward", "srk_slab_middle", "srk_slab_finish",
+    "srk_slab_forward", "srk_slab_middle", "srk_slab_finish", "srk_debug_phase_buffer",
 )
 
 _lib = None
@@ -82,6 +82,7 @@ def load():
         "srk_slab_forward": (c_int, [vp, vp, vp, vp]),
         "srk_slab_middle": (c_int, [vp, vp, vp, vp]),
         "srk_slab_finish": (c_int, [vp, vp, vp, vp, c_dbl, c_dbl, c_dbl, vp]),
+        "srk_debug_phase_buffer": (c_int, [vp, vp, c_int]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

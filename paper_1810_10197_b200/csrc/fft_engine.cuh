@@ -81,6 +81,34 @@ struct GenPlan {
 // barriers between stages only need to order the warp itself, except the
 // first stage's load->store barrier when its input (staging) aliases other
 // columns' tile space.
+// Shared-memory twiddle table: the first quarter wave exp(-2 pi i r / M),
+// r < M/4, stored XOR-swizzled (conflict-free for the power-of-two strides of
+// the stage lookups).  w^m = (-i)^(m / (M/4)) * tab[m mod M/4] is exact (the
+// quarter-turn rotations only swap / negate), so every twiddle equals the
+// correctly rounded full-table value.  Filled once per CTA from the global
+// table (twiddles read through L1 missed ~60% under the FFT tiles' smem
+// carve-out and were the largest single stall source).
+template <int M>
+struct TwTab {
+  static constexpr int Q = M / 4;
+  static constexpr int N = (M % 4 == 0) ? ((Q + 7) / 8) * 8 : 0;
+};
+SRK_DEV int tw_swz(int r) { return r ^ ((r >> 3) & 7); }
+template <int M>
+__device__ __forceinline__ void tw_fill(cplx* tws, const cplx* __restrict__ tw) {
+  for (int i = threadIdx.x; i < TwTab<M>::Q; i += blockDim.x) tws[tw_swz(i)] = __ldg(&tw[i]);
+}
+template <int M>
+__device__ __forceinline__ cplx tw_get(const cplx* tws, unsigned m) {
+  static_assert(M % 4 == 0, "quarter-wave table needs 4 | M");
+  constexpr unsigned Q = M / 4;
+  const unsigned q = m / Q, r = m - q * Q;
+  const cplx w = tws[tw_swz((int)r)];
+  const double a = (q & 1u) ? w.y : w.x;
+  const double b = (q & 1u) ? -w.x : w.y;
+  return (q & 2u) ? make_double2(-a, -b) : make_double2(a, b);
+}
+
 template <bool WS, int TPC>
 __device__ __forceinline__ void stage_sync() {
   if constexpr (WS && TPC <= 32)
@@ -132,7 +160,7 @@ struct FastStage {
           const unsigned kts = k * (unsigned)TS;
 #pragma unroll
           for (int t = 1; t < R; ++t) {
-            cplx w = __ldg(&tw[(unsigned)t * kts]);
+            cplx w = tw_get<M>(tw, (unsigned)t * kts);  // tw: shared-memory table
             if (SIGN > 0) w.y = -w.y;
             v[b][t] = cmul(v[b][t], w);
           }
@@ -208,7 +236,7 @@ struct FastStageW {
           const unsigned kts = k * (unsigned)TS;
 #pragma unroll
           for (int t = 1; t < R; ++t) {
-            cplx w = __ldg(&tw[(unsigned)t * kts]);
+            cplx w = tw_get<M>(tw, (unsigned)t * kts);  // tw: shared-memory table
             if (SIGN > 0) w.y = -w.y;
             v[b][t] = cmul(v[b][t], w);
           }
@@ -246,6 +274,7 @@ struct FastFFT {
   static constexpr int NT = C * TPC;
   static constexpr bool kFast = true;
   static constexpr int RPROD = (1 * ... * Rs);
+  static constexpr int TWN = TwTab<M_>::N;  // shared twiddle table entries (before the tile)
   // RPROD < M: a prefix of a longer plan (the remaining stages are run by the
   // caller, e.g. the fused middle stage of the NS3 z-pass)
   static_assert(M_ % RPROD == 0, "radices must divide M");
@@ -297,6 +326,7 @@ __device__ __forceinline__ void gen_dft(int R, cplx* v) {
 template <class L>
 struct GenericFFT {
   static constexpr bool kFast = false;
+  static constexpr int TWN = 0;
   static constexpr int M = 0;  // runtime
   static constexpr int C = L::C;
   static constexpr int NT = L::C;

@@ -71,7 +71,18 @@ struct PassArgs {
   double nu, ri, re_pr;
   int nsig;     // PK_INV_CURLY: output signals; block planes run signal-fastest
                 // (p = x*nsig + s) so the 6 signals of one x share L2-resident inputs
+  unsigned long long* dbg;  // optional phase timestamps (tools/phase_timing.py)
 };
+
+// Phase timestamps of every 97th CTA (diagnostics only; dbg == nullptr in
+// production launches, so the branch is uniform and never taken).
+#define SRK_TS_INIT(ptr, nts)                                                          \
+  unsigned long long* dbg_ =                                                           \
+      ((ptr) && (blockIdx.x % 97 == 0) && threadIdx.x == 0) ? (ptr) + (blockIdx.x / 97) * (nts) : nullptr;
+#define SRK_TS(i)          \
+  if (dbg_) {              \
+    dbg_[i] = clock64();   \
+  }
 
 SRK_DEV unsigned row_off(int row, unsigned rs, int rpb, long long bstride) {
   if (rpb <= 0) return (unsigned)row * rs;
@@ -100,13 +111,10 @@ __device__ __forceinline__ void stage_rows(cplx* dst, const cplx* __restrict__ s
 // output rows (slab all-to-all layouts).
 enum PassFlags { PF_CTN = 1, PF_BIN = 2, PF_BOUT = 4 };
 
-template <class Eng, int KIND, int SIGN, int FL = 0>
-__global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(const PassArgs a) {
-  extern __shared__ __align__(16) cplx sm[];
-  constexpr int C = Eng::C;
-  constexpr bool CTN = (FL & PF_CTN) && Eng::kFast;
-  const int bid = blockIdx.x;
-  int plane, wt;
+// Block -> (plane, first column) of a strided pass.
+template <int KIND, int C>
+SRK_DEV void tile_of(const PassArgs& a, int bid, int& plane, int& w0) {
+  int wt;
   if (a.sig_minor) {
     plane = bid % a.planes;
     wt = bid / a.planes;
@@ -114,9 +122,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
     plane = bid / a.tpp;
     wt = bid % a.tpp;
   }
-  const int w0 = wt * C;
-  const int ncols = min(C, a.Qp - w0);
-  const unsigned rs = (unsigned)a.row_stride;  // intra-plane offsets fit in 32 bits
+  w0 = wt * C;
   if constexpr (KIND == PK_INV_CURLY) {
     // blocks of XB x-planes, signal-major inside a block: the 5 input planes of
     // XB x values stay L2-resident while the 6 signals read them
@@ -126,6 +132,23 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
     const int s_ = r / XB, x_ = xb * XB + (r - (r / XB) * XB);
     plane = s_ * a.xplanes + x_;
   }
+}
+
+template <class Eng, int KIND, int SIGN, int FL = 0>
+__global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(const PassArgs a) {
+  extern __shared__ __align__(16) cplx smraw[];
+  cplx* const sm = smraw + Eng::TWN;
+  const cplx* const twp = Eng::kFast ? smraw : a.tw;
+  if constexpr (Eng::kFast) tw_fill<Eng::M>(smraw, a.tw);  // ordered by the staging barrier
+  constexpr int C = Eng::C;
+  constexpr bool CTN = (FL & PF_CTN) && Eng::kFast;
+  SRK_TS_INIT(a.dbg, 3)
+  SRK_TS(0)
+  const int bid = blockIdx.x;
+  int plane, w0;
+  tile_of<KIND, C>(a, bid, plane, w0);
+  const int ncols = min(C, a.Qp - w0);
+  const unsigned rs = (unsigned)a.row_stride;  // intra-plane offsets fit in 32 bits
   const cplx* __restrict__ inp = a.in + plane * a.in_plane_stride + w0;
   cplx* __restrict__ outp = a.out + plane * a.out_plane_stride + w0;
   const int M = CTN ? Eng::M : a.M;
@@ -139,6 +162,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
       stage_rows<C>(sm, inp, n, rs, ncols, in_rpb, a.in_bstride);
       cp_async_wait_all();
       __syncthreads();
+      SRK_TS(1)
     }
     auto ld = [&](int row, int col) -> cplx {
       const int cr = pad_src(row, n, M);
@@ -149,7 +173,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
       return cmk(v.x * f, v.y * f);
     };
     auto st = [&](int row, int col, cplx v) { outp[row_off(row, rs, out_rpb, a.out_bstride) + (unsigned)col] = v; };
-    Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, a.tw, ncols, ld, st);
+    Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, twp, ncols, ld, st);
   } else if constexpr (KIND == PK_INV_RHS) {
     // plane = signal s: [u_0..u_{d-1}, w (3 comps in 3D, 1 in 2D), rho]
     const int d = a.dims;
@@ -192,6 +216,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
       if (is_curl) stage_rows<C>(sm + n * C, pb, n, rs, ncols, in_rpb, a.in_bstride);
       cp_async_wait_all();
       __syncthreads();
+      SRK_TS(1)
     }
     auto ld = [&](int row, int col) -> cplx {
       const int cr = pad_src(row, n, M);
@@ -209,7 +234,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
       return cmk(v.x * f, v.y * f);
     };
     auto st = [&](int row, int col, cplx v) { outp[row_off(row, rs, out_rpb, a.out_bstride) + (unsigned)col] = v; };
-    Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, a.tw, ncols, ld, st);
+    Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, twp, ncols, ld, st);
   } else if constexpr (KIND == PK_INV_KX) {
     // 3D K1.  k_y and k_z are constant along x, so the x inverse commutes with
     // them: only k_x u1 and k_x u2 need their own transforms; the curl is
@@ -224,6 +249,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
       stage_rows<C>(sm, pa, n, rs, ncols, in_rpb, a.in_bstride);
       cp_async_wait_all();
       __syncthreads();
+      SRK_TS(1)
     }
     auto ld = [&](int row, int col) -> cplx {
       const int cr = pad_src(row, n, M);
@@ -235,7 +261,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
       return cmk(u.x * f, u.y * f);
     };
     auto st = [&](int row, int col, cplx v) { outp[row_off(row, rs, out_rpb, a.out_bstride) + (unsigned)col] = v; };
-    Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, a.tw, ncols, ld, st);
+    Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, twp, ncols, ld, st);
   } else if constexpr (KIND == PK_INV_CURLY) {
     // 3D K2.  plane = (s, x), s over [u0, u1, u2, w0, w1, w2, (rho)]; the input
     // planes are the K1 signals [U0, U1, U2, X1 = F(kx u1), X2 = F(kx u2), R]:
@@ -260,6 +286,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
       if (is_curl) stage_rows<C>(sm + n * C, pb, n, rs, ncols, in_rpb, a.in_bstride);
       cp_async_wait_all();
       __syncthreads();
+      SRK_TS(1)
     }
     auto ld = [&](int row, int col) -> cplx {
       const int cr = pad_src(row, n, M);
@@ -276,7 +303,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
       return ok ? v : cmk(0.0, 0.0);
     };
     auto st = [&](int row, int col, cplx v) { outp[row_off(row, rs, out_rpb, a.out_bstride) + (unsigned)col] = v; };
-    Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, a.tw, ncols, ld, st);
+    Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, twp, ncols, ld, st);
   } else {  // PK_FWD: forward C2C + truncation (+ scale, Nyquist / DC-imag zeroing)
     const bool zn = a.zero_nyq != 0;
     const bool zdc = (a.zero_dc_imag != 0) && (w0 == 0) && (a.y0 == 0);
@@ -285,6 +312,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
       stage_rows<C>(sm, inp, M, rs, ncols, in_rpb, a.in_bstride);
       cp_async_wait_all();
       __syncthreads();
+      SRK_TS(1)
     }
     auto ld = [&](int row, int col) -> cplx {
       return Eng::kFast ? sm[row * C + col] : inp[row_off(row, rs, in_rpb, a.in_bstride) + (unsigned)col];
@@ -297,7 +325,11 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
       if (zdc && c == 0 && col == 0) o.y = 0.0;
       outp[row_off(c == -2 ? (n >> 1) : c, rs, out_rpb, a.out_bstride) + (unsigned)col] = o;
     };
-    Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, a.tw, ncols, ld, st);
+    Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, twp, ncols, ld, st);
+  }
+  if (a.dbg) {
+    __syncthreads();
+    SRK_TS(2)
   }
 }
 
@@ -322,7 +354,8 @@ struct ZArgs {
   int So; // output real signals per pencil
   long long in_sig_stride, out_sig_stride;  // complex elements (P*K) or real (P*M)
   int zero_nyq;  // R2C: zero the kz = n/2 plane (narrow)
-  int mode;      // NS3 fused z-pass experiment switch (0 = prefetch in the forward half)
+  int mode;      // unused (kept for ABI stability of the struct)
+  unsigned long long* dbg;  // optional phase timestamps (tools/phase_timing.py)
 };
 
 template <int OP>
@@ -357,7 +390,10 @@ SRK_DEV void zphys(const double* r, double* o) {
 // (So columns) -- a different plan when So < S so all threads stay busy.
 template <class Eng, class L, int OP, class EngF = Eng>
 __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 192 ? 2 : 1)) k_zpass(const ZArgs a, int S_rt, int So_rt) {
-  extern __shared__ __align__(16) cplx sm[];
+  extern __shared__ __align__(16) cplx smraw[];
+  cplx* const sm = smraw + Eng::TWN;  // [twiddle table][tile]
+  const cplx* const twp = Eng::kFast ? smraw : a.tw;
+  if constexpr (Eng::kFast) tw_fill<Eng::M>(smraw, a.tw);  // first use is after a CTA barrier
   const int p0 = 2 * blockIdx.x;
   const int S = (OP >= ZOP_NS3) ? ZSig<OP>::S : S_rt;
   const int So = (OP >= ZOP_NS3) ? ZSig<OP>::So : So_rt;
@@ -431,11 +467,11 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 192 ? 2 : 1)) k_zpass(con
           if (pen < a.P) a.out_real[s * a.out_sig_stride + (long long)pen * M + n] = v.y;
         }
       };
-      Eng::template run<+1, true, false>(a.gp, sm, a.tw, S, ld, st);
+      Eng::template run<+1, true, false>(a.gp, sm, twp, S, ld, st);
       return;
     } else {
       auto st = [&](int n, int c, cplx v) { sm[L::idx(n, c)] = v; };
-      Eng::template run<+1, true, true>(a.gp, sm, a.tw, S, ld, st);
+      Eng::template run<+1, true, true>(a.gp, sm, twp, S, ld, st);
       __syncthreads();
       // ---- physical space: per row n, both pencils ----
       for (int n = threadIdx.x; n < M; n += blockDim.x) {
@@ -468,14 +504,14 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 192 ? 2 : 1)) k_zpass(con
       return cmk(v[0], v[1]);
     };
     auto st = [&](int n, int c, cplx v) { sm[L::idx(n, c)] = v; };
-    Eng::template run<-1, false, true>(a.gp, sm, a.tw, So, ld, st);
+    Eng::template run<-1, false, true>(a.gp, sm, twp, So, ld, st);
   } else {
     auto ld = [&](int n, int c) -> cplx { return sm[L::idx(n, c)]; };
     // only rows [0, K-1) and (M-K+1, M) feed the kept modes (kz = n/2 is zeroed)
     auto st = [&](int n, int c, cplx v) {
       if (n < K - 1 || n > M - K + 1) sm[L::idx(n, c)] = v;
     };
-    EngF::template run<-1, true, true>(a.gp, sm, a.tw, So, ld, st);
+    EngF::template run<-1, true, true>(a.gp, sm, twp, So, ld, st);
   }
   __syncthreads();
   // ---- extraction: two real spectra from each complex column, keep K modes ----
@@ -515,11 +551,16 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 192 ? 2 : 1)) k_zpass(con
 // ---------------------------------------------------------------------------
 template <int M, class L, class EngI, int EF, int... FR>
 __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(const ZArgs a, int, int) {
-  extern __shared__ __align__(16) cplx sm[];
+  extern __shared__ __align__(16) cplx smraw[];
+  cplx* const sm = smraw + EngI::TWN;  // [twiddle table][tile]
+  const cplx* const twp = smraw;
+  tw_fill<M>(smraw, a.tw);  // ordered by the mbarrier-init barrier
   constexpr int S = 6, So = 3, NT = M / 4, K = M / 3 + 1, Q = M / 4;
   static_assert(EngI::NT == NT, "inverse prefix must use M/4 threads");
   const int p0 = 2 * blockIdx.x;
   const int tid = threadIdx.x;
+  SRK_TS_INIT(a.dbg, 6)
+  SRK_TS(0)
   // ---- staging: 12 real-signal rows of K modes via 1D TMA bulk copies ----
   cplx* stg = sm;
   __shared__ __align__(8) unsigned long long mbar;
@@ -541,6 +582,7 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
     for (int i = tid; i < S * K; i += NT) stg[S * K + i] = cmk(0.0, 0.0);
   mbar_wait(&mbar, 0);
   __syncthreads();
+  SRK_TS(1)
   auto hs = [&](int g, int k) -> cplx {
     const bool head = k < K;
     const bool tail = k >= M - (K - 1);
@@ -557,9 +599,10 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
       return cmk(A.x - B.y, A.y + B.x);
     };
     auto st = [&](int n, int c, cplx v) { sm[L::idx(n, c)] = v; };
-    EngI::template run_ws<+1, true, true>(a.gp, sm, a.tw, S, ld, st);
+    EngI::template run_ws<+1, true, true>(a.gp, sm, twp, S, ld, st);
   }
   __syncthreads();
+  SRK_TS(2)
   // ---- fused: last inverse radix-4 (Ls = M/4) | u x w | first forward radix-4 ----
   {
     const int j = tid;
@@ -578,7 +621,7 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
     cplx w[4];
 #pragma unroll
     for (int t = 1; t < 4; ++t) {
-      w[t] = __ldg(&a.tw[t * j]);
+      w[t] = tw_get<M>(twp, (unsigned)(t * j));
       w[t].y = -w[t].y;  // inverse sign
     }
     __syncthreads();
@@ -610,6 +653,7 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
     }
   }
   __syncthreads();
+  SRK_TS(3)
   // ---- forward suffix stages (Ls = 4 ...) on the 3 packed columns ----
   {
     // EF elements per thread: 12 puts all M/4 threads on the 3 forward columns
@@ -621,9 +665,10 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
     auto st = [&](int n, int c, cplx v) {
       if (n < K - 1 || n > M - K + 1) sm[L::idx(n, c)] = v;
     };
-    FastStageW<M, EF, L, -1, true, true, 4, FR...>::go(sm, a.tw, col, tj, act, ld, st);
+    FastStageW<M, EF, L, -1, true, true, 4, FR...>::go(sm, twp, col, tj, act, ld, st);
   }
   __syncthreads();
+  SRK_TS(4)
   // ---- extraction: two real spectra per complex column, K modes, kz = n/2 zeroed ----
   for (int i = tid; i < So * K; i += NT) {
     const int c = i / K, k = i - (i / K) * K;
@@ -638,6 +683,10 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
       const int pp = g / So, s = g - pp * So, pen = p0 + pp;
       if (pen < a.P) a.out[s * a.out_sig_stride + (long long)pen * K + k] = h ? B : A;
     }
+  }
+  if (a.dbg) {
+    __syncthreads();
+    SRK_TS(5)
   }
 }
 
@@ -656,7 +705,9 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
 template <class Eng, int FL>
 __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_xfwd_proj(const PassArgs a) {
   namespace cg = cooperative_groups;
-  extern __shared__ __align__(16) cplx sm[];
+  extern __shared__ __align__(16) cplx smraw[];
+  cplx* const sm = smraw + Eng::TWN;
+  tw_fill<Eng::M>(smraw, a.tw);  // ordered by the staging barrier
   constexpr int C = Eng::C;
   constexpr bool CTN = (FL & PF_CTN) && Eng::kFast;
   cg::cluster_group cluster = cg::this_cluster();
@@ -687,7 +738,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_xfwd_proj
       if (zdc && c == 0 && col == 0) ov.y = 0.0;
       G[(c == -2 ? (n >> 1) : c) * C + col] = ov;
     };
-    Eng::template run<-1, true, true>(a.gp, sm, a.tw, ncols, ld, st);
+    Eng::template run<-1, true, true>(a.gp, sm, smraw, ncols, ld, st);
   }
   cluster.sync();
   // ---- projection of component o on the tile (rows = coarse x, cols = (y, kz)) ----

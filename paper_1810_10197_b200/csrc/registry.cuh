@@ -51,7 +51,7 @@ struct GenCols {
   static constexpr int C = C_;
 };
 
-#define SRK_ENTRY(KFN, ENG, SMB) KEntry{(const void*)(KFN), ENG::NT, ENG::C, (int)(SMB)}
+#define SRK_ENTRY(KFN, ENG, SMB) KEntry{(const void*)(KFN), ENG::NT, ENG::C, (int)(SMB) + ENG::TWN * 16}
 
 // Strided kinds of one fast length (SE / SL in scope).
 #define SRK_RHS_SMEM(M, CS) ((SL::SIZE > 2 * (2 * M / 3) * CS ? SL::SIZE : 2 * (2 * M / 3) * CS) * 16)
@@ -145,5 +145,5 @@ struct GenCols {
     using ZL = ColTile<M, 6>;                                                                           \
     using EI = FastFFT<M, 24, ZL, SRK_UNPAREN IR>;                                                 \
     t[KK_Z_NS3] = KEntry{(const void*)(k_zpass_ns3f<M, ZL, EI, EF, SRK_UNPAREN FR>), M / 4, 6,      \
-                         (int)(ZL::SIZE * 16), 0};                                                 \
+                         (int)(ZL::SIZE * 16) + EI::TWN * 16, 0};                                  \
   }

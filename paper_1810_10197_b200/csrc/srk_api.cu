@@ -148,6 +148,8 @@ struct srk_plan {
   int last_launches = 0;
   // optional per-kernel timing of srk_rhs (srk_rhs_timed)
   bool timing = false;
+  unsigned long long* dbg = nullptr;  // phase timestamps (srk_debug_phase_buffer)
+  int dbg_launch = -1;                // ... recorded by this launch of the chain
   cudaEvent_t ev[16];
   int nev = 0;
   cudaStream_t tstream = nullptr;
@@ -204,6 +206,7 @@ int launch_col(srk_plan* p, int kind, PassArgs a, cudaStream_t st) {
   a.tpp = (a.Qp + e.cols - 1) / e.cols;
   const long long grid = (long long)a.planes * a.tpp;
   if (grid <= 0) return SRK_OK;
+  a.dbg = (p->dbg && p->last_launches == p->dbg_launch) ? p->dbg : nullptr;
   void* args[] = {&a};
   cudaError_t err = cudaLaunchKernel(e.fn, dim3((unsigned)grid), dim3(e.nt), args, e.smem, st);
   if (err != cudaSuccess) return fail(SRK_ERR_CUDA, std::string("colpass launch: ") + cudaGetErrorString(err));
@@ -569,7 +572,7 @@ int srk_rhs(srk_plan* p, const void* y_, void* f_, double nu, double ri, double 
   z.in_sig_stride = (long long)P * p->K;
   z.out_sig_stride = (long long)P * p->K;
   z.zero_nyq = 1;
-  z.mode = getenv("SRK_ZMODE") ? atoi(getenv("SRK_ZMODE")) : 0;
+  z.dbg = (p->dbg && p->last_launches == p->dbg_launch) ? p->dbg : nullptr;
   int kind = d == 3 ? (p->density ? KK_Z_B3 : KK_Z_NS3) : (p->density ? KK_Z_B2 : KK_Z_NS2);
   if ((rc = launch_z(p, kind, z, 0, 0, st))) return rc;
   const cplx* xin = zout;
@@ -643,6 +646,13 @@ int srk_rhs_timed(srk_plan* p, const void* y, void* f, double nu, double ri, dou
 }
 
 int srk_rhs_launch_count(const srk_plan* p) { return p ? p->last_launches : 0; }
+
+int srk_debug_phase_buffer(srk_plan* p, void* dev_buf, int launch_index) {
+  if (!p) return fail(SRK_ERR_INVALID, "null plan");
+  p->dbg = (unsigned long long*)dev_buf;
+  p->dbg_launch = launch_index;
+  return SRK_OK;
+}
 
 int srk_widen(srk_plan* p, const void* spec, int ncomp, void* phys, void* stream) {
   if (!p) return fail(SRK_ERR_INVALID, "null plan");
