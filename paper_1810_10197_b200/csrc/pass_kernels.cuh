@@ -393,7 +393,10 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 192 ? 2 : 1)) k_zpass(con
   extern __shared__ __align__(16) cplx smraw[];
   cplx* const sm = smraw + Eng::TWN;  // [twiddle table][tile]
   const cplx* const twp = Eng::kFast ? smraw : a.tw;
-  if constexpr (Eng::kFast) tw_fill<Eng::M>(smraw, a.tw);  // first use is after a CTA barrier
+  if constexpr (Eng::kFast) {
+    tw_fill<Eng::M>(smraw, a.tw);  // first use is after a CTA barrier
+    cp_async_wait_all();
+  }
   const int p0 = 2 * blockIdx.x;
   const int S = (OP >= ZOP_NS3) ? ZSig<OP>::S : S_rt;
   const int So = (OP >= ZOP_NS3) ? ZSig<OP>::So : So_rt;
@@ -554,7 +557,7 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
   extern __shared__ __align__(16) cplx smraw[];
   cplx* const sm = smraw + EngI::TWN;  // [twiddle table][tile]
   const cplx* const twp = smraw;
-  tw_fill<M>(smraw, a.tw);  // ordered by the mbarrier-init barrier
+  tw_fill<M>(smraw, a.tw);  // cp.async; waited for before the staging barrier
   constexpr int S = 6, So = 3, NT = M / 4, K = M / 3 + 1, Q = M / 4;
   static_assert(EngI::NT == NT, "inverse prefix must use M/4 threads");
   const int p0 = 2 * blockIdx.x;
@@ -581,6 +584,7 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
   if (p0 + 1 >= a.P)
     for (int i = tid; i < S * K; i += NT) stg[S * K + i] = cmk(0.0, 0.0);
   mbar_wait(&mbar, 0);
+  cp_async_wait_all();
   __syncthreads();
   SRK_TS(1)
   auto hs = [&](int g, int k) -> cplx {

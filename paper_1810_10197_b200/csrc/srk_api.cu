@@ -208,6 +208,11 @@ int launch_col(srk_plan* p, int kind, PassArgs a, cudaStream_t st) {
   if (grid <= 0) return SRK_OK;
   a.dbg = (p->dbg && p->last_launches == p->dbg_launch) ? p->dbg : nullptr;
   void* args[] = {&a};
+  static const int smem_pad = getenv("SRK_SMEM_PAD") ? atoi(getenv("SRK_SMEM_PAD")) : 0;  // experiments: occupancy
+  if (smem_pad) {
+    e.smem += smem_pad;
+    cudaFuncSetAttribute(e.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, e.smem);
+  }
   cudaError_t err = cudaLaunchKernel(e.fn, dim3((unsigned)grid), dim3(e.nt), args, e.smem, st);
   if (err != cudaSuccess) return fail(SRK_ERR_CUDA, std::string("colpass launch: ") + cudaGetErrorString(err));
   p->last_launches++;
