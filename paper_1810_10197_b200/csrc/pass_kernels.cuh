@@ -72,6 +72,8 @@ struct PassArgs {
   int nsig;     // PK_INV_CURLY: output signals; block planes run signal-fastest
                 // (p = x*nsig + s) so the 6 signals of one x share L2-resident inputs
   unsigned long long* dbg;  // optional phase timestamps (tools/phase_timing.py)
+  int tma;       // 1: stage the input tile with 3D TMA copies (tensor map = kernel parameter)
+  int tma_rows;  // rows per TMA box (divides the staged row count)
 };
 
 // Phase timestamps of every 97th CTA (diagnostics only; dbg == nullptr in
@@ -134,9 +136,29 @@ SRK_DEV void tile_of(const PassArgs& a, int bid, int& plane, int& w0) {
   }
 }
 
+// TMA staging of a strided tile: rows [0, rows) x columns [w0, w0 + C) of one or
+// two source planes into the dense [row][C] staging layout (second plane at
+// +n*C), by one elected thread in rows/box 3D tensor copies.  Columns past the
+// plane end are zero-filled by the TMA bounds check.
+template <int C>
+__device__ __forceinline__ void tma_stage(cplx* sm, const CUtensorMap* tm, int w0, int rows, int box, int plA,
+                                          int plB, int boff, unsigned long long* bar) {
+  if (threadIdx.x == 0) {
+    const int nb = rows / box;
+    const unsigned bytes = (unsigned)(nb * box * C * 16) * (plB >= 0 ? 2u : 1u);
+    mbar_expect_tx(bar, bytes);
+    for (int b = 0; b < nb; ++b) tma_load_3d(sm + b * box * C, tm, 2 * w0, b * box, plA, bar);
+    if (plB >= 0)
+      for (int b = 0; b < nb; ++b) tma_load_3d(sm + boff + b * box * C, tm, 2 * w0, b * box, plB, bar);
+  }
+  cp_async_wait_all();  // this thread's twiddle-table copies
+  mbar_wait(bar, 0);
+  __syncthreads();
+}
+
 template <class Eng, int KIND, int SIGN, int FL = 0>
-__global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(const PassArgs a) {
-  extern __shared__ __align__(16) cplx smraw[];
+__global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(const PassArgs a, const __grid_constant__ CUtensorMap tm) {
+  extern __shared__ __align__(128) cplx smraw[];
   cplx* const sm = smraw + Eng::TWN;
   const cplx* const twp = Eng::kFast ? smraw : a.tw;
   if constexpr (Eng::kFast) tw_fill<Eng::M>(smraw, a.tw);  // ordered by the staging barrier
@@ -155,10 +177,24 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
   const int n = CTN ? 2 * Eng::M / 3 : a.n;
   const int in_rpb = (FL & PF_BIN) ? a.in_rpb : 0;
   const int out_rpb = (FL & PF_BOUT) ? a.out_rpb : 0;
+  // TMA staging: plain (unblocked) input rows of the fast engines
+  constexpr bool kTMA = Eng::kFast && !(FL & PF_BIN) && KIND != PK_INV_RHS;
+  __shared__ __align__(8) unsigned long long tbar;
+  const bool use_tma = kTMA && a.tma;
+  if (use_tma) {
+    if (threadIdx.x == 0) {
+      mbar_init(&tbar, 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+  }
 
   if constexpr (KIND == PK_INV) {
     const double sc = a.scale;
-    if constexpr (Eng::kFast) {
+    if (use_tma) {
+      tma_stage<C>(sm, &tm, w0, n, a.tma_rows, plane, -1, 0, &tbar);
+      SRK_TS(1)
+    } else if constexpr (Eng::kFast) {
       stage_rows<C>(sm, inp, n, rs, ncols, in_rpb, a.in_bstride);
       cp_async_wait_all();
       __syncthreads();
@@ -245,7 +281,10 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
     const bool use_kx = (s == 3 || s == 4);
     const cplx* __restrict__ pa = a.in + w0 + comp * a.comp_stride;
     const double sc = a.scale;
-    if constexpr (Eng::kFast) {
+    if (use_tma) {  // host guarantees comp_stride == in_plane_stride
+      tma_stage<C>(sm, &tm, w0, n, a.tma_rows, comp, -1, 0, &tbar);
+      SRK_TS(1)
+    } else if constexpr (Eng::kFast) {
       stage_rows<C>(sm, pa, n, rs, ncols, in_rpb, a.in_bstride);
       cp_async_wait_all();
       __syncthreads();
@@ -281,7 +320,10 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
     const int mycol = Eng::col_of(threadIdx.x);
     const double kz = (double)(w0 + mycol) * a.ck2;
     cplx* sb_ = sm + (is_curl ? n * C : 0);
-    if constexpr (Eng::kFast) {
+    if (use_tma) {
+      tma_stage<C>(sm, &tm, w0, n, a.tma_rows, ca * X + x, is_curl ? cb * X + x : -1, n * C, &tbar);
+      SRK_TS(1)
+    } else if constexpr (Eng::kFast) {
       stage_rows<C>(sm, pa, n, rs, ncols, in_rpb, a.in_bstride);
       if (is_curl) stage_rows<C>(sm + n * C, pb, n, rs, ncols, in_rpb, a.in_bstride);
       cp_async_wait_all();
@@ -308,7 +350,10 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_colpass(c
     const bool zn = a.zero_nyq != 0;
     const bool zdc = (a.zero_dc_imag != 0) && (w0 == 0) && (a.y0 == 0);
     const double sc = a.scale;
-    if constexpr (Eng::kFast) {
+    if (use_tma) {
+      tma_stage<C>(sm, &tm, w0, M, a.tma_rows, plane, -1, 0, &tbar);
+      SRK_TS(1)
+    } else if constexpr (Eng::kFast) {
       stage_rows<C>(sm, inp, M, rs, ncols, in_rpb, a.in_bstride);
       cp_async_wait_all();
       __syncthreads();

@@ -195,6 +195,60 @@ int curly_xblk(int X) {
   return 1;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
+typedef CUresult (*srk_encode_tiled_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                         const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                         CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                         CUtensorMapFloatOOBfill);
+srk_encode_tiled_fn encode_tiled() {
+  static srk_encode_tiled_fn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (getenv("SRK_NO_TMA")) return (srk_encode_tiled_fn) nullptr;  // A/B switch: cp.async staging
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (srk_encode_tiled_fn) nullptr;
+    return (srk_encode_tiled_fn)f;
+  }();
+  return fn;
+}
+
+CUtensorMapL2promotion promo() {
+  static const int v = getenv("SRK_TMA_PROMO") ? atoi(getenv("SRK_TMA_PROMO")) : 3;
+  return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                         : v == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
+
+// Tensor map of a strided pass's input: 3D {2*Qp doubles, rows, planes}, box
+// {2*C doubles, rows/nb <= 256, 1}.  Leaves a.tma = 0 when TMA does not apply
+// (generic lengths, blocked slab rows, 2D curl kinds, box constraints).
+void setup_tma(int kind, int cols, PassArgs& a, CUtensorMap* tm) {
+  a.tma = 0;
+  const bool inv = kind == KK_INV || kind == KK_INV_P || kind == KK_INV_KX || kind == KK_INV_KX_SLAB ||
+                   kind == KK_INV_CURLY;
+  const bool fwd = kind == KK_FWD || kind == KK_FWD_P || kind == KK_FWD_P_SLABO;
+  if (!(inv || fwd) || a.in_rpb != 0 || !g_fast->count(a.M)) return;
+  static const int skip_mask = getenv("SRK_TMA_SKIP") ? atoi(getenv("SRK_TMA_SKIP")) : 0;  // experiments
+  if (skip_mask & (1 << kind)) return;
+  if ((kind == KK_INV_KX || kind == KK_INV_KX_SLAB) && a.comp_stride != a.in_plane_stride) return;
+  srk_encode_tiled_fn enc = encode_tiled();
+  if (!enc) return;
+  const int rows = fwd ? a.M : a.n;
+  const int nb = (rows + 255) / 256;
+  if (rows % nb) return;
+  const int box = rows / nb;
+  cuuint64_t dims[3] = {(cuuint64_t)(2 * a.Qp), (cuuint64_t)rows, (cuuint64_t)a.planes};
+  cuuint64_t strides[2] = {(cuuint64_t)a.row_stride * 16, (cuuint64_t)a.in_plane_stride * 16};
+  cuuint32_t boxd[3] = {(cuuint32_t)(2 * cols), (cuuint32_t)box, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  if (enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)a.in, dims, strides, boxd, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, promo(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return;
+  a.tma = 1;
+  a.tma_rows = box;
+}
+
 int launch_col(srk_plan* p, int kind, PassArgs a, cudaStream_t st) {
   const bool padded_kind = kind == KK_INV_P || kind == KK_FWD_P || kind == KK_INV_RHS || kind >= KK_INV_RHS_SLAB;
   if (padded_kind && 3 * a.n != 2 * a.M) return fail(SRK_ERR_INVALID, "padded pass needs M = 3n/2");
@@ -207,7 +261,10 @@ int launch_col(srk_plan* p, int kind, PassArgs a, cudaStream_t st) {
   const long long grid = (long long)a.planes * a.tpp;
   if (grid <= 0) return SRK_OK;
   a.dbg = (p->dbg && p->last_launches == p->dbg_launch) ? p->dbg : nullptr;
-  void* args[] = {&a};
+  alignas(64) CUtensorMap tm;
+  memset(&tm, 0, sizeof(tm));
+  setup_tma(kind, e.cols, a, &tm);
+  void* args[] = {&a, &tm};
   static const int smem_pad = getenv("SRK_SMEM_PAD") ? atoi(getenv("SRK_SMEM_PAD")) : 0;  // experiments: occupancy
   if (smem_pad) {
     e.smem += smem_pad;

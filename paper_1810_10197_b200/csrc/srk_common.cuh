@@ -2,6 +2,7 @@
 // and the in-register DFT butterflies used by the FFT engines (fft_engine.cuh).
 #pragma once
 
+#include <cuda.h>  // CUtensorMap
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -241,6 +242,17 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
       "r"(phase)
+      : "memory");
+}
+
+// 3D TMA tile load (cp.async.bulk.tensor) completing on an mbarrier; the tensor
+// map is a __grid_constant__ kernel parameter.
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2,
+                                            unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_u32(dst)),
+      "l"((unsigned long long)tm), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
 }
 
