@@ -400,6 +400,7 @@ struct ZArgs {
   long long in_sig_stride, out_sig_stride;  // complex elements (P*K) or real (P*M)
   int zero_nyq;  // R2C: zero the kz = n/2 plane (narrow)
   int mode;      // unused (kept for ABI stability of the struct)
+  int pf_dist;   // NS3 z-pass: > 0 prefetch the inputs of block bid + pf_dist into L2
   unsigned long long* dbg;  // optional phase timestamps (tools/phase_timing.py)
 };
 
@@ -625,6 +626,14 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
       const int pp = g / S, s = g - pp * S, pen = p0 + pp;
       if (pen < a.P) bulk_g2s(stg + g * K, a.in + s * a.in_sig_stride + (long long)pen * K, (unsigned)(K * 16), &mbar);
     }
+    // warm L2 with the rows of the pencil pair about one wave of CTAs ahead
+    if (a.pf_dist) {
+      const int q0 = p0 + 2 * a.pf_dist;
+      for (int g = 0; g < 2 * S; ++g) {
+        const int pp = g / S, s = g - pp * S, pen = q0 + pp;
+        if (pen < a.P) bulk_prefetch_l2(a.in + s * a.in_sig_stride + (long long)pen * K, (unsigned)(K * 16));
+      }
+    }
   }
   if (p0 + 1 >= a.P)
     for (int i = tid; i < S * K; i += NT) stg[S * K + i] = cmk(0.0, 0.0);
@@ -718,20 +727,28 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
   }
   __syncthreads();
   SRK_TS(4)
-  // ---- extraction: two real spectra per complex column, K modes, kz = n/2 zeroed ----
+  // ---- extraction: two real spectra per complex column, K modes, kz = n/2 zeroed.
+  // The 6 output rows are assembled in the idle tile columns So..S-1 and
+  // written by 1D TMA bulk stores (one elected thread), so the CTA retires
+  // without waiting on per-thread global stores.
+  static_assert(2 * So * K <= (S - So) * L::PITCH, "output rows must fit the idle tile columns");
+  cplx* const ost = sm + So * L::PITCH;  // [g][K], g = 2c + h
   for (int i = tid; i < So * K; i += NT) {
     const int c = i / K, k = i - (i / K) * K;
     const bool live = k != K - 1;
     const cplx Zk = live ? sm[L::idx(k, c)] : cmk(0.0, 0.0);
     const cplx Zm = live ? sm[L::idx(k == 0 ? 0 : M - k, c)] : cmk(0.0, 0.0);
-    const cplx A = cmk(0.5 * (Zk.x + Zm.x), 0.5 * (Zk.y - Zm.y));
-    const cplx B = cmk(0.5 * (Zk.y + Zm.y), -0.5 * (Zk.x - Zm.x));
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int g = 2 * c + h;
+    ost[(2 * c) * K + k] = cmk(0.5 * (Zk.x + Zm.x), 0.5 * (Zk.y - Zm.y));
+    ost[(2 * c + 1) * K + k] = cmk(0.5 * (Zk.y + Zm.y), -0.5 * (Zk.x - Zm.x));
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  if (tid == 0) {
+    for (int g = 0; g < 2 * So; ++g) {
       const int pp = g / So, s = g - pp * So, pen = p0 + pp;
-      if (pen < a.P) a.out[s * a.out_sig_stride + (long long)pen * K + k] = h ? B : A;
+      if (pen < a.P) bulk_s2g(a.out + s * a.out_sig_stride + (long long)pen * K, ost + g * K, (unsigned)(K * 16));
     }
+    bulk_commit_and_wait_read();
   }
   if (a.dbg) {
     __syncthreads();
