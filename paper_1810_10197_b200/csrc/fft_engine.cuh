@@ -53,6 +53,8 @@ struct RowTile {
   }
   SRK_DEV static int col_of(int tid, int) { return tid % C_; }
   SRK_DEV static int tj_of(int tid, int) { return tid / C_; }
+  // idx(base + q, c) - idx(base, c) for base a multiple of 8
+  static constexpr int roff(int q) { return C_ >= 8 ? q * C_ : (q + (q >> 3)) * 4; }
 };
 
 template <int M_, int C_, int MINPITCH = 0>
@@ -66,6 +68,7 @@ struct ColTile {
   __device__ __forceinline__ static int idx(int row, int col) { return col * PITCH + row + (row >> 3); }
   SRK_DEV static int col_of(int tid, int tpc) { return tid / tpc; }
   SRK_DEV static int tj_of(int tid, int tpc) { return tid % tpc; }
+  static constexpr int roff(int q) { return q + (q >> 3); }
 };
 
 struct GenPlan {
@@ -314,6 +317,95 @@ struct FastFFT {
     const bool act = (tid < NT) && (col < ncols);
     __builtin_assume(tj >= 0 && tj < TPC);
     FastStageW<M_, E_, L, SIGN, LD_SMEM, ST_SMEM, 1, Rs...>::go(sm, tw, col, tj, act, ld, st);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// One butterfly per thread per stage: the stage with radix R runs on M/R
+// threads per column (the rest idle), so a plan may mix radices that do not
+// divide a common per-thread element count -- e.g. 768 = 24 * 32 in two
+// stages: one shared-memory round trip instead of two for 8 * 8 * 12.
+// ---------------------------------------------------------------------------
+template <int M, class L, int SIGN, bool LD_SMEM, bool ST_SMEM, int Ls, int R, int... Rest>
+struct OneStage {
+  template <class LD, class ST>
+  __device__ __forceinline__ static void go(cplx* sm, const cplx* tw, int col, int tj, bool act_col, LD& ld,
+                                            ST& st) {
+    constexpr int STRIDE = M / R;  // butterflies per column
+    constexpr bool FIRST = (Ls == 1);
+    constexpr bool LAST = (sizeof...(Rest) == 0);
+    const bool act = act_col && tj < STRIDE;
+    const int j = tj;
+    cplx v[R];
+    if (act) {
+      if constexpr (FIRST) {
+#pragma unroll
+        for (int t = 0; t < R; ++t) v[t] = ld(j + t * STRIDE, col);
+      } else if constexpr (STRIDE % 8 == 0) {
+        const int a0 = L::idx(j, col);
+#pragma unroll
+        for (int t = 0; t < R; ++t) v[t] = sm[a0 + t * (STRIDE / 8) * L::STEP8];
+      } else {
+#pragma unroll
+        for (int t = 0; t < R; ++t) v[t] = sm[L::idx(j + t * STRIDE, col)];
+      }
+    }
+    if constexpr ((!FIRST || LD_SMEM) && (!LAST || ST_SMEM)) __syncthreads();
+    if (act) {
+      const unsigned k = (unsigned)j % (unsigned)Ls;
+      if constexpr (Ls > 1) stage_twiddle<M, R, SIGN>(v, tw, k * (unsigned)(M / (Ls * R)));
+      DFT<R, SIGN>::run(v);
+      const int base = (int)(((unsigned)j - k) * (unsigned)R + k);
+      if constexpr (LAST) {
+#pragma unroll
+        for (int q = 0; q < R; ++q) st(base + q * Ls, col, v[q]);
+      } else if constexpr (Ls % 8 == 0) {
+        const int a0 = L::idx(base, col);
+#pragma unroll
+        for (int q = 0; q < R; ++q) sm[a0 + q * (Ls / 8) * L::STEP8] = v[q];
+      } else if constexpr (Ls == 1 && R % 8 == 0) {
+        const int a0 = L::idx(base, col);  // base = j*R, a multiple of 8
+#pragma unroll
+        for (int q = 0; q < R; ++q) sm[a0 + L::roff(q)] = v[q];
+      } else {
+#pragma unroll
+        for (int q = 0; q < R; ++q) sm[L::idx(base + q * Ls, col)] = v[q];
+      }
+    }
+    if constexpr (!LAST) {
+      __syncthreads();
+      OneStage<M, L, SIGN, LD_SMEM, ST_SMEM, Ls * R, Rest...>::go(sm, tw, col, tj, act_col, ld, st);
+    }
+  }
+};
+
+template <int A, int... Bs>
+constexpr int cmin() {
+  if constexpr (sizeof...(Bs) == 0)
+    return A;
+  else
+    return A < cmin<Bs...>() ? A : cmin<Bs...>();
+}
+
+template <int M_, class L, int... Rs>
+struct FastFFT1 {
+  static constexpr int M = M_;
+  static constexpr int TPC = M_ / cmin<Rs...>();
+  static constexpr int C = L::C;
+  static constexpr int NT = C * TPC;
+  static constexpr bool kFast = true;
+  static constexpr int TWN = TwTab<M_>::N;
+  static_assert((1 * ... * Rs) == M_, "radices must multiply to M");
+  SRK_DEV static int col_of(int tid) { return L::col_of(tid, TPC); }
+  template <int SIGN, bool LD_SMEM, bool ST_SMEM, class LD, class ST>
+  __device__ __forceinline__ static void run(const GenPlan&, cplx* sm, const cplx* __restrict__ tw, int ncols,
+                                             LD& ld, ST& st) {
+    const int tid = threadIdx.x;
+    const int col = L::col_of(tid, TPC);
+    const int tj = L::tj_of(tid, TPC);
+    const bool act = (tid < NT) && (col < ncols);
+    __builtin_assume(tj >= 0 && tj < TPC);
+    OneStage<M_, L, SIGN, LD_SMEM, ST_SMEM, 1, Rs...>::go(sm, tw, col, tj, act, ld, st);
   }
 };
 

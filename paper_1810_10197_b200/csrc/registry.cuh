@@ -101,6 +101,30 @@ struct GenCols {
     t[KK_Z_B2] = SRK_ENTRY((k_zpass<E4, Z4, ZOP_B2>), E4, Z4::SIZE * 16);                          \
   }
 
+// Strided passes on the one-butterfly-per-thread engine (radices SR, CS
+// columns); z passes on FastFFT<M, E, ...> as in SRK_DEFINE_SIZE_F.
+#define SRK_DEFINE_SIZE_1(NAME, M, CS, SR, E, EF, FR, ...)                                         \
+  void NAME(KEntry* t) {                                                                           \
+    using SL = RowTile<M, CS>;                                                                     \
+    using SE = FastFFT1<M, SL, SRK_UNPAREN SR>;                                                    \
+    SRK_STRIDED_KINDS(M, CS)                                                                       \
+    using Z4 = ColTile<M, 4>;                                                                      \
+    using Z3 = ColTile<M, 3>;                                                                      \
+    using Z6 = ColTile<M, 6>;                                                                      \
+    using Z7 = ColTile<M, 7>;                                                                      \
+    using E4 = FastFFT<M, E, Z4, __VA_ARGS__>;                                                     \
+    using E3 = FastFFT<M, E, Z3, __VA_ARGS__>;                                                     \
+    using E6 = FastFFT<M, E, Z6, __VA_ARGS__>;                                                     \
+    using E7 = FastFFT<M, E, Z7, __VA_ARGS__>;                                                     \
+    using E6F = FastFFT<M, EF, Z6, SRK_UNPAREN FR>;                                                \
+    t[KK_Z_C2R] = SRK_ENTRY((k_zpass<E4, Z4, ZOP_C2R>), E4, Z4::SIZE * 16);                        \
+    t[KK_Z_R2C] = SRK_ENTRY((k_zpass<E4, Z4, ZOP_R2C>), E4, Z4::SIZE * 16);                        \
+    t[KK_Z_NS3] = SRK_ENTRY((k_zpass<E6, Z6, ZOP_NS3, E6F>), E6, Z6::SIZE * 16);                   \
+    t[KK_Z_NS2] = SRK_ENTRY((k_zpass<E3, Z3, ZOP_NS2>), E3, Z3::SIZE * 16);                        \
+    t[KK_Z_B3] = SRK_ENTRY((k_zpass<E7, Z7, ZOP_B3>), E7, Z7::SIZE * 16);                          \
+    t[KK_Z_B2] = SRK_ENTRY((k_zpass<E4, Z4, ZOP_B2>), E4, Z4::SIZE * 16);                          \
+  }
+
 // Separate strided-pass plan (ES elements/thread, CSS columns, radices SR) and
 // z-pass plan (E, CS, radices ...).
 #define SRK_DEFINE_SIZE_S(NAME, M, ES, CSS, SR, E, ...)                                             \

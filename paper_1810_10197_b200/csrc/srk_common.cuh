@@ -27,29 +27,30 @@ SRK_DEV cplx cmul_si(cplx a) {
 }
 
 // ---------------------------------------------------------------------------
-// Multiply by the compile-time constant exp(SIGN * 2*pi*i * m / 48).
-// Cheap paths for multiples of pi/4; generic complex multiply otherwise.
+// Multiply by the compile-time constant exp(SIGN * 2*pi*i * m / 96) (96 =
+// lcm of the composite radices 6, 8, 12, 16, 24, 32).  Cheap paths for
+// multiples of pi/4; generic complex multiply otherwise.
 // ---------------------------------------------------------------------------
-template <int M48, int SIGN>
+template <int M96, int SIGN>
 SRK_DEV cplx twc(cplx a) {
-  constexpr int m = ((M48 % 48) + 48) % 48;
+  constexpr int m = ((M96 % 96) + 96) % 96;
   if constexpr (m == 0) {
     return a;
-  } else if constexpr (m == 12) {
-    return cmul_si<SIGN>(a);
   } else if constexpr (m == 24) {
+    return cmul_si<SIGN>(a);
+  } else if constexpr (m == 48) {
     return make_double2(-a.x, -a.y);
-  } else if constexpr (m == 36) {
+  } else if constexpr (m == 72) {
     return cmul_si<-SIGN>(a);
-  } else if constexpr (m == 6 || m == 18 || m == 30 || m == 42) {
+  } else if constexpr (m == 12 || m == 36 || m == 60 || m == 84) {
     constexpr double r = 0.7071067811865476;  // sqrt(2)/2
-    constexpr double c = kcos48(m) > 0 ? 1.0 : -1.0;
-    constexpr double s = (ksin48(m) > 0 ? 1.0 : -1.0) * (SIGN > 0 ? 1.0 : -1.0);
+    constexpr double c = kcos96(m) > 0 ? 1.0 : -1.0;
+    constexpr double s = (ksin96(m) > 0 ? 1.0 : -1.0) * (SIGN > 0 ? 1.0 : -1.0);
     // (a.x + i a.y)(c + i s) r
     return make_double2((c * a.x - s * a.y) * r, (s * a.x + c * a.y) * r);
   } else {
-    constexpr double c = kcos48(m);
-    constexpr double s = (SIGN > 0 ? 1.0 : -1.0) * ksin48(m);
+    constexpr double c = kcos96(m);
+    constexpr double s = (SIGN > 0 ? 1.0 : -1.0) * ksin96(m);
     return make_double2(fma(a.x, c, -a.y * s), fma(a.x, s, a.y * c));
   }
 }
@@ -137,10 +138,10 @@ struct DFT<7, SIGN> : DFTPrime<7, SIGN> {};
 template <int A, int B, int SIGN>
 struct DFTComposite {
   static constexpr int R = A * B;
-  static_assert(48 % R == 0, "composite radix must divide 48");
+  static_assert(96 % R == 0, "composite radix must divide 96");
   template <int b, int q1>
   SRK_DEV static void tw(cplx (&u)[B][A]) {
-    u[b][q1] = twc<(b * q1 * (48 / R)), SIGN>(u[b][q1]);
+    u[b][q1] = twc<(b * q1 * (96 / R)), SIGN>(u[b][q1]);
   }
   template <int b, int q1>
   SRK_DEV static void tw_row(cplx (&u)[B][A]) {
@@ -186,6 +187,8 @@ template <int SIGN>
 struct DFT<16, SIGN> : DFTComposite<4, 4, SIGN> {};
 template <int SIGN>
 struct DFT<24, SIGN> : DFTComposite<8, 3, SIGN> {};
+template <int SIGN>
+struct DFT<32, SIGN> : DFTComposite<4, 8, SIGN> {};
 
 // ---------------------------------------------------------------------------
 // Row maps for the 3/2-rule padding (spectral.py:229-258 widen, :276-301 narrow).
