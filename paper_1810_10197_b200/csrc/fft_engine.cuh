@@ -114,18 +114,47 @@ __device__ __forceinline__ cplx tw_get(const cplx* tws, unsigned m) {
   return (q & 2u) ? make_double2(-a, -b) : make_double2(a, b);
 }
 
-// v[t] *= w^t, w = exp(SIGN 2 pi i kts / M), t = 1..R-1: the power-of-two
-// exponents come from the table, the others are products of those (at most
-// two extra roundings, ~1e-16 relative; half the shared-memory lookups --
-// measured 0.8 ms faster per 512^3 RHS than looking every exponent up).
+// v[t] *= w^t, w = exp(SIGN 2 pi i kts / M), t = 1..R-1: only w^1, w^2, w^4
+// (and w^8, w^16) come from the table; w^(8a+b) = w^(8a) * w^b is formed on
+// the fly, so at most 10 powers are live (a few extra roundings, ~5e-16
+// relative).  Products instead of per-exponent table lookups measured 0.8 ms
+// faster per 512^3 RHS; SRK_TW_BINARY keeps all R-1 powers (binary products).
+template <int M, int SIGN>
+__device__ __forceinline__ cplx tw_pow(const cplx* tw, unsigned e) {
+  cplx w = tw_get<M>(tw, e);
+  if (SIGN > 0) w.y = -w.y;
+  return w;
+}
 template <int M, int R, int SIGN>
 __device__ __forceinline__ void stage_twiddle(cplx* v, const cplx* tw, unsigned kts) {
+#ifndef SRK_TW_BINARY
+  constexpr int B = R < 8 ? R : 8;
+  cplx wb[8];
+#pragma unroll
+  for (int b = 1; b < B; ++b) {
+    if ((b & (b - 1)) == 0)
+      wb[b] = tw_pow<M, SIGN>(tw, (unsigned)b * kts);
+    else
+      wb[b] = cmul(wb[b & (b - 1)], wb[b & -b]);
+    v[b] = cmul(v[b], wb[b]);
+  }
+  if constexpr (R > 8) {
+    cplx w8 = tw_pow<M, SIGN>(tw, 8u * kts);
+    cplx w16 = (R > 16) ? tw_pow<M, SIGN>(tw, 16u * kts) : w8;
+#pragma unroll
+    for (int a = 1; 8 * a < R; ++a) {
+      const cplx wa = a == 1 ? w8 : (a == 2 ? w16 : cmul(w8, w16));
+      v[8 * a] = cmul(v[8 * a], wa);
+#pragma unroll
+      for (int b = 1; b < 8 && 8 * a + b < R; ++b) v[8 * a + b] = cmul(v[8 * a + b], cmul(wa, wb[b]));
+    }
+  }
+#else
   cplx pw[R];
 #pragma unroll
   for (int t = 1; t < R; ++t) {
     if ((t & (t - 1)) == 0) {
-      pw[t] = tw_get<M>(tw, (unsigned)t * kts);
-      if (SIGN > 0) pw[t].y = -pw[t].y;
+      pw[t] = tw_pow<M, SIGN>(tw, (unsigned)t * kts);
     } else {
       int hb = 1;
       while (2 * hb <= t) hb *= 2;
@@ -134,6 +163,8 @@ __device__ __forceinline__ void stage_twiddle(cplx* v, const cplx* tw, unsigned 
   }
 #pragma unroll
   for (int t = 1; t < R; ++t) v[t] = cmul(v[t], pw[t]);
+#endif
+  static_assert(R <= 32, "stage_twiddle covers radices up to 32");
 }
 
 template <bool WS, int TPC>
@@ -176,7 +207,8 @@ struct FastStage {
         }
       }
     }
-    if constexpr ((!FIRST || LD_SMEM) && (!LAST || ST_SMEM)) __syncthreads();
+    // twiddles + butterflies before the load->store barrier: only the
+    // transformed values are live across it
     if (act) {
 #pragma unroll
       for (int b = 0; b < NB; ++b) {
@@ -188,6 +220,14 @@ struct FastStage {
           stage_twiddle<M, R, SIGN>(v[b], tw, kts);
         }
         DFT<R, SIGN>::run(v[b]);
+      }
+    }
+    if constexpr ((!FIRST || LD_SMEM) && (!LAST || ST_SMEM)) __syncthreads();
+    if (act) {
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const unsigned j = (unsigned)tj + (unsigned)(b * TPC);
+        const unsigned k = j % (unsigned)Ls;
         const int base = (int)((j - k) * (unsigned)R + k);
         if constexpr (LAST) {
 #pragma unroll
@@ -242,12 +282,8 @@ struct FastStageW {
         }
       }
     }
-    if constexpr ((!FIRST || LD_SMEM) && (!LAST || ST_SMEM)) {
-      if constexpr (FIRST)
-        __syncthreads();  // staging may alias other columns
-      else
-        stage_sync<true, TPC>();
-    }
+    // twiddles + butterflies before the load->store barrier: only the
+    // transformed values are live across it
     if (act) {
 #pragma unroll
       for (int b = 0; b < NB; ++b) {
@@ -259,6 +295,19 @@ struct FastStageW {
           stage_twiddle<M, R, SIGN>(v[b], tw, kts);
         }
         DFT<R, SIGN>::run(v[b]);
+      }
+    }
+    if constexpr ((!FIRST || LD_SMEM) && (!LAST || ST_SMEM)) {
+      if constexpr (FIRST)
+        __syncthreads();  // staging may alias other columns
+      else
+        stage_sync<true, TPC>();
+    }
+    if (act) {
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const unsigned j = (unsigned)tj + (unsigned)(b * TPC);
+        const unsigned k = j % (unsigned)Ls;
         const int base = (int)((j - k) * (unsigned)R + k);
         if constexpr (LAST) {
 #pragma unroll
@@ -350,11 +399,13 @@ struct OneStage {
         for (int t = 0; t < R; ++t) v[t] = sm[L::idx(j + t * STRIDE, col)];
       }
     }
-    if constexpr ((!FIRST || LD_SMEM) && (!LAST || ST_SMEM)) __syncthreads();
-    if (act) {
-      const unsigned k = (unsigned)j % (unsigned)Ls;
+    const unsigned k = (unsigned)j % (unsigned)Ls;
+    if (act) {  // twiddles + butterfly before the load->store barrier
       if constexpr (Ls > 1) stage_twiddle<M, R, SIGN>(v, tw, k * (unsigned)(M / (Ls * R)));
       DFT<R, SIGN>::run(v);
+    }
+    if constexpr ((!FIRST || LD_SMEM) && (!LAST || ST_SMEM)) __syncthreads();
+    if (act) {
       const int base = (int)(((unsigned)j - k) * (unsigned)R + k);
       if constexpr (LAST) {
 #pragma unroll

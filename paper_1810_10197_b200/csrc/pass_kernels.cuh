@@ -74,6 +74,8 @@ struct PassArgs {
   unsigned long long* dbg;  // optional phase timestamps (tools/phase_timing.py)
   int tma;       // 1: stage the input tile with 3D TMA copies (tensor map = kernel parameter)
   int tma_rows;  // rows per TMA box (divides the staged row count)
+  int tma_out;   // 1: inverse passes write their output tile with 3D TMA stores
+  int tmo_rows;  // rows per output box (divides M)
 };
 
 // Phase timestamps of every 97th CTA (diagnostics only; dbg == nullptr in
@@ -157,7 +159,8 @@ __device__ __forceinline__ void tma_stage(cplx* sm, const CUtensorMap* tm, int w
 }
 
 template <class Eng, int KIND, int SIGN, int FL = 0>
-__global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : (Eng::NT <= 192 ? 2 : 1))) k_colpass(const PassArgs a, const __grid_constant__ CUtensorMap tm) {
+__global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : (Eng::NT <= 192 ? 2 : 1))) k_colpass(const PassArgs a, const __grid_constant__ CUtensorMap tm,
+                                                                  const __grid_constant__ CUtensorMap tmo) {
   extern __shared__ __align__(128) cplx smraw[];
   cplx* const sm = smraw + Eng::TWN;
   const cplx* const twp = Eng::kFast ? smraw : a.tw;
@@ -181,6 +184,27 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : (Eng::NT <= 192
   constexpr bool kTMA = Eng::kFast && !(FL & PF_BIN) && KIND != PK_INV_RHS;
   __shared__ __align__(8) unsigned long long tbar;
   const bool use_tma = kTMA && a.tma;
+  // TMA output: the last stage writes a dense [M][C] tile in smem (over the
+  // FFT tile, after the stage's load barrier), then one thread stores it
+#ifdef SRK_NO_TMAO_BUILD
+  constexpr bool kTMAO = false;
+#else
+  // (K2 only: measured 5.48 -> 5.30 ms at 512^3; the x-pass K1, whose output
+  // rows are 2 MB apart, was slower with TMA stores, 2.98 -> 3.43 ms)
+  constexpr bool kTMAO = Eng::kFast && !(FL & PF_BOUT) && KIND == PK_INV_CURLY;
+#endif
+  const bool use_tmo = kTMAO && a.tma_out;
+  auto flush_out = [&]() {
+    if (use_tmo) {
+      fence_proxy_async_smem();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (int b = 0; b < M / a.tmo_rows; ++b)
+          tma_store_3d(&tmo, sm + b * a.tmo_rows * C, 2 * w0, b * a.tmo_rows, plane);
+        bulk_commit_and_wait_read();
+      }
+    }
+  };
   if (use_tma) {
     if (threadIdx.x == 0) {
       mbar_init(&tbar, 1);
@@ -208,8 +232,14 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : (Eng::NT <= 192
       const double f = ok ? sc : 0.0;
       return cmk(v.x * f, v.y * f);
     };
-    auto st = [&](int row, int col, cplx v) { outp[row_off(row, rs, out_rpb, a.out_bstride) + (unsigned)col] = v; };
-    Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, twp, ncols, ld, st);
+    auto st = [&](int row, int col, cplx v) {
+      if (use_tmo)
+        sm[row * C + col] = v;
+      else
+        outp[row_off(row, rs, out_rpb, a.out_bstride) + (unsigned)col] = v;
+    };
+    Eng::template run<SIGN, Eng::kFast, kTMAO>(a.gp, sm, twp, ncols, ld, st);
+    flush_out();
   } else if constexpr (KIND == PK_INV_RHS) {
     // plane = signal s: [u_0..u_{d-1}, w (3 comps in 3D, 1 in 2D), rho]
     const int d = a.dims;
@@ -299,8 +329,14 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : (Eng::NT <= 192
       const double f = ok ? (use_kx ? kx * sc : sc) : 0.0;
       return cmk(u.x * f, u.y * f);
     };
-    auto st = [&](int row, int col, cplx v) { outp[row_off(row, rs, out_rpb, a.out_bstride) + (unsigned)col] = v; };
-    Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, twp, ncols, ld, st);
+    auto st = [&](int row, int col, cplx v) {
+      if (use_tmo)
+        sm[row * C + col] = v;
+      else
+        outp[row_off(row, rs, out_rpb, a.out_bstride) + (unsigned)col] = v;
+    };
+    Eng::template run<SIGN, Eng::kFast, kTMAO>(a.gp, sm, twp, ncols, ld, st);
+    flush_out();
   } else if constexpr (KIND == PK_INV_CURLY) {
     // 3D K2.  plane = (s, x), s over [u0, u1, u2, w0, w1, w2, (rho)]; the input
     // planes are the K1 signals [U0, U1, U2, X1 = F(kx u1), X2 = F(kx u2), R]:
@@ -344,8 +380,14 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : (Eng::NT <= 192
       cplx v = is_curl ? cmk(-df.y, df.x) : A;
       return ok ? v : cmk(0.0, 0.0);
     };
-    auto st = [&](int row, int col, cplx v) { outp[row_off(row, rs, out_rpb, a.out_bstride) + (unsigned)col] = v; };
-    Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, twp, ncols, ld, st);
+    auto st = [&](int row, int col, cplx v) {
+      if (use_tmo)
+        sm[row * C + col] = v;
+      else
+        outp[row_off(row, rs, out_rpb, a.out_bstride) + (unsigned)col] = v;
+    };
+    Eng::template run<SIGN, Eng::kFast, kTMAO>(a.gp, sm, twp, ncols, ld, st);
+    flush_out();
   } else {  // PK_FWD: forward C2C + truncation (+ scale, Nyquist / DC-imag zeroing)
     const bool zn = a.zero_nyq != 0;
     const bool zdc = (a.zero_dc_imag != 0) && (w0 == 0) && (a.y0 == 0);

@@ -262,6 +262,28 @@ int zpass_prefetch_distance() {
   return d;
 }
 
+// Output tensor map of the 3D K2 pass (y inverse): {2*Qp doubles, M rows,
+// planes}, box {2*C, M/nb <= 256, 1} (plain output rows only).
+void setup_tma_out(int kind, int cols, PassArgs& a, CUtensorMap* tm) {
+  a.tma_out = 0;
+  const bool inv = kind == KK_INV_CURLY || kind == KK_INV_CURLY_SLAB;  // see kTMAO in k_colpass
+  if (!inv || a.out_rpb != 0 || !g_fast->count(a.M) || getenv("SRK_NO_TMAO")) return;
+  srk_encode_tiled_fn enc = encode_tiled();
+  if (!enc) return;
+  const int nb = (a.M + 255) / 256;
+  if (a.M % nb) return;
+  const int box = a.M / nb;
+  cuuint64_t dims[3] = {(cuuint64_t)(2 * a.Qp), (cuuint64_t)a.M, (cuuint64_t)a.planes};
+  cuuint64_t strides[2] = {(cuuint64_t)a.row_stride * 16, (cuuint64_t)a.out_plane_stride * 16};
+  cuuint32_t boxd[3] = {(cuuint32_t)(2 * cols), (cuuint32_t)box, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  if (enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)a.out, dims, strides, boxd, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return;
+  a.tma_out = 1;
+  a.tmo_rows = box;
+}
+
 int launch_col(srk_plan* p, int kind, PassArgs a, cudaStream_t st) {
   const bool padded_kind = kind == KK_INV_P || kind == KK_FWD_P || kind == KK_INV_RHS || kind >= KK_INV_RHS_SLAB;
   if (padded_kind && 3 * a.n != 2 * a.M) return fail(SRK_ERR_INVALID, "padded pass needs M = 3n/2");
@@ -277,7 +299,10 @@ int launch_col(srk_plan* p, int kind, PassArgs a, cudaStream_t st) {
   alignas(64) CUtensorMap tm;
   memset(&tm, 0, sizeof(tm));
   setup_tma(kind, e.cols, a, &tm);
-  void* args[] = {&a, &tm};
+  alignas(64) CUtensorMap tmo;
+  memset(&tmo, 0, sizeof(tmo));
+  setup_tma_out(kind, e.cols, a, &tmo);
+  void* args[] = {&a, &tm, &tmo};
   static const int smem_pad = getenv("SRK_SMEM_PAD") ? atoi(getenv("SRK_SMEM_PAD")) : 0;  // experiments: occupancy
   if (smem_pad) {
     e.smem += smem_pad;
