@@ -76,6 +76,14 @@ struct PassArgs {
   int tma_rows;  // rows per TMA box (divides the staged row count)
   int tma_out;   // 1: inverse passes write their output tile with 3D TMA stores
   int tmo_rows;  // rows per output box (divides M)
+  // Column groups (kz chunks of the pipelined slab RHS): the Qp columns of a
+  // plane are ngrp groups of kc columns; group g, local column c sits at
+  // memory column g*in_kst + in_k0 + c of the input (out_* for the output),
+  // global kz = kz0 + c.  Unchunked passes: ngrp = 1, kc = Qp, offsets 0
+  // (normalised by the host).  tpg = tiles per group, tpp = ngrp * tpg.
+  int kc, ngrp, tpg, in_k0, out_k0, kz0;
+  long long in_kst, out_kst;
+  long long in_rs, out_rs;  // row strides of input / output (0 -> row_stride)
 };
 
 // Phase timestamps of every 97th CTA (diagnostics only; dbg == nullptr in
@@ -115,9 +123,9 @@ __device__ __forceinline__ void stage_rows(cplx* dst, const cplx* __restrict__ s
 // output rows (slab all-to-all layouts).
 enum PassFlags { PF_CTN = 1, PF_BIN = 2, PF_BOUT = 4 };
 
-// Block -> (plane, first column) of a strided pass.
+// Block -> (plane, column group, first local column) of a strided pass.
 template <int KIND, int C>
-SRK_DEV void tile_of(const PassArgs& a, int bid, int& plane, int& w0) {
+SRK_DEV void tile_of(const PassArgs& a, int bid, int& plane, int& g, int& wl) {
   int wt;
   if (a.sig_minor) {
     plane = bid % a.planes;
@@ -126,7 +134,8 @@ SRK_DEV void tile_of(const PassArgs& a, int bid, int& plane, int& w0) {
     plane = bid / a.tpp;
     wt = bid % a.tpp;
   }
-  w0 = wt * C;
+  g = wt / a.tpg;
+  wl = (wt - g * a.tpg) * C;
   if constexpr (KIND == PK_INV_CURLY) {
     // blocks of XB x-planes, signal-major inside a block: the 5 input planes of
     // XB x values stay L2-resident while the 6 signals read them
@@ -138,20 +147,20 @@ SRK_DEV void tile_of(const PassArgs& a, int bid, int& plane, int& w0) {
   }
 }
 
-// TMA staging of a strided tile: rows [0, rows) x columns [w0, w0 + C) of one or
+// TMA staging of a strided tile: rows [0, rows) x local columns [wl, wl + C) of one or
 // two source planes into the dense [row][C] staging layout (second plane at
 // +n*C), by one elected thread in rows/box 3D tensor copies.  Columns past the
 // plane end are zero-filled by the TMA bounds check.
 template <int C>
-__device__ __forceinline__ void tma_stage(cplx* sm, const CUtensorMap* tm, int w0, int rows, int box, int plA,
-                                          int plB, int boff, unsigned long long* bar) {
+__device__ __forceinline__ void tma_stage(cplx* sm, const CUtensorMap* tm, int wl, int g, int rows, int box,
+                                          int plA, int plB, int boff, unsigned long long* bar) {
   if (threadIdx.x == 0) {
     const int nb = rows / box;
     const unsigned bytes = (unsigned)(nb * box * C * 16) * (plB >= 0 ? 2u : 1u);
     mbar_expect_tx(bar, bytes);
-    for (int b = 0; b < nb; ++b) tma_load_3d(sm + b * box * C, tm, 2 * w0, b * box, plA, bar);
+    for (int b = 0; b < nb; ++b) tma_load_4d(sm + b * box * C, tm, 2 * wl, g, b * box, plA, bar);
     if (plB >= 0)
-      for (int b = 0; b < nb; ++b) tma_load_3d(sm + boff + b * box * C, tm, 2 * w0, b * box, plB, bar);
+      for (int b = 0; b < nb; ++b) tma_load_4d(sm + boff + b * box * C, tm, 2 * wl, g, b * box, plB, bar);
   }
   cp_async_wait_all();  // this thread's twiddle-table copies
   mbar_wait(bar, 0);
@@ -170,12 +179,15 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : (Eng::NT <= 192
   SRK_TS_INIT(a.dbg, 3)
   SRK_TS(0)
   const int bid = blockIdx.x;
-  int plane, w0;
-  tile_of<KIND, C>(a, bid, plane, w0);
-  const int ncols = min(C, a.Qp - w0);
-  const unsigned rs = (unsigned)a.row_stride;  // intra-plane offsets fit in 32 bits
-  const cplx* __restrict__ inp = a.in + plane * a.in_plane_stride + w0;
-  cplx* __restrict__ outp = a.out + plane * a.out_plane_stride + w0;
+  int plane, g, wl;
+  tile_of<KIND, C>(a, bid, plane, g, wl);
+  const int ncols = min(C, a.kc - wl);
+  const long long w_in = (long long)g * a.in_kst + a.in_k0 + wl;    // memory column of the tile
+  const long long w_out = (long long)g * a.out_kst + a.out_k0 + wl;
+  const unsigned rs = (unsigned)a.in_rs;    // intra-plane offsets fit in 32 bits
+  const unsigned rso = (unsigned)a.out_rs;
+  const cplx* __restrict__ inp = a.in + plane * a.in_plane_stride + w_in;
+  cplx* __restrict__ outp = a.out + plane * a.out_plane_stride + w_out;
   const int M = CTN ? Eng::M : a.M;
   const int n = CTN ? 2 * Eng::M / 3 : a.n;
   const int in_rpb = (FL & PF_BIN) ? a.in_rpb : 0;
@@ -200,7 +212,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : (Eng::NT <= 192
       __syncthreads();
       if (threadIdx.x == 0) {
         for (int b = 0; b < M / a.tmo_rows; ++b)
-          tma_store_3d(&tmo, sm + b * a.tmo_rows * C, 2 * w0, b * a.tmo_rows, plane);
+          tma_store_4d(&tmo, sm + b * a.tmo_rows * C, 2 * wl, g, b * a.tmo_rows, plane);
         bulk_commit_and_wait_read();
       }
     }
@@ -216,7 +228,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : (Eng::NT <= 192
   if constexpr (KIND == PK_INV) {
     const double sc = a.scale;
     if (use_tma) {
-      tma_stage<C>(sm, &tm, w0, n, a.tma_rows, plane, -1, 0, &tbar);
+      tma_stage<C>(sm, &tm, wl, g, n, a.tma_rows, plane, -1, 0, &tbar);
       SRK_TS(1)
     } else if constexpr (Eng::kFast) {
       stage_rows<C>(sm, inp, n, rs, ncols, in_rpb, a.in_bstride);
@@ -236,7 +248,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : (Eng::NT <= 192
       if (use_tmo)
         sm[row * C + col] = v;
       else
-        outp[row_off(row, rs, out_rpb, a.out_bstride) + (unsigned)col] = v;
+        outp[row_off(row, rso, out_rpb, a.out_bstride) + (unsigned)col] = v;
     };
     Eng::template run<SIGN, Eng::kFast, kTMAO>(a.gp, sm, twp, ncols, ld, st);
     flush_out();
@@ -245,10 +257,10 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : (Eng::NT <= 192
     const int d = a.dims;
     const int wc = (d == 3) ? 3 : 1;
     const int s = plane;
-    const cplx* __restrict__ base = a.in + w0;  // component 0
+    const cplx* __restrict__ base = a.in + w_in;  // component 0 (2D: unchunked)
     // per-thread column constants (the column of a thread never changes)
     const int mycol = Eng::col_of(threadIdx.x);
-    const int q = w0 + mycol;
+    const int q = wl + mycol;
     double ky = 0.0, kz = 0.0;
     if (d == 3) {
       const int y = q / a.K, kzi = q - y * a.K;
@@ -299,7 +311,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : (Eng::NT <= 192
       const double f = ok ? sc : 0.0;
       return cmk(v.x * f, v.y * f);
     };
-    auto st = [&](int row, int col, cplx v) { outp[row_off(row, rs, out_rpb, a.out_bstride) + (unsigned)col] = v; };
+    auto st = [&](int row, int col, cplx v) { outp[row_off(row, rso, out_rpb, a.out_bstride) + (unsigned)col] = v; };
     Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, twp, ncols, ld, st);
   } else if constexpr (KIND == PK_INV_KX) {
     // 3D K1.  k_y and k_z are constant along x, so the x inverse commutes with
@@ -309,10 +321,10 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : (Eng::NT <= 192
     const int s = plane;
     const int comp = (s < 3) ? s : (s == 3 ? 1 : (s == 4 ? 2 : 3));
     const bool use_kx = (s == 3 || s == 4);
-    const cplx* __restrict__ pa = a.in + w0 + comp * a.comp_stride;
+    const cplx* __restrict__ pa = a.in + w_in + comp * a.comp_stride;
     const double sc = a.scale;
     if (use_tma) {  // host guarantees comp_stride == in_plane_stride
-      tma_stage<C>(sm, &tm, w0, n, a.tma_rows, comp, -1, 0, &tbar);
+      tma_stage<C>(sm, &tm, wl, g, n, a.tma_rows, comp, -1, 0, &tbar);
       SRK_TS(1)
     } else if constexpr (Eng::kFast) {
       stage_rows<C>(sm, pa, n, rs, ncols, in_rpb, a.in_bstride);
@@ -333,7 +345,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : (Eng::NT <= 192
       if (use_tmo)
         sm[row * C + col] = v;
       else
-        outp[row_off(row, rs, out_rpb, a.out_bstride) + (unsigned)col] = v;
+        outp[row_off(row, rso, out_rpb, a.out_bstride) + (unsigned)col] = v;
     };
     Eng::template run<SIGN, Eng::kFast, kTMAO>(a.gp, sm, twp, ncols, ld, st);
     flush_out();
@@ -351,13 +363,13 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : (Eng::NT <= 192
     else if (s == 4) { ca = 0; fa_kz = 1; cb = 4; is_curl = true; }
     else if (s == 5) { ca = 3; cb = 0; fb_ky = 1; is_curl = true; }
     else if (s == 6) { ca = cb = 5; }
-    const cplx* __restrict__ pa = a.in + (long long)(ca * X + x) * a.in_plane_stride + w0;
-    const cplx* __restrict__ pb = a.in + (long long)(cb * X + x) * a.in_plane_stride + w0;
+    const cplx* __restrict__ pa = a.in + (long long)(ca * X + x) * a.in_plane_stride + w_in;
+    const cplx* __restrict__ pb = a.in + (long long)(cb * X + x) * a.in_plane_stride + w_in;
     const int mycol = Eng::col_of(threadIdx.x);
-    const double kz = (double)(w0 + mycol) * a.ck2;
+    const double kz = (double)(a.kz0 + wl + mycol) * a.ck2;  // global kz of the column
     cplx* sb_ = sm + (is_curl ? n * C : 0);
     if (use_tma) {
-      tma_stage<C>(sm, &tm, w0, n, a.tma_rows, ca * X + x, is_curl ? cb * X + x : -1, n * C, &tbar);
+      tma_stage<C>(sm, &tm, wl, g, n, a.tma_rows, ca * X + x, is_curl ? cb * X + x : -1, n * C, &tbar);
       SRK_TS(1)
     } else if constexpr (Eng::kFast) {
       stage_rows<C>(sm, pa, n, rs, ncols, in_rpb, a.in_bstride);
@@ -384,16 +396,16 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : (Eng::NT <= 192
       if (use_tmo)
         sm[row * C + col] = v;
       else
-        outp[row_off(row, rs, out_rpb, a.out_bstride) + (unsigned)col] = v;
+        outp[row_off(row, rso, out_rpb, a.out_bstride) + (unsigned)col] = v;
     };
     Eng::template run<SIGN, Eng::kFast, kTMAO>(a.gp, sm, twp, ncols, ld, st);
     flush_out();
   } else {  // PK_FWD: forward C2C + truncation (+ scale, Nyquist / DC-imag zeroing)
     const bool zn = a.zero_nyq != 0;
-    const bool zdc = (a.zero_dc_imag != 0) && (w0 == 0) && (a.y0 == 0);
+    const bool zdc = (a.zero_dc_imag != 0) && (g == 0) && (a.kz0 + wl == 0) && (a.y0 == 0);
     const double sc = a.scale;
     if (use_tma) {
-      tma_stage<C>(sm, &tm, w0, M, a.tma_rows, plane, -1, 0, &tbar);
+      tma_stage<C>(sm, &tm, wl, g, M, a.tma_rows, plane, -1, 0, &tbar);
       SRK_TS(1)
     } else if constexpr (Eng::kFast) {
       stage_rows<C>(sm, inp, M, rs, ncols, in_rpb, a.in_bstride);
@@ -410,7 +422,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : (Eng::NT <= 192
       cplx o = cmk(v.x * sc, v.y * sc);
       if (c == -2) o = cmk(0.0, 0.0);
       if (zdc && c == 0 && col == 0) o.y = 0.0;
-      outp[row_off(c == -2 ? (n >> 1) : c, rs, out_rpb, a.out_bstride) + (unsigned)col] = o;
+      outp[row_off(c == -2 ? (n >> 1) : c, rso, out_rpb, a.out_bstride) + (unsigned)col] = o;
     };
     Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, twp, ncols, ld, st);
   }

@@ -220,9 +220,23 @@ CUtensorMapL2promotion promo() {
                          : v == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
 }
 
-// Tensor map of a strided pass's input: 3D {2*Qp doubles, rows, planes}, box
-// {2*C doubles, rows/nb <= 256, 1}.  Leaves a.tma = 0 when TMA does not apply
-// (generic lengths, blocked slab rows, 2D curl kinds, box constraints).
+// Tensor map of a strided pass's input: 4D {2*kc doubles, ngrp column groups,
+// rows, planes} based at the chunk's first column, box {2*C, 1, rows/nb <= 256,
+// 1}.  Leaves a.tma = 0 when TMA does not apply (generic lengths, blocked slab
+// rows, 2D curl kinds, box constraints).
+bool encode_pass_map(CUtensorMap* tm, const cplx* base, const PassArgs& a, long long kst, long long rs,
+                     long long pst, int rows, int box, int cols, CUtensorMapL2promotion pr) {
+  srk_encode_tiled_fn enc = encode_tiled();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)(2 * a.kc), (cuuint64_t)a.ngrp, (cuuint64_t)rows, (cuuint64_t)a.planes};
+  cuuint64_t strides[3] = {(cuuint64_t)(a.ngrp > 1 ? kst : a.kc) * 16, (cuuint64_t)rs * 16, (cuuint64_t)pst * 16};
+  cuuint32_t boxd[4] = {(cuuint32_t)(2 * cols), 1, (cuuint32_t)box, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)base, dims, strides, boxd, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, pr,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 void setup_tma(int kind, int cols, PassArgs& a, CUtensorMap* tm) {
   a.tma = 0;
   const bool inv = kind == KK_INV || kind == KK_INV_P || kind == KK_INV_KX || kind == KK_INV_KX_SLAB ||
@@ -232,21 +246,46 @@ void setup_tma(int kind, int cols, PassArgs& a, CUtensorMap* tm) {
   static const int skip_mask = getenv("SRK_TMA_SKIP") ? atoi(getenv("SRK_TMA_SKIP")) : 0;  // experiments
   if (skip_mask & (1 << kind)) return;
   if ((kind == KK_INV_KX || kind == KK_INV_KX_SLAB) && a.comp_stride != a.in_plane_stride) return;
-  srk_encode_tiled_fn enc = encode_tiled();
-  if (!enc) return;
   const int rows = fwd ? a.M : a.n;
   const int nb = (rows + 255) / 256;
   if (rows % nb) return;
   const int box = rows / nb;
-  cuuint64_t dims[3] = {(cuuint64_t)(2 * a.Qp), (cuuint64_t)rows, (cuuint64_t)a.planes};
-  cuuint64_t strides[2] = {(cuuint64_t)a.row_stride * 16, (cuuint64_t)a.in_plane_stride * 16};
-  cuuint32_t boxd[3] = {(cuuint32_t)(2 * cols), (cuuint32_t)box, 1};
-  cuuint32_t es[3] = {1, 1, 1};
-  if (enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)a.in, dims, strides, boxd, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-          CU_TENSOR_MAP_SWIZZLE_NONE, promo(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+  if (!encode_pass_map(tm, a.in + a.in_k0, a, a.in_kst, a.in_rs, a.in_plane_stride, rows, box, cols, promo()))
     return;
   a.tma = 1;
   a.tma_rows = box;
+}
+
+// Output tensor map of the 3D K2 pass (y inverse): {2*Qp doubles, M rows,
+// planes}, box {2*C, M/nb <= 256, 1} (plain output rows only).
+void setup_tma_out(int kind, int cols, PassArgs& a, CUtensorMap* tm) {
+  a.tma_out = 0;
+  const bool inv = kind == KK_INV_CURLY || kind == KK_INV_CURLY_SLAB;  // see kTMAO in k_colpass
+  if (!inv || a.out_rpb != 0 || !g_fast->count(a.M) || getenv("SRK_NO_TMAO")) return;
+  const int nb = (a.M + 255) / 256;
+  if (a.M % nb) return;
+  const int box = a.M / nb;
+  // the map ends at the chunk's last column: partial tiles are clipped, so a
+  // chunk never writes its neighbour's columns
+  if (!encode_pass_map(tm, a.out + a.out_k0, a, a.out_kst, a.out_rs, a.out_plane_stride, a.M, box, cols,
+                       CU_TENSOR_MAP_L2_PROMOTION_NONE))
+    return;
+  a.tma_out = 1;
+  a.tmo_rows = box;
+}
+
+// Column-group defaults (unchunked passes) and tile counts.
+void normalise_cols(PassArgs& a, int cols) {
+  if (a.kc == 0) {
+    a.kc = a.Qp;
+    a.ngrp = 1;
+    a.in_kst = a.out_kst = 0;
+    a.in_k0 = a.out_k0 = a.kz0 = 0;
+  }
+  if (a.in_rs == 0) a.in_rs = a.row_stride;
+  if (a.out_rs == 0) a.out_rs = a.row_stride;
+  a.tpg = (a.kc + cols - 1) / cols;
+  a.tpp = a.ngrp * a.tpg;
 }
 
 // NS3 z-pass L2 warm-up distance: one wave of resident CTAs (2 per SM); measured
@@ -262,28 +301,6 @@ int zpass_prefetch_distance() {
   return d;
 }
 
-// Output tensor map of the 3D K2 pass (y inverse): {2*Qp doubles, M rows,
-// planes}, box {2*C, M/nb <= 256, 1} (plain output rows only).
-void setup_tma_out(int kind, int cols, PassArgs& a, CUtensorMap* tm) {
-  a.tma_out = 0;
-  const bool inv = kind == KK_INV_CURLY || kind == KK_INV_CURLY_SLAB;  // see kTMAO in k_colpass
-  if (!inv || a.out_rpb != 0 || !g_fast->count(a.M) || getenv("SRK_NO_TMAO")) return;
-  srk_encode_tiled_fn enc = encode_tiled();
-  if (!enc) return;
-  const int nb = (a.M + 255) / 256;
-  if (a.M % nb) return;
-  const int box = a.M / nb;
-  cuuint64_t dims[3] = {(cuuint64_t)(2 * a.Qp), (cuuint64_t)a.M, (cuuint64_t)a.planes};
-  cuuint64_t strides[2] = {(cuuint64_t)a.row_stride * 16, (cuuint64_t)a.out_plane_stride * 16};
-  cuuint32_t boxd[3] = {(cuuint32_t)(2 * cols), (cuuint32_t)box, 1};
-  cuuint32_t es[3] = {1, 1, 1};
-  if (enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)a.out, dims, strides, boxd, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return;
-  a.tma_out = 1;
-  a.tmo_rows = box;
-}
-
 int launch_col(srk_plan* p, int kind, PassArgs a, cudaStream_t st) {
   const bool padded_kind = kind == KK_INV_P || kind == KK_FWD_P || kind == KK_INV_RHS || kind >= KK_INV_RHS_SLAB;
   if (padded_kind && 3 * a.n != 2 * a.M) return fail(SRK_ERR_INVALID, "padded pass needs M = 3n/2");
@@ -292,7 +309,7 @@ int launch_col(srk_plan* p, int kind, PassArgs a, cudaStream_t st) {
   if (rc) return rc;
   if ((rc = get_tw(p, a.M, &a.tw))) return rc;
   if ((rc = ensure_smem(e))) return rc;
-  a.tpp = (a.Qp + e.cols - 1) / e.cols;
+  normalise_cols(a, e.cols);
   const long long grid = (long long)a.planes * a.tpp;
   if (grid <= 0) return SRK_OK;
   a.dbg = (p->dbg && p->last_launches == p->dbg_launch) ? p->dbg : nullptr;
