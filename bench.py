@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--grid", dest="n", type=int, default=512, help="N of the N^3 grid")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--chunks", type=int, default=None,
+                    help="slab mode: kz chunks of the pipelined RHS (exchange of chunk c overlaps chunk c+1); "
+                         "default 4 for N > 1, 1 on a single GPU (nothing to overlap)")
     ap.add_argument("--mode", default="auto", choices=["auto", "single", "slab", "replicas"],
                     help="auto: single GPU at N=1, slab decomposition (strong scaling) for N>1")
     return ap.parse_args()
@@ -354,7 +357,8 @@ def run_slab(args, rank, world, local_rank):
     params = srk.PhysParams(reynolds=2000.0)
     energy, k_f = 0.5, 2.0
     red = dist_sum_in_rank_order()
-    rhs = SlabFlowRHS(g, params, rank, world)
+    chunks = args.chunks if args.chunks is not None else (4 if world > 1 else 1)
+    rhs = SlabFlowRHS(g, params, rank, world, chunks=chunks)
     plan = rhs.backend.h
     y0 = hit_slab(g, rank, world, a=4.0, energy=energy, seed=42, allreduce=red)
     pair = srk.make_bs5()
@@ -399,23 +403,31 @@ def run_slab(args, rank, world, local_rank):
     value = evals / T  # every rank works on the same global stages
 
     # phase timing of one RHS: 3 kernel groups + 2 exchanges (max over ranks)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
     yk = s["y"]
     fk = torch.empty_like(yk)
     b = rhs.backend
+    def xchg(r, sd):
+        w = rhs.exchange(r, sd)
+        if w is not None:
+            w.wait()
+
     ev[0].record(st)
     b.forward(yk, rhs.send1)
     ev[1].record(st)
-    rhs.exchange(rhs.recv1, rhs.send1)
+    xchg(rhs.recv1, rhs.send1)
     ev[2].record(st)
     b.middle(rhs.recv1, rhs.send2)
     ev[3].record(st)
-    rhs.exchange(rhs.recv2, rhs.send2)
+    xchg(rhs.recv2, rhs.send2)
     ev[4].record(st)
     b.finish(rhs.recv2, yk, fk)
     ev[5].record(st)
+    # the pipelined RHS as the steps run it (exchanges overlapped with kernels)
+    rhs(0.0, yk, out=fk)
+    ev[6].record(st)
     torch.cuda.synchronize()
-    ph = torch.tensor([ev[i].elapsed_time(ev[i + 1]) for i in range(5)], dtype=torch.float64, device=dev)
+    ph = torch.tensor([ev[i].elapsed_time(ev[i + 1]) for i in range(6)], dtype=torch.float64, device=dev)
     dist.all_reduce(ph, op=dist.ReduceOp.MAX)
     ph = ph.cpu().numpy()
     geo = slab_geometry(g, world)
@@ -437,14 +449,16 @@ def run_slab(args, rank, world, local_rank):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (device-side seeded HIT-spectrum slabs, E=0.5)",
         "config": {"workload": f"forced_hit_bs5_{n}^3", "n": n, "nu": 5e-4, "tol": 1e-6, "k_f": 2.0,
-                   "parallelism": f"y-slab x{world}, NCCL all-to-all", "l2": "inputs larger than L2"},
+                   "parallelism": f"y-slab x{world}, NCCL all-to-all, {len(rhs.chunks)} kz chunks pipelined",
+                   "l2": "inputs larger than L2"},
         "gpts_stage_per_s": value * n ** 3 / 1e9,
         "rhs_evals": evals,
         "stage_hbm_frac": model_bytes(n)["b_stage_bs5"] * value / world / (peak * 1e9),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": None, "kernel": names[dom], "peak_source": peak_src,
                      "phase_ms": {"forward": ph[0], "a2a1": ph[1], "middle": ph[2], "a2a2": ph[3],
-                                  "finish": ph[4]}},
+                                  "finish": ph[4], "serial_rhs": float(sum(ph[:5])),
+                                  "pipelined_rhs": ph[5], "kz_chunks": len(rhs.chunks)}},
         "nvlink": {"bytes_per_rhs_per_gpu": a2a_bytes, "achieved_GBps": a2a_bytes / (a2a_ms * 1e-3) / 1e9
                    if world > 1 else None, "peak_GBps": 770.0, "peak_source": "B200_PROFILING.md peer copy"},
         "cpu_baseline": None, "e2e": None, "gpu_launches": launches, "clocks": clk.summary(),

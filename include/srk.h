@@ -144,6 +144,27 @@ int srk_slab_middle(srk_plan* plan, const void* recv1, void* send2, void* stream
 int srk_slab_finish(srk_plan* plan, const void* recv2, const void* y, void* f, double nu, double ri, double re_pr,
                     void* stream);
 
+/* Pipelined slab RHS (SURVEY §8e "pipeline over kz-chunks"): the same kernel
+ * groups split over kz chunks [k0, k0+kc) so that the caller's exchange of
+ * chunk c overlaps the kernels of chunk c+1.  Chunk c of send1 / recv1 occupies
+ * elements [S1*m0*ny*k0, S1*m0*ny*(k0+kc)) laid out [rank][s][x_loc][y_loc][kc]
+ * (send2 / recv2 likewise with So*Mx*n1, [rank][o][x_loc][y_loc][kc]); the
+ * pointers passed are the chunk starts.  Order per RHS:
+ *   for c: srk_slab_forward_kz (K1)     -> exchange(send1_c -> recv1_c)
+ *   for c: srk_slab_inverse_y_kz (K2)   (after recv1_c landed)
+ *   srk_slab_zpass (K3)
+ *   for c: srk_slab_forward_y_kz (K4)   -> exchange(send2_c -> recv2_c)
+ *   for c: srk_slab_forward_x_kz (K5)   (after recv2_c landed)
+ *   srk_slab_project (K6)
+ * kc = K, k0 = 0 is the unchunked RHS.  Replaces the same reference call
+ * chain as srk_rhs (physics.py:188-206 -> spectral.py:215-337). */
+int srk_slab_forward_kz(srk_plan* plan, const void* y, void* send1_chunk, int k0, int kc, void* stream);
+int srk_slab_inverse_y_kz(srk_plan* plan, const void* recv1_chunk, int k0, int kc, void* stream);
+int srk_slab_zpass(srk_plan* plan, void* stream);
+int srk_slab_forward_y_kz(srk_plan* plan, void* send2_chunk, int k0, int kc, void* stream);
+int srk_slab_forward_x_kz(srk_plan* plan, const void* recv2_chunk, int k0, int kc, void* stream);
+int srk_slab_project(srk_plan* plan, const void* y, void* f, double nu, double ri, double re_pr, void* stream);
+
 /* Diagnostics: when dev_buf (u64) is non-NULL, launch number launch_index of
  * the next srk_rhs chain (0 = K1) records clock64() phase timestamps of every
  * 97th CTA into it (3 per CTA for the axis passes, 6 for the NS3 z-pass;

@@ -27,6 +27,8 @@ EXPORTS = (
     "srk_leray_project", "srk_combine", "srk_step_reduce", "srk_band_energy",
     "srk_band_scale", "srk_rhs_launch_count", "srk_rhs_timed", "srk_plan_create_slab", "srk_slab_sizes",
     "srk_slab_forward", "srk_slab_middle", "srk_slab_finish", "srk_debug_phase_buffer",
+    "srk_slab_forward_kz", "srk_slab_inverse_y_kz", "srk_slab_zpass", "srk_slab_forward_y_kz",
+    "srk_slab_forward_x_kz", "srk_slab_project",
 )
 
 _lib = None
@@ -83,6 +85,12 @@ def load():
         "srk_slab_middle": (c_int, [vp, vp, vp, vp]),
         "srk_slab_finish": (c_int, [vp, vp, vp, vp, c_dbl, c_dbl, c_dbl, vp]),
         "srk_debug_phase_buffer": (c_int, [vp, vp, c_int]),
+        "srk_slab_forward_kz": (c_int, [vp, vp, vp, c_int, c_int, vp]),
+        "srk_slab_inverse_y_kz": (c_int, [vp, vp, c_int, c_int, vp]),
+        "srk_slab_zpass": (c_int, [vp, vp]),
+        "srk_slab_forward_y_kz": (c_int, [vp, vp, c_int, c_int, vp]),
+        "srk_slab_forward_x_kz": (c_int, [vp, vp, c_int, c_int, vp]),
+        "srk_slab_project": (c_int, [vp, vp, vp, c_dbl, c_dbl, c_dbl, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -153,14 +153,25 @@ SRK_DEV void tile_of(const PassArgs& a, int bid, int& plane, int& g, int& wl) {
 // plane end are zero-filled by the TMA bounds check.
 template <int C>
 __device__ __forceinline__ void tma_stage(cplx* sm, const CUtensorMap* tm, int wl, int g, int rows, int box,
-                                          int plA, int plB, int boff, unsigned long long* bar) {
+                                          int rpb, int plA, int plB, int boff, unsigned long long* bar) {
   if (threadIdx.x == 0) {
     const int nb = rows / box;
     const unsigned bytes = (unsigned)(nb * box * C * 16) * (plB >= 0 ? 2u : 1u);
     mbar_expect_tx(bar, bytes);
-    for (int b = 0; b < nb; ++b) tma_load_4d(sm + b * box * C, tm, 2 * wl, g, b * box, plA, bar);
-    if (plB >= 0)
-      for (int b = 0; b < nb; ++b) tma_load_4d(sm + boff + b * box * C, tm, 2 * wl, g, b * box, plB, bar);
+    // rows are (row in block, block) -- blocked slab receive layouts; plain rows
+    // are one block of `rows`
+    if (rpb > 0) {  // 5D map
+      for (int b = 0; b < nb; ++b) {
+        const int r0 = b * box, blk = r0 / rpb;
+        tma_load_5d(sm + b * box * C, tm, 2 * wl, g, r0 - blk * rpb, blk, plA, bar);
+        if (plB >= 0) tma_load_5d(sm + boff + b * box * C, tm, 2 * wl, g, r0 - blk * rpb, blk, plB, bar);
+      }
+    } else {  // 4D map
+      for (int b = 0; b < nb; ++b) {
+        tma_load_4d(sm + b * box * C, tm, 2 * wl, g, b * box, plA, bar);
+        if (plB >= 0) tma_load_4d(sm + boff + b * box * C, tm, 2 * wl, g, b * box, plB, bar);
+      }
+    }
   }
   cp_async_wait_all();  // this thread's twiddle-table copies
   mbar_wait(bar, 0);
@@ -193,7 +204,8 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : (Eng::NT <= 192
   const int in_rpb = (FL & PF_BIN) ? a.in_rpb : 0;
   const int out_rpb = (FL & PF_BOUT) ? a.out_rpb : 0;
   // TMA staging: plain (unblocked) input rows of the fast engines
-  constexpr bool kTMA = Eng::kFast && !(FL & PF_BIN) && KIND != PK_INV_RHS;
+  constexpr bool kTMA = Eng::kFast && KIND != PK_INV_RHS;
+  const int trpb = in_rpb;  // > 0: blocked input rows (5D TMA map)
   __shared__ __align__(8) unsigned long long tbar;
   const bool use_tma = kTMA && a.tma;
   // TMA output: the last stage writes a dense [M][C] tile in smem (over the
@@ -228,7 +240,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : (Eng::NT <= 192
   if constexpr (KIND == PK_INV) {
     const double sc = a.scale;
     if (use_tma) {
-      tma_stage<C>(sm, &tm, wl, g, n, a.tma_rows, plane, -1, 0, &tbar);
+      tma_stage<C>(sm, &tm, wl, g, n, a.tma_rows, trpb, plane, -1, 0, &tbar);
       SRK_TS(1)
     } else if constexpr (Eng::kFast) {
       stage_rows<C>(sm, inp, n, rs, ncols, in_rpb, a.in_bstride);
@@ -324,7 +336,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : (Eng::NT <= 192
     const cplx* __restrict__ pa = a.in + w_in + comp * a.comp_stride;
     const double sc = a.scale;
     if (use_tma) {  // host guarantees comp_stride == in_plane_stride
-      tma_stage<C>(sm, &tm, wl, g, n, a.tma_rows, comp, -1, 0, &tbar);
+      tma_stage<C>(sm, &tm, wl, g, n, a.tma_rows, trpb, comp, -1, 0, &tbar);
       SRK_TS(1)
     } else if constexpr (Eng::kFast) {
       stage_rows<C>(sm, pa, n, rs, ncols, in_rpb, a.in_bstride);
@@ -369,7 +381,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : (Eng::NT <= 192
     const double kz = (double)(a.kz0 + wl + mycol) * a.ck2;  // global kz of the column
     cplx* sb_ = sm + (is_curl ? n * C : 0);
     if (use_tma) {
-      tma_stage<C>(sm, &tm, wl, g, n, a.tma_rows, ca * X + x, is_curl ? cb * X + x : -1, n * C, &tbar);
+      tma_stage<C>(sm, &tm, wl, g, n, a.tma_rows, trpb, ca * X + x, is_curl ? cb * X + x : -1, n * C, &tbar);
       SRK_TS(1)
     } else if constexpr (Eng::kFast) {
       stage_rows<C>(sm, pa, n, rs, ncols, in_rpb, a.in_bstride);
@@ -405,7 +417,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : (Eng::NT <= 192
     const bool zdc = (a.zero_dc_imag != 0) && (g == 0) && (a.kz0 + wl == 0) && (a.y0 == 0);
     const double sc = a.scale;
     if (use_tma) {
-      tma_stage<C>(sm, &tm, wl, g, M, a.tma_rows, plane, -1, 0, &tbar);
+      tma_stage<C>(sm, &tm, wl, g, M, a.tma_rows, trpb, plane, -1, 0, &tbar);
       SRK_TS(1)
     } else if constexpr (Eng::kFast) {
       stage_rows<C>(sm, inp, M, rs, ncols, in_rpb, a.in_bstride);

@@ -225,11 +225,24 @@ CUtensorMapL2promotion promo() {
 // 1}.  Leaves a.tma = 0 when TMA does not apply (generic lengths, blocked slab
 // rows, 2D curl kinds, box constraints).
 bool encode_pass_map(CUtensorMap* tm, const cplx* base, const PassArgs& a, long long kst, long long rs,
-                     long long pst, int rows, int box, int cols, CUtensorMapL2promotion pr) {
+                     long long pst, int rows, int box, int cols, CUtensorMapL2promotion pr, int rpb = 0,
+                     long long bstride = 0) {
   srk_encode_tiled_fn enc = encode_tiled();
   if (!enc) return false;
+  const cuuint64_t ks = (cuuint64_t)(a.ngrp > 1 ? kst : a.kc) * 16;
+  if (rpb > 0) {  // rank 5: {columns, column groups, row in block, block, plane}
+    cuuint64_t dims[5] = {(cuuint64_t)(2 * a.kc), (cuuint64_t)a.ngrp, (cuuint64_t)rpb, (cuuint64_t)(rows / rpb),
+                          (cuuint64_t)a.planes};
+    cuuint64_t strides[4] = {ks, (cuuint64_t)rs * 16, (cuuint64_t)bstride * 16, (cuuint64_t)pst * 16};
+    cuuint32_t boxd[5] = {(cuuint32_t)(2 * cols), 1, (cuuint32_t)box, 1, 1};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void*)base, dims, strides, boxd, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, pr,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  // rank 4: {columns, column groups, rows, plane}
   cuuint64_t dims[4] = {(cuuint64_t)(2 * a.kc), (cuuint64_t)a.ngrp, (cuuint64_t)rows, (cuuint64_t)a.planes};
-  cuuint64_t strides[3] = {(cuuint64_t)(a.ngrp > 1 ? kst : a.kc) * 16, (cuuint64_t)rs * 16, (cuuint64_t)pst * 16};
+  cuuint64_t strides[3] = {ks, (cuuint64_t)rs * 16, (cuuint64_t)pst * 16};
   cuuint32_t boxd[4] = {(cuuint32_t)(2 * cols), 1, (cuuint32_t)box, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)base, dims, strides, boxd, es,
@@ -241,16 +254,21 @@ void setup_tma(int kind, int cols, PassArgs& a, CUtensorMap* tm) {
   a.tma = 0;
   const bool inv = kind == KK_INV || kind == KK_INV_P || kind == KK_INV_KX || kind == KK_INV_KX_SLAB ||
                    kind == KK_INV_CURLY;
-  const bool fwd = kind == KK_FWD || kind == KK_FWD_P || kind == KK_FWD_P_SLABO;
-  if (!(inv || fwd) || a.in_rpb != 0 || !g_fast->count(a.M)) return;
+  const bool fwd = kind == KK_FWD || kind == KK_FWD_P || kind == KK_FWD_P_SLABO || kind == KK_FWD_P_SLABI;
+  const bool slab_in = kind == KK_INV_CURLY_SLAB || kind == KK_INV_P_SLAB;  // blocked input rows
+  if (!(inv || fwd || slab_in) || !g_fast->count(a.M)) return;
   static const int skip_mask = getenv("SRK_TMA_SKIP") ? atoi(getenv("SRK_TMA_SKIP")) : 0;  // experiments
+  if (a.in_rpb > 0 && getenv("SRK_NO_TMA5")) return;
   if (skip_mask & (1 << kind)) return;
   if ((kind == KK_INV_KX || kind == KK_INV_KX_SLAB) && a.comp_stride != a.in_plane_stride) return;
   const int rows = fwd ? a.M : a.n;
-  const int nb = (rows + 255) / 256;
-  if (rows % nb) return;
-  const int box = rows / nb;
-  if (!encode_pass_map(tm, a.in + a.in_k0, a, a.in_kst, a.in_rs, a.in_plane_stride, rows, box, cols, promo()))
+  const int rb = a.in_rpb > 0 ? a.in_rpb : rows;  // boxes must not straddle row blocks
+  if (rows % rb) return;
+  const int nb = (rb + 255) / 256;
+  if (rb % nb) return;
+  const int box = rb / nb;
+  if (!encode_pass_map(tm, a.in + a.in_k0, a, a.in_kst, a.in_rs, a.in_plane_stride, rows, box, cols, promo(),
+                       a.in_rpb, a.in_bstride))
     return;
   a.tma = 1;
   a.tma_rows = box;
@@ -1040,6 +1058,162 @@ int srk_slab_finish(srk_plan* p, const void* recv2, const void* y, void* f, doub
   pa.ri = ri;
   pa.re_pr = re_pr;
   srk_launch_project(pa, st);
+  return check_launch("k_project");
+}
+
+
+// ---- pipelined slab RHS: kz-chunked kernel groups (see srk.h) -----------------
+static int bad_chunk(const srk_plan* p, int k0, int kc) {
+  return !p || !p->Mx || k0 < 0 || kc < 1 || k0 + kc > p->K;
+}
+
+int srk_slab_forward_kz(srk_plan* p, const void* y, void* send1, int k0, int kc, void* stream) {
+  if (bad_chunk(p, k0, kc)) return fail(SRK_ERR_INVALID, "not a slab plan / bad kz chunk");
+  const int d = p->dims;
+  const long long Ny = p->n1, Mx = p->Mx;
+  PassArgs a = x_pass(p, (const cplx*)y, (cplx*)send1, p->S1, p->n0, p->m0, p->m0, p->n0);
+  // columns: groups y_loc of kc kz values; input rows of n1*K, output rows of n1*kc
+  a.kc = kc;
+  a.ngrp = (int)Ny;
+  a.in_kst = p->K;
+  a.in_k0 = k0;
+  a.out_kst = kc;
+  a.out_k0 = 0;
+  a.kz0 = k0;
+  a.in_rs = Ny * p->K;
+  a.out_rs = Ny * kc;
+  a.out_plane_stride = Mx * Ny * kc;
+  a.out_rpb = (int)Mx;
+  a.out_bstride = (long long)p->S1 * Mx * Ny * kc;
+  a.scale = std::pow(1.5, d) / ((double)p->m0 * p->m1 * p->m2);
+  a.dims = d;
+  a.n1 = p->n1;
+  a.K = p->K;
+  a.ck0 = p->ck0;
+  a.ck1 = p->ck1;
+  a.ck2 = p->ck2;
+  a.comp_stride = p->modes;
+  a.y0 = p->y0;
+  a.n1g = p->n1g;
+  return launch_col(p, KK_INV_KX_SLAB, a, (cudaStream_t)stream);
+}
+
+int srk_slab_inverse_y_kz(srk_plan* p, const void* recv1, int k0, int kc, void* stream) {
+  if (bad_chunk(p, k0, kc)) return fail(SRK_ERR_INVALID, "not a slab plan / bad kz chunk");
+  int rc = need_ws(p);
+  if (rc) return rc;
+  const long long K = p->K, Ny = p->n1, Mx = p->Mx, m1 = p->m1;
+  PassArgs b = base_pass();
+  b.in = (const cplx*)recv1;
+  b.out = p->B;
+  b.M = p->m1;
+  b.n = p->n1g;
+  b.planes = p->S * p->Mx;
+  b.Qp = kc;
+  b.kc = kc;
+  b.ngrp = 1;
+  b.in_k0 = 0;
+  b.out_k0 = k0;
+  b.kz0 = k0;
+  b.in_rs = kc;
+  b.out_rs = K;
+  b.in_plane_stride = Ny * kc;
+  b.out_plane_stride = m1 * K;
+  b.in_rpb = (int)Ny;
+  b.in_bstride = (long long)p->S1 * Mx * Ny * kc;
+  b.xplanes = p->Mx;
+  b.xblk = curly_xblk(p->Mx);
+  b.nsig = p->S;
+  b.ck1 = p->ck1;
+  b.ck2 = p->ck2;
+  return launch_col(p, KK_INV_CURLY_SLAB, b, (cudaStream_t)stream);
+}
+
+int srk_slab_zpass(srk_plan* p, void* stream) {
+  if (!p || !p->Mx) return fail(SRK_ERR_INVALID, "not a slab plan");
+  int rc = need_ws(p);
+  if (rc) return rc;
+  const long long K = p->K;
+  const int P = (int)(p->Mx * p->m1);
+  ZArgs z = z_args(p, p->m2, p->n2, P);
+  z.in = p->B;
+  z.out = p->A;
+  z.in_sig_stride = (long long)P * K;
+  z.out_sig_stride = (long long)P * K;
+  z.zero_nyq = 1;
+  z.pf_dist = zpass_prefetch_distance();
+  return launch_z(p, p->density ? KK_Z_B3 : KK_Z_NS3, z, 0, 0, (cudaStream_t)stream);
+}
+
+int srk_slab_forward_y_kz(srk_plan* p, void* send2, int k0, int kc, void* stream) {
+  if (bad_chunk(p, k0, kc)) return fail(SRK_ERR_INVALID, "not a slab plan / bad kz chunk");
+  int rc = need_ws(p);
+  if (rc) return rc;
+  const long long K = p->K, Ny = p->n1, Mx = p->Mx, m1 = p->m1;
+  PassArgs c = base_pass();
+  c.in = p->A;
+  c.out = (cplx*)send2;
+  c.M = p->m1;
+  c.n = p->n1g;
+  c.planes = p->So * p->Mx;
+  c.Qp = kc;
+  c.kc = kc;
+  c.ngrp = 1;
+  c.in_k0 = k0;
+  c.out_k0 = 0;
+  c.kz0 = k0;
+  c.in_rs = K;
+  c.out_rs = kc;
+  c.in_plane_stride = m1 * K;
+  c.out_plane_stride = Ny * kc;
+  c.out_rpb = (int)Ny;
+  c.out_bstride = (long long)p->So * Mx * Ny * kc;
+  c.zero_nyq = 1;
+  return launch_col(p, KK_FWD_P_SLABO, c, (cudaStream_t)stream);
+}
+
+int srk_slab_forward_x_kz(srk_plan* p, const void* recv2, int k0, int kc, void* stream) {
+  if (bad_chunk(p, k0, kc)) return fail(SRK_ERR_INVALID, "not a slab plan / bad kz chunk");
+  int rc = need_ws(p);
+  if (rc) return rc;
+  const long long K = p->K, Ny = p->n1, Mx = p->Mx;
+  // G (So, n0, ny, K) goes to workspace B (free after the z-pass): K4 of later
+  // chunks still reads the z-pass output in A
+  PassArgs c5 = x_pass(p, (const cplx*)recv2, p->B, p->So, p->m0, p->n0, p->m0, p->n0);
+  c5.kc = kc;
+  c5.ngrp = (int)Ny;
+  c5.in_kst = kc;
+  c5.in_k0 = 0;
+  c5.out_kst = K;
+  c5.out_k0 = k0;
+  c5.kz0 = k0;
+  c5.in_rs = Ny * kc;
+  c5.out_rs = Ny * K;
+  c5.in_plane_stride = Mx * Ny * kc;
+  c5.in_rpb = (int)Mx;
+  c5.in_bstride = (long long)p->So * Mx * Ny * kc;
+  c5.scale = std::pow(1.0 / 1.5, p->dims);
+  c5.zero_nyq = 1;
+  c5.zero_dc_imag = 1;
+  c5.y0 = p->y0;
+  return launch_col(p, KK_FWD_P_SLABI, c5, (cudaStream_t)stream);
+}
+
+int srk_slab_project(srk_plan* p, const void* y, void* f, double nu, double ri, double re_pr, void* stream) {
+  if (!p || !p->Mx) return fail(SRK_ERR_INVALID, "not a slab plan");
+  int rc = need_ws(p);
+  if (rc) return rc;
+  ProjArgs pa;
+  pa.g = geom(p);
+  pa.G = p->B;
+  pa.y = (const cplx*)y;
+  pa.f = (cplx*)f;
+  pa.modes = p->modes;
+  pa.density = p->density;
+  pa.nu = nu;
+  pa.ri = ri;
+  pa.re_pr = re_pr;
+  srk_launch_project(pa, (cudaStream_t)stream);
   return check_launch("k_project");
 }
 

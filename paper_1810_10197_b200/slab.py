@@ -17,6 +17,12 @@ unpack pass.  Reductions (error norm, E_kin, eps, Z, forcing band energy) are
 per-slab device sums, all-gathered and added in rank order so every rank takes
 the same accept/reject decision bit for bit.
 
+With ``chunks > 1`` (SURVEY §8e "pipeline over kz-chunks") the same kernel
+groups run per kz chunk and each chunk's exchange is issued asynchronously, so
+K1 of chunk c+1 and K2 of chunk c-1 overlap the all-to-all of chunk c (and K4 /
+K5 likewise for the second exchange); only the z-pass (K3, needs every kz of a
+pencil) separates the two halves.
+
 The stage functions are pluggable (``backend``) so the CPU test-suite can run
 the same orchestration on gloo with a numpy restatement of the three kernel
 groups (tests/slab_numpy_backend.py).
@@ -95,6 +101,35 @@ class CudaSlabBackend:
                                                float(p.reynolds) * float(p.prandtl), _native.stream_ptr()))
         _native.count(2)
 
+    # ---- kz-chunked kernel groups (pipelined RHS) ----
+    def forward_kz(self, y, send1_c, k0, kc):
+        _native.check(self.lib.srk_slab_forward_kz(self.h, _native.ptr(y), _native.ptr(send1_c), k0, kc,
+                                                   _native.stream_ptr()))
+        _native.count(1)
+
+    def inverse_y_kz(self, recv1_c, k0, kc):
+        _native.check(self.lib.srk_slab_inverse_y_kz(self.h, _native.ptr(recv1_c), k0, kc, _native.stream_ptr()))
+        _native.count(1)
+
+    def zpass(self):
+        _native.check(self.lib.srk_slab_zpass(self.h, _native.stream_ptr()))
+        _native.count(1)
+
+    def forward_y_kz(self, send2_c, k0, kc):
+        _native.check(self.lib.srk_slab_forward_y_kz(self.h, _native.ptr(send2_c), k0, kc, _native.stream_ptr()))
+        _native.count(1)
+
+    def forward_x_kz(self, recv2_c, k0, kc):
+        _native.check(self.lib.srk_slab_forward_x_kz(self.h, _native.ptr(recv2_c), k0, kc, _native.stream_ptr()))
+        _native.count(1)
+
+    def project(self, y, f):
+        p = self.params
+        _native.check(self.lib.srk_slab_project(self.h, _native.ptr(y), _native.ptr(f), 1.0 / p.reynolds,
+                                                float(p.richardson), float(p.reynolds) * float(p.prandtl),
+                                                _native.stream_ptr()))
+        _native.count(1)
+
     def __del__(self):
         try:
             self.lib.srk_plan_destroy(self.h)
@@ -102,16 +137,35 @@ class CudaSlabBackend:
             pass
 
 
-def dist_all_to_all(group=None):
-    """Equal-split all-to-all over torch.distributed (NCCL on GPUs, gloo on CPU)."""
+def dist_all_to_all(group=None, async_op=False):
+    """Equal-split all-to-all over torch.distributed (NCCL on GPUs, gloo on CPU).
+
+    ``async_op=True`` returns the work handle: ``wait()`` orders the caller's
+    current CUDA stream after the exchange without blocking the host, so the
+    kernels queued meanwhile overlap it (the kz-chunk pipeline)."""
     import torch.distributed as dist
 
     def exchange(recv, send):
         if recv.is_complex():  # NCCL / gloo move the (re, im) float64 pairs
             recv, send = torch.view_as_real(recv), torch.view_as_real(send)
-        dist.all_to_all_single(recv, send, group=group)
+        return dist.all_to_all_single(recv, send, group=group, async_op=async_op)
 
     return exchange
+
+
+def kz_chunks(K, n):
+    """Split [0, K) into n chunks whose widths are multiples of 4 (the strided
+    tile width), the remainder going to the last one."""
+    n = max(1, min(n, K // 4 if K >= 4 else 1))
+    base = (K // n) // 4 * 4 or K
+    out, k0 = [], 0
+    for c in range(n):
+        kc = base if c < n - 1 else K - k0
+        if kc <= 0:
+            break
+        out.append((k0, kc))
+        k0 += kc
+    return out
 
 
 def dist_sum_in_rank_order(group=None):
@@ -142,12 +196,19 @@ class SlabFlowRHS:
     """``f(t, y_slab)`` for one rank of a slab-decomposed grid (drop-in for FlowRHS)."""
 
     def __init__(self, grid: Grid, params: PhysParams, rank: int, nranks: int, density=False, backend=None,
-                 exchange=None):
+                 exchange=None, chunks=1):
+        """``chunks`` > 1 pipelines the RHS over kz chunks: the exchange of
+        chunk c (asynchronous, ``exchange`` must then return a handle with
+        ``wait()``) overlaps the kernels of the neighbouring chunks."""
         self.grid, self.params, self.rank, self.nranks = grid, params, rank, nranks
         self.density = bool(density)
         self.geo = slab_geometry(grid, nranks, density)
         self.backend = backend if backend is not None else CudaSlabBackend(grid, params, rank, nranks, density)
-        self.exchange = exchange if exchange is not None else dist_all_to_all()
+        self.chunks = kz_chunks(self.geo["K"], chunks)
+        self.pipelined = len(self.chunks) > 1
+        if exchange is None:
+            exchange = dist_all_to_all(async_op=self.pipelined)
+        self.exchange = exchange
         g = self.geo
         self.send1, self.recv1 = self.backend.empty(g["send1"]), self.backend.empty(g["send1"])
         self.send2, self.recv2 = self.backend.empty(g["send2"]), self.backend.empty(g["send2"])
@@ -158,13 +219,42 @@ class SlabFlowRHS:
         g = self.geo
         return (g["n0"], g["ny"], g["K"])
 
+    def _views(self, buf, per_kz, k0, kc):
+        return buf[per_kz * k0:per_kz * (k0 + kc)]
+
     def __call__(self, t, y, out=None):
         f = out if out is not None else (torch.empty_like(y) if isinstance(y, torch.Tensor) else np.empty_like(y))
-        self.backend.forward(y, self.send1)
-        self.exchange(self.recv1, self.send1)
-        self.backend.middle(self.recv1, self.send2)
-        self.exchange(self.recv2, self.send2)
-        self.backend.finish(self.recv2, y, f)
+        if not self.pipelined:
+            self.backend.forward(y, self.send1)
+            self.exchange(self.recv1, self.send1)
+            self.backend.middle(self.recv1, self.send2)
+            self.exchange(self.recv2, self.send2)
+            self.backend.finish(self.recv2, y, f)
+            self.calls += 1
+            return f
+        g, be = self.geo, self.backend
+        p1 = g["send1"] // g["K"]  # elements per kz of a send1 chunk (S1 * m0 * ny)
+        p2 = g["send2"] // g["K"]
+        work = []
+        for k0, kc in self.chunks:  # K1 of chunk c+1 overlaps the exchange of chunk c
+            s1 = self._views(self.send1, p1, k0, kc)
+            be.forward_kz(y, s1, k0, kc)
+            work.append(self.exchange(self._views(self.recv1, p1, k0, kc), s1))
+        for (k0, kc), w in zip(self.chunks, work):  # K2 of chunk c overlaps the later exchanges
+            if w is not None:
+                w.wait()
+            be.inverse_y_kz(self._views(self.recv1, p1, k0, kc), k0, kc)
+        be.zpass()
+        work = []
+        for k0, kc in self.chunks:
+            s2 = self._views(self.send2, p2, k0, kc)
+            be.forward_y_kz(s2, k0, kc)
+            work.append(self.exchange(self._views(self.recv2, p2, k0, kc), s2))
+        for (k0, kc), w in zip(self.chunks, work):
+            if w is not None:
+                w.wait()
+            be.forward_x_kz(self._views(self.recv2, p2, k0, kc), k0, kc)
+        be.project(y, f)
         self.calls += 1
         return f
 

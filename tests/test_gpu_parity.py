@@ -340,6 +340,59 @@ def test_slab_kernels_emulated_ranks_match_single_gpu(P, shape):
     assert rel(f, f_ref) <= 1e-14
 
 
+@pytest.mark.parametrize("P,shape,nchunks", [(2, (32, 32, 32), 4), (3, (32, 48, 16), 2), (4, (64, 64, 64), 3),
+                                             (2, (256, 256, 256), 4), (2, (512, 512, 512), 4)])
+def test_slab_kz_pipeline_emulated_ranks_match_single_gpu(P, shape, nchunks):
+    """The kz-chunked slab kernels (SURVEY §8e pipeline) on one GPU: P virtual
+    ranks, per-chunk all-to-alls emulated by block copies, vs the unsplit RHS.
+    512^3 covers the two-stage 768 engine, ragged last chunks (kc = 65: a
+    one-column tile) and the K2 TMA store clipped at the chunk end."""
+    from paper_1810_10197_b200.slab import CudaSlabBackend, kz_chunks, scatter_slab, slab_geometry
+
+    g = srk.Grid(shape)
+    params = srk.PhysParams(321.0)
+    if shape[0] >= 256:
+        y = srk.hit_init(g, srk.ProblemSpec("hit", a=4.0, energy=0.5, seed=8)).fields
+    else:
+        y = dev(O.hit(O.OGrid(shape), a=4.0, energy=0.5, seed=8))
+    f_ref = srk.FlowRHS(g, params)(0.0, y)
+    geo = slab_geometry(g, P)
+    K = geo["K"]
+    chunks = kz_chunks(K, nchunks)
+    assert len(chunks) == nchunks and sum(kc for _, kc in chunks) == K
+    backs = [CudaSlabBackend(g, params, r, P) for r in range(P)]
+    ys = [scatter_slab(y, r, P) for r in range(P)]
+    del y
+    p1, p2 = geo["send1"] // K, geo["send2"] // K
+
+    def a2a(sends):
+        blk = sends[0].numel() // P
+        return [torch.cat([sends[q][r * blk:(r + 1) * blk] for q in range(P)]) for r in range(P)]
+
+    s1 = [b.empty(geo["send1"]) for b in backs]
+    for k0, kc in chunks:
+        views = [s[p1 * k0:p1 * (k0 + kc)] for s in s1]
+        for r in range(P):
+            backs[r].forward_kz(ys[r], views[r], k0, kc)
+        for r, rv in enumerate(a2a(views)):
+            backs[r].inverse_y_kz(rv, k0, kc)
+    del s1
+    for b in backs:
+        b.zpass()
+    s2 = [b.empty(geo["send2"]) for b in backs]
+    for k0, kc in chunks:
+        views = [s[p2 * k0:p2 * (k0 + kc)] for s in s2]
+        for r in range(P):
+            backs[r].forward_y_kz(views[r], k0, kc)
+        for r, rv in enumerate(a2a(views)):
+            backs[r].forward_x_kz(rv, k0, kc)
+    fs = [torch.empty_like(ys[r]) for r in range(P)]
+    for r in range(P):
+        backs[r].project(ys[r], fs[r])
+    f = torch.cat(fs, dim=2)
+    assert float(torch.linalg.norm(f - f_ref) / torch.linalg.norm(f_ref)) <= 1e-14
+
+
 def test_slab_reduction_partials_sum_to_global():
     from paper_1810_10197_b200.diagnostics import reduce_sums
     from paper_1810_10197_b200.slab import CudaSlabBackend, scatter_slab

@@ -22,7 +22,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, shape, density, q):
+def _worker(rank, world, port, shape, density, q, chunks=1):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -43,7 +43,8 @@ def _worker(rank, world, port, shape, density, q):
         params = PhysParams(reynolds=80.0, richardson=1.5, prandtl=0.7)
         g = Grid(shape)
         be = NumpySlabBackend(g, params, rank, world, density)
-        rhs = SlabFlowRHS(g, params, rank, world, density=density, backend=be)
+        rhs = SlabFlowRHS(g, params, rank, world, density=density, backend=be, chunks=chunks)
+        assert rhs.pipelined == (chunks > 1)
         ys = torch.from_numpy(scatter_slab(y, rank, world))
         f = rhs(0.0, ys)
         parts = [torch.empty_like(f) for _ in range(world)]
@@ -63,13 +64,15 @@ def _worker(rank, world, port, shape, density, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,shape,density", [(2, (16, 16, 12), False), (3, (16, 12, 8), False),
-                                                 (2, (8, 8, 8), True)])
-def test_slab_rhs_matches_oracle(world, shape, density):
+@pytest.mark.parametrize("world,shape,density,chunks", [(2, (16, 16, 12), False, 1), (3, (16, 12, 8), False, 1),
+                                                        (2, (8, 8, 8), True, 1),
+                                                        # kz-chunk pipeline, async gloo exchanges
+                                                        (2, (16, 16, 30), False, 3), (3, (12, 12, 34), True, 4)])
+def test_slab_rhs_matches_oracle(world, shape, density, chunks):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, shape, density, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, shape, density, q, chunks)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
