@@ -430,6 +430,57 @@ struct OneStage {
   }
 };
 
+// Stages after a caller-run prefix (Ls > 1), one butterfly per thread with the
+// thread -> (column, butterfly) map redone per stage, so every stage spreads
+// its ncols * M/R butterflies over the whole CTA (NS3 z-pass forward suffix:
+// 3 columns on M/4 threads).  Requires ncols * M/R <= blockDim.x.
+template <int M, class L, int SIGN, int Ls, int R, int... Rest>
+struct OneStageZ {
+  template <class ST>
+  __device__ __forceinline__ static void go(cplx* sm, const cplx* tw, int ncols, ST& st) {
+    constexpr int STRIDE = M / R;
+    constexpr bool LAST = (sizeof...(Rest) == 0);
+    const int tid = threadIdx.x;
+    const int col = tid / STRIDE, j = tid - col * STRIDE;
+    const bool act = col < ncols;
+    cplx v[R];
+    if (act) {
+      if constexpr (STRIDE % 8 == 0) {
+        const int a0 = L::idx(j, col);
+#pragma unroll
+        for (int t = 0; t < R; ++t) v[t] = sm[a0 + t * (STRIDE / 8) * L::STEP8];
+      } else {
+#pragma unroll
+        for (int t = 0; t < R; ++t) v[t] = sm[L::idx(j + t * STRIDE, col)];
+      }
+    }
+    const unsigned k = (unsigned)j % (unsigned)Ls;
+    if (act) {
+      stage_twiddle<M, R, SIGN>(v, tw, k * (unsigned)(M / (Ls * R)));
+      DFT<R, SIGN>::run(v);
+    }
+    __syncthreads();
+    if (act) {
+      const int base = (int)(((unsigned)j - k) * (unsigned)R + k);
+      if constexpr (LAST) {
+#pragma unroll
+        for (int q = 0; q < R; ++q) st(base + q * Ls, col, v[q]);
+      } else if constexpr (Ls % 8 == 0) {
+        const int a0 = L::idx(base, col);
+#pragma unroll
+        for (int q = 0; q < R; ++q) sm[a0 + q * (Ls / 8) * L::STEP8] = v[q];
+      } else {
+#pragma unroll
+        for (int q = 0; q < R; ++q) sm[L::idx(base + q * Ls, col)] = v[q];
+      }
+    }
+    if constexpr (!LAST) {
+      __syncthreads();
+      OneStageZ<M, L, SIGN, Ls * R, Rest...>::go(sm, tw, ncols, st);
+    }
+  }
+};
+
 template <int A, int... Bs>
 constexpr int cmin() {
   if constexpr (sizeof...(Bs) == 0)

@@ -8,5 +8,14 @@ SRK_DEFINE_SIZE_1(srk_reg_768_base, 768, 4, (24, 32), 24, 24, (8, 8, 12), 8, 8, 
 #endif
 void srk_reg_768(KEntry* t) {
   srk_reg_768_base(t);
+#ifndef SRK_Z768F
+#define SRK_Z768F 2  // forward suffix: 0 (8,24) on 96 threads 9.10 ms, 1 (12,16) 9.50, 2 (16,12) 8.97
+#endif
+#if SRK_Z768F == 0
   SRK_NS3F(768, (24, 8), 24, (8, 24))
+#elif SRK_Z768F == 1
+  SRK_NS3F(768, (24, 8), 0, (12, 16))
+#else
+  SRK_NS3F(768, (24, 8), 0, (16, 12))
+#endif
 }

@@ -781,7 +781,7 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
   // ---- forward suffix stages (Ls = 4 ...) on the 3 packed columns ----
   {
     // EF elements per thread: 12 puts all M/4 threads on the 3 forward columns
-    constexpr int TPC = M / EF;
+    constexpr int TPC = M / (EF > 0 ? EF : 24);
     const int col = tid / TPC, tj = tid - (tid / TPC) * TPC;
     const bool act = col < So;
     __builtin_assume(tj >= 0 && tj < TPC);
@@ -789,7 +789,10 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
     auto st = [&](int n, int c, cplx v) {
       if (n < K - 1 || n > M - K + 1) sm[L::idx(n, c)] = v;
     };
-    FastStageW<M, EF, L, -1, true, true, 4, FR...>::go(sm, twp, col, tj, act, ld, st);
+    if constexpr (EF == 0)  // one butterfly per thread, all threads on the 3 columns
+      OneStageZ<M, L, -1, 4, FR...>::go(sm, twp, So, st);
+    else
+      FastStageW<M, (EF > 0 ? EF : 24), L, -1, true, true, 4, FR...>::go(sm, twp, col, tj, act, ld, st);
   }
   __syncthreads();
   SRK_TS(4)
