@@ -8,6 +8,6 @@ timeout 900 python bench.py --mode slab --steps 3 --warmup 3 > gpurun_out/bench_
 timeout 300 python tools/rhs_timing.py --n 512 --reps 5 > gpurun_out/t512.log 2>&1
 timeout 300 python tools/phase_timing.py 512 > gpurun_out/phase512.log 2>&1
 timeout 300 python tools/rhs_timing.py --n 512 --reps 2 > gpurun_out/t512b.log 2>&1 && \
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 20 -c 60 --csv --log-file gpurun_out/launches512.csv python tools/rhs_timing.py --n 512 --reps 2 > gpurun_out/ncu_l.log 2>&1 && \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 6 -c 12 --csv --log-file gpurun_out/launches512.csv python tools/rhs_timing.py --n 512 --reps 2 > gpurun_out/ncu_l.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_(zpass|colpass|project)" -c 6 -o gpurun_out/prof512_full python tools/rhs_timing.py --n 512 --reps 2 > gpurun_out/ncu_f.log 2>&1
 echo done
