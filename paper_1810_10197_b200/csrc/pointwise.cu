@@ -7,6 +7,7 @@
 // changes the rounding relative to physics.py / integrators.py.
 #include "pointwise.cuh"
 
+#include <algorithm>
 #include <cstdlib>
 
 #define DMUL __dmul_rn
@@ -75,6 +76,111 @@ __device__ __forceinline__ double k2_at(long long idx, const GeomArgs& g, bool s
   const double k0 = DMUL(mode_full(x, g.n0), g.ck0);
   const double k1 = DMUL((double)kz, g.ck2);
   return DADD(DMUL(k0, k0), DMUL(k1, k1));
+}
+
+// kvec() with 32-bit index arithmetic (mode counts < 2^32)
+__device__ __forceinline__ KVec kvec32(unsigned idx, const GeomArgs& g) {
+  KVec r;
+  const unsigned K = (unsigned)g.K;
+  const unsigned xy = idx / K;
+  const int kz = (int)(idx - xy * K);
+  if (g.dims == 3) {
+    const unsigned n1 = (unsigned)g.n1, xq = xy / n1;
+    const int y = (int)(xy - xq * n1), x = (int)xq;
+    r.k[0] = DMUL(mode_full(x, g.n0), g.ck0);
+    r.k[1] = DMUL(mode_full(g.y0 + y, g.n1g), g.ck1);
+    r.k[2] = DMUL((double)kz, g.ck2);
+    r.k2 = DADD(DADD(DMUL(r.k[0], r.k[0]), DMUL(r.k[1], r.k[1])), DMUL(r.k[2], r.k[2]));
+  } else {
+    r.k[0] = DMUL(mode_full((int)xy, g.n0), g.ck0);
+    r.k[1] = DMUL((double)kz, g.ck2);
+    r.k[2] = 0.0;
+    r.k2 = DADD(DMUL(r.k[0], r.k[0]), DMUL(r.k[1], r.k[1]));
+  }
+  r.inv_k2 = (r.k2 == 0.0) ? 0.0 : __ddiv_rn(1.0, r.k2);
+  return r;
+}
+
+// K6, TMA-streamed (default): the G and state components of a chunk of
+// SRK_PT_CH modes arrive by 1D bulk copies in a two-stage shared-memory ring
+// (one elected thread, mbarrier completion); f is stored straight from
+// registers.  Same arithmetic as k_project.
+#define SRK_PT_CH 256
+template <int DIMS, bool DENS>
+__global__ void __launch_bounds__(SRK_PT_CH) k_project_tma(const ProjArgs a) {
+  extern __shared__ __align__(128) cplx psm[];
+  constexpr int CH = SRK_PT_CH;
+  constexpr int d = DIMS;
+  constexpr int NG = DENS ? 2 * d : d;  // G components
+  constexpr int NY = DENS ? d + 1 : d;  // state components
+  constexpr int NS = NG + NY;
+  __shared__ __align__(8) unsigned long long mb[2];
+  const int tid = threadIdx.x;
+  const long long n = a.modes;
+  const long long nch = (n + CH - 1) / CH;
+  const int G = gridDim.x;
+  if (tid == 0) {
+    mbar_init(&mb[0], 1);
+    mbar_init(&mb[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](long long k, int b) {
+    if (tid != 0 || k >= nch) return;
+    const long long i0 = k * CH;
+    const unsigned cnt = (unsigned)min((long long)CH, n - i0);
+    cplx* st = psm + b * NS * CH;
+    mbar_expect_tx(&mb[b], cnt * 16u * NS);
+#pragma unroll
+    for (int j = 0; j < NG; ++j) bulk_g2s(st + j * CH, a.G + j * n + i0, cnt * 16u, &mb[b]);
+#pragma unroll
+    for (int j = 0; j < NY; ++j) bulk_g2s(st + (NG + j) * CH, a.y + j * n + i0, cnt * 16u, &mb[b]);
+  };
+  issue(blockIdx.x, 0);
+  issue(blockIdx.x + G, 1);
+  unsigned phase = 0;
+  for (int it = 0; (long long)blockIdx.x + (long long)it * G < nch; ++it) {
+    const long long k = blockIdx.x + (long long)it * G;
+    const int b = it & 1;
+    const long long i0 = k * CH;
+    const int cnt = (int)min((long long)CH, n - i0);
+    mbar_wait(&mb[b], (phase >> b) & 1u);
+    phase ^= 1u << b;
+    const cplx* st = psm + b * NS * CH;
+    if (tid < cnt) {
+      const long long i = i0 + tid;
+      const KVec kv = kvec32((unsigned)i, a.g);
+      cplx Gv[3];
+#pragma unroll
+      for (int j = 0; j < d; ++j) Gv[j] = st[j * CH + tid];
+      cplx rho = make_double2(0.0, 0.0);
+      if constexpr (DENS) {
+        rho = st[(NG + d) * CH + tid];
+        Gv[d - 1] = rsub(Gv[d - 1], rmul(a.ri, rho));
+      }
+      cplx kd = rmul(kv.k[0], Gv[0]);
+#pragma unroll
+      for (int j = 1; j < d; ++j) kd = radd(kd, rmul(kv.k[j], Gv[j]));
+      kd = rmul(kv.inv_k2, kd);
+      const double nuk2 = DMUL(a.nu, kv.k2);
+#pragma unroll
+      for (int j = 0; j < d; ++j) {
+        cplx o = rsub(Gv[j], rmul(kv.k[j], kd));
+        o = rsub(o, rmul(nuk2, st[(NG + j) * CH + tid]));
+        a.f[j * n + i] = o;
+      }
+      if constexpr (DENS) {
+        cplx div = rmul(kv.k[0], st[d * CH + tid]);
+#pragma unroll
+        for (int j = 1; j < d; ++j) div = radd(div, rmul(kv.k[j], st[(d + j) * CH + tid]));
+        cplx o = make_double2(div.y, -div.x);  // -1j * div
+        o = rsub(o, rmul(__ddiv_rn(kv.k2, a.re_pr), rho));
+        a.f[d * n + i] = o;
+      }
+    }
+    __syncthreads();  // stage b consumed
+    issue(k + 2LL * G, b);
+  }
 }
 
 // K6: f = P[G] - nu k^2 u (physics.py:119-129); Boussinesq adds the buoyancy
@@ -435,7 +541,32 @@ __global__ void k_band_scale(cplx* __restrict__ u, const long long* __restrict__
   *p = rmul(gamma, *p);
 }
 
+template <int DIMS, bool DENS>
+static void launch_project_tma(const ProjArgs& a, cudaStream_t st) {
+  constexpr int NS = (DENS ? 2 * DIMS : DIMS) + (DENS ? DIMS + 1 : DIMS);
+  const int smem = 2 * NS * SRK_PT_CH * 16;
+  static int blocks = 0;
+  if (!blocks) {
+    cudaFuncSetAttribute(k_project_tma<DIMS, DENS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_project_tma<DIMS, DENS>, SRK_PT_CH, smem);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    blocks = std::max(1, per_sm) * sms;
+  }
+  const long long nch = (a.modes + SRK_PT_CH - 1) / SRK_PT_CH;
+  k_project_tma<DIMS, DENS><<<(int)std::min<long long>(blocks, nch), SRK_PT_CH, smem, st>>>(a);
+}
+
 void srk_launch_project(const ProjArgs& a, cudaStream_t st) {
+  static const bool legacy = getenv("SRK_PROJECT_LEGACY") != nullptr;  // A/B switch
+  if (!legacy && a.modes < (1LL << 32)) {
+    if (a.g.dims == 3)
+      a.density ? launch_project_tma<3, true>(a, st) : launch_project_tma<3, false>(a, st);
+    else
+      a.density ? launch_project_tma<2, true>(a, st) : launch_project_tma<2, false>(a, st);
+    return;
+  }
   long long blocks = (a.modes + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   k_project<<<(int)blocks, 256, 0, st>>>(a);
