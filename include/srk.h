@@ -68,6 +68,20 @@ int srk_plan_set_workspace(srk_plan* plan, void* ptr, int64_t bytes);
  * y, f: (d [+1], ...kshape) complex128; f must not alias y. */
 int srk_rhs(srk_plan* plan, const void* y, void* f, double nu, double ri, double re_pr, void* stream);
 
+/* srk_rhs fused with the next rk_step accumulation (integrators.py:327-339 for
+ * the next stage input, :336-339 for y_new of a non-FSAL pair):
+ *   f     = FlowRHS(y)
+ *   ynext = ybase + sum_{j < nterms} coef[j] * F[j] + coef_self * f
+ * summed in that order (ascending stage index, f being the highest), one
+ * rounding per multiply and add: bitwise equal to srk_rhs followed by
+ * srk_combine(ybase, [F..., f], [coef..., coef_self]).  On the 3D NS path the
+ * projection kernel forms ynext while f is still in registers (f is not read
+ * back); other shapes run the two calls.  nterms <= 6 on the fused path
+ * (<= 7 otherwise); F / coef are HOST arrays; ynext must not alias y, f, F. */
+int srk_rhs_combine(srk_plan* plan, const void* y, void* f, double nu, double ri, double re_pr,
+                    const void* ybase, int nterms, const void* const* F, const double* coef, double coef_self,
+                    void* ynext, void* stream);
+
 /* DealiasWorkspace.widen (spectral.py:215-261): spec (ncomp, kshape) ->
  * phys (ncomp, 3n0/2, 3n1/2[, 3n2/2]) float64. */
 int srk_widen(srk_plan* plan, const void* spec, int ncomp, void* phys, void* stream);

@@ -22,7 +22,7 @@ SRK_ERR_WORKSPACE = 4
 # Every symbol include/srk.h declares (checked by tests/test_native_abi.py).
 EXPORTS = (
     "srk_abi_version", "srk_last_error", "srk_plan_create", "srk_plan_destroy",
-    "srk_plan_workspace_bytes", "srk_plan_set_workspace", "srk_rhs", "srk_widen",
+    "srk_plan_workspace_bytes", "srk_plan_set_workspace", "srk_rhs", "srk_rhs_combine", "srk_widen",
     "srk_narrow", "srk_forward_transform", "srk_inverse_transform", "srk_curl",
     "srk_leray_project", "srk_combine", "srk_step_reduce", "srk_band_energy",
     "srk_band_scale", "srk_rhs_launch_count", "srk_rhs_timed", "srk_plan_create_slab", "srk_slab_sizes",
@@ -67,6 +67,7 @@ def load():
         "srk_plan_workspace_bytes": (c_int, [vp, P(i64)]),
         "srk_plan_set_workspace": (c_int, [vp, vp, i64]),
         "srk_rhs": (c_int, [vp, vp, vp, c_dbl, c_dbl, c_dbl, vp]),
+        "srk_rhs_combine": (c_int, [vp, vp, vp, c_dbl, c_dbl, c_dbl, vp, c_int, P(vp), P(c_dbl), c_dbl, vp, vp]),
         "srk_widen": (c_int, [vp, vp, c_int, vp, vp]),
         "srk_narrow": (c_int, [vp, vp, c_int, vp, vp]),
         "srk_forward_transform": (c_int, [vp, vp, c_int, vp, vp]),

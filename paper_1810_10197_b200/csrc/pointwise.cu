@@ -102,18 +102,29 @@ __device__ __forceinline__ KVec kvec32(unsigned idx, const GeomArgs& g) {
 }
 
 // K6, TMA-streamed (default): the G and state components of a chunk of
-// SRK_PT_CH modes arrive by 1D bulk copies in a two-stage shared-memory ring
-// (one elected thread, mbarrier completion); f is stored straight from
-// registers.  Same arithmetic as k_project.
+// CH modes arrive by 1D bulk copies in a two-stage shared-memory ring (one
+// elected thread, mbarrier completion); f is stored straight from registers.
+// Same arithmetic as k_project.
+//
+// NTC >= 0 (3D NS): the next RK stage input is formed in the same pass
+// (integrators.py:327-339 / :336-339):
+//   ynext = ybase + sum_{t < NTC} c_t F_t + cself * f
+// ascending in the stage index with f = the tendency just computed (the last,
+// highest-index term), one rounding per multiply and add -- bitwise what
+// k_combine produces from the stored f, without reading f back.  ybase and the
+// F_t ride in the same ring; chunks shrink to 128 modes to keep two CTAs/SM.
 #define SRK_PT_CH 256
-template <int DIMS, bool DENS>
-__global__ void __launch_bounds__(SRK_PT_CH) k_project_tma(const ProjArgs a) {
+#define SRK_PC_CH 128
+template <int DIMS, bool DENS, int NTC = -1>
+__global__ void __launch_bounds__(NTC < 0 ? SRK_PT_CH : SRK_PC_CH) k_project_tma(const ProjArgs a) {
   extern __shared__ __align__(128) cplx psm[];
-  constexpr int CH = SRK_PT_CH;
+  constexpr int CH = NTC < 0 ? SRK_PT_CH : SRK_PC_CH;
   constexpr int d = DIMS;
   constexpr int NG = DENS ? 2 * d : d;  // G components
   constexpr int NY = DENS ? d + 1 : d;  // state components
-  constexpr int NS = NG + NY;
+  constexpr int NC = NTC < 0 ? 0 : d * (NTC + 1);  // ybase + F_t components
+  constexpr int NS = NG + NY + NC;
+  static_assert(NTC < 0 || (DIMS == 3 && !DENS), "fused stage combination: 3D NS only");
   __shared__ __align__(8) unsigned long long mb[2];
   const int tid = threadIdx.x;
   const long long n = a.modes;
@@ -135,6 +146,15 @@ __global__ void __launch_bounds__(SRK_PT_CH) k_project_tma(const ProjArgs a) {
     for (int j = 0; j < NG; ++j) bulk_g2s(st + j * CH, a.G + j * n + i0, cnt * 16u, &mb[b]);
 #pragma unroll
     for (int j = 0; j < NY; ++j) bulk_g2s(st + (NG + j) * CH, a.y + j * n + i0, cnt * 16u, &mb[b]);
+    if constexpr (NTC >= 0) {
+#pragma unroll
+      for (int j = 0; j < d; ++j) bulk_g2s(st + (NG + NY + j) * CH, a.yb + j * n + i0, cnt * 16u, &mb[b]);
+#pragma unroll
+      for (int t = 0; t < (NTC < 0 ? 0 : NTC); ++t)
+#pragma unroll
+        for (int j = 0; j < d; ++j)
+          bulk_g2s(st + (NG + NY + d + t * d + j) * CH, a.F[t] + j * n + i0, cnt * 16u, &mb[b]);
+    }
   };
   issue(blockIdx.x, 0);
   issue(blockIdx.x + G, 1);
@@ -168,6 +188,13 @@ __global__ void __launch_bounds__(SRK_PT_CH) k_project_tma(const ProjArgs a) {
         cplx o = rsub(Gv[j], rmul(kv.k[j], kd));
         o = rsub(o, rmul(nuk2, st[(NG + j) * CH + tid]));
         a.f[j * n + i] = o;
+        if constexpr (NTC >= 0) {
+          cplx acc = st[(NG + NY + j) * CH + tid];
+#pragma unroll
+          for (int t = 0; t < (NTC < 0 ? 0 : NTC); ++t)
+            acc = radd(acc, rmul(a.c[t], st[(NG + NY + d + t * d + j) * CH + tid]));
+          a.ynext[j * n + i] = radd(acc, rmul(a.cself, o));
+        }
       }
       if constexpr (DENS) {
         cplx div = rmul(kv.k[0], st[d * CH + tid]);
@@ -541,21 +568,36 @@ __global__ void k_band_scale(cplx* __restrict__ u, const long long* __restrict__
   *p = rmul(gamma, *p);
 }
 
-template <int DIMS, bool DENS>
+template <int DIMS, bool DENS, int NTC = -1>
 static void launch_project_tma(const ProjArgs& a, cudaStream_t st) {
-  constexpr int NS = (DENS ? 2 * DIMS : DIMS) + (DENS ? DIMS + 1 : DIMS);
-  const int smem = 2 * NS * SRK_PT_CH * 16;
+  constexpr int CH = NTC < 0 ? SRK_PT_CH : SRK_PC_CH;
+  constexpr int NS = (DENS ? 2 * DIMS : DIMS) + (DENS ? DIMS + 1 : DIMS) + (NTC < 0 ? 0 : DIMS * (NTC + 1));
+  const int smem = 2 * NS * CH * 16;
   static int blocks = 0;
   if (!blocks) {
-    cudaFuncSetAttribute(k_project_tma<DIMS, DENS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_project_tma<DIMS, DENS, NTC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int per_sm = 0, dev = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_project_tma<DIMS, DENS>, SRK_PT_CH, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_project_tma<DIMS, DENS, NTC>, CH, smem);
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     blocks = std::max(1, per_sm) * sms;
   }
-  const long long nch = (a.modes + SRK_PT_CH - 1) / SRK_PT_CH;
-  k_project_tma<DIMS, DENS><<<(int)std::min<long long>(blocks, nch), SRK_PT_CH, smem, st>>>(a);
+  const long long nch = (a.modes + CH - 1) / CH;
+  k_project_tma<DIMS, DENS, NTC><<<(int)std::min<long long>(blocks, nch), CH, smem, st>>>(a);
+}
+
+// K6 with the next stage input formed in the same pass (3D NS, modes < 2^32,
+// at most SRK_PC_MAXT earlier stages); returns false when the shape does not qualify
+bool srk_launch_project_comb(const ProjArgs& a, cudaStream_t st) {
+  if (a.g.dims != 3 || a.density || a.modes >= (1LL << 32) || a.nt < 0 || a.nt > SRK_PC_MAXT) return false;
+  switch (a.nt) {
+#define CASE(N) \
+  case N: launch_project_tma<3, false, N>(a, st); break;
+    CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6)
+#undef CASE
+    default: return false;
+  }
+  return true;
 }
 
 void srk_launch_project(const ProjArgs& a, cudaStream_t st) {

@@ -22,6 +22,14 @@ struct ProjArgs {
   long long modes;  // n0*n1*K
   int density;
   double nu, ri, re_pr;
+  // fused next-stage combination (k_project_tma<3, false, NT>):
+  //   ynext = yb + sum_{t < nt} c[t] F[t] + cself * f
+  const cplx* yb;
+  const cplx* F[SRK_MAX_TERMS];
+  double c[SRK_MAX_TERMS];
+  int nt;
+  double cself;
+  cplx* ynext;
 };
 
 struct CombArgs {
@@ -51,6 +59,8 @@ struct RedArgs {
 };
 
 void srk_launch_project(const ProjArgs& a, cudaStream_t st);
+#define SRK_PC_MAXT 6
+bool srk_launch_project_comb(const ProjArgs& a, cudaStream_t st);
 void srk_launch_curl(const GeomArgs& g, const cplx* u, cplx* w, long long n, cudaStream_t st);
 void srk_launch_leray(const GeomArgs& g, const cplx* u, cplx* o, long long n, cudaStream_t st);
 void srk_launch_combine(const CombArgs& a, cudaStream_t st);

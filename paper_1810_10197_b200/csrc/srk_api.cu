@@ -662,7 +662,65 @@ int srk_plan_set_workspace(srk_plan* p, void* ptr, int64_t bytes) {
   return SRK_OK;
 }
 
+namespace {
+// next-stage accumulation carried by one RHS call (srk_rhs_combine)
+struct CombSpec {
+  const cplx* yb;
+  int nt;
+  const cplx* F[SRK_MAX_TERMS];
+  double c[SRK_MAX_TERMS];
+  double cself;
+  cplx* ynext;
+};
+int rhs_impl(srk_plan* p, const void* y_, void* f_, double nu, double ri, double re_pr, void* stream,
+             const CombSpec* cs);
+}  // namespace
+
 int srk_rhs(srk_plan* p, const void* y_, void* f_, double nu, double ri, double re_pr, void* stream) {
+  return rhs_impl(p, y_, f_, nu, ri, re_pr, stream, nullptr);
+}
+
+int srk_rhs_combine(srk_plan* p, const void* y, void* f, double nu, double ri, double re_pr, const void* ybase,
+                    int nterms, const void* const* F, const double* coef, double coef_self, void* ynext,
+                    void* stream) {
+  if (nterms < 0 || nterms + 1 > SRK_MAX_TERMS) return fail(SRK_ERR_INVALID, "srk_rhs_combine: at most 7 terms");
+  if (!ynext || ynext == y || ynext == f) return fail(SRK_ERR_INVALID, "srk_rhs_combine: ynext must not alias y or f");
+  CombSpec cs;
+  memset(&cs, 0, sizeof(cs));
+  cs.yb = (const cplx*)ybase;
+  cs.nt = nterms;
+  for (int j = 0; j < nterms; ++j) {
+    if (F[j] == ynext) return fail(SRK_ERR_INVALID, "srk_rhs_combine: ynext must not alias a term");
+    cs.F[j] = (const cplx*)F[j];
+    cs.c[j] = coef[j];
+  }
+  cs.cself = coef_self;
+  cs.ynext = (cplx*)ynext;
+  return rhs_impl(p, y, f, nu, ri, re_pr, stream, &cs);
+}
+
+namespace {
+// unfused tail of srk_rhs_combine: ynext = yb + sum c F + cself f (k_combine)
+int comb_after(srk_plan* p, const CombSpec* cs, const cplx* f, cudaStream_t st) {
+  CombArgs a;
+  memset(&a, 0, sizeof(a));
+  a.y = cs->yb;
+  for (int j = 0; j < cs->nt; ++j) {
+    a.F[j] = cs->F[j];
+    a.c[j] = cs->c[j];
+  }
+  a.F[cs->nt] = f;
+  a.c[cs->nt] = cs->cself;
+  a.nt = cs->nt + 1;
+  a.out = cs->ynext;
+  a.n = (long long)(p->dims + (p->density ? 1 : 0)) * p->modes;
+  srk_launch_combine(a, st);
+  p->last_launches++;
+  return check_launch("k_combine");
+}
+
+int rhs_impl(srk_plan* p, const void* y_, void* f_, double nu, double ri, double re_pr, void* stream,
+             const CombSpec* cs) {
   if (!p) return fail(SRK_ERR_INVALID, "null plan");
   int rc = need_ws(p);
   if (rc) return rc;
@@ -740,11 +798,12 @@ int srk_rhs(srk_plan* p, const void* y_, void* f_, double nu, double ri, double 
     c5.ck1 = p->ck1;
     c5.ck2 = p->ck2;
     c5.comp_stride = p->modes;
-    return launch_fwd_proj(p, KK_FWD_PROJ, c5, st);
+    if ((rc = launch_fwd_proj(p, KK_FWD_PROJ, c5, st))) return rc;
+    return cs ? comb_after(p, cs, f, st) : SRK_OK;
   }
   if ((rc = launch_col(p, KK_FWD_P, c5, st))) return rc;
   // K6: projection + viscous (+ Boussinesq terms)
-  ProjArgs pa;
+  ProjArgs pa{};
   pa.g = geom(p);
   pa.G = gbuf;
   pa.y = y;
@@ -754,11 +813,25 @@ int srk_rhs(srk_plan* p, const void* y_, void* f_, double nu, double ri, double 
   pa.nu = nu;
   pa.ri = ri;
   pa.re_pr = re_pr;
-  srk_launch_project(pa, st);
+  bool fused = false;
+  if (cs && !getenv("SRK_NO_PCOMB")) {
+    pa.yb = cs->yb;
+    pa.nt = cs->nt;
+    for (int j = 0; j < cs->nt; ++j) {
+      pa.F[j] = cs->F[j];
+      pa.c[j] = cs->c[j];
+    }
+    pa.cself = cs->cself;
+    pa.ynext = cs->ynext;
+    fused = srk_launch_project_comb(pa, st);
+  }
+  if (!fused) srk_launch_project(pa, st);
   p->last_launches++;
   if (p->timing && p->nev < 16) cudaEventRecord(p->ev[p->nev++], st);
-  return check_launch("k_project");
+  if ((rc = check_launch("k_project"))) return rc;
+  return (cs && !fused) ? comb_after(p, cs, f, st) : SRK_OK;
 }
+}  // namespace
 
 int srk_rhs_timed(srk_plan* p, const void* y, void* f, double nu, double ri, double re_pr, void* stream,
                   float* ms_out, int max_kernels) {
@@ -1047,7 +1120,7 @@ int srk_slab_finish(srk_plan* p, const void* recv2, const void* y, void* f, doub
     return launch_fwd_proj(p, KK_FWD_PROJ_SLAB, c5, st);
   }
   if ((rc = launch_col(p, KK_FWD_P_SLABI, c5, st))) return rc;
-  ProjArgs pa;
+  ProjArgs pa{};
   pa.g = geom(p);
   pa.G = p->A;
   pa.y = (const cplx*)y;
@@ -1203,7 +1276,7 @@ int srk_slab_project(srk_plan* p, const void* y, void* f, double nu, double ri, 
   if (!p || !p->Mx) return fail(SRK_ERR_INVALID, "not a slab plan");
   int rc = need_ws(p);
   if (rc) return rc;
-  ProjArgs pa;
+  ProjArgs pa{};
   pa.g = geom(p);
   pa.G = p->B;
   pa.y = (const cplx*)y;

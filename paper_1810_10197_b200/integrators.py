@@ -166,31 +166,56 @@ def _as_dev_fn(f):
         if not isinstance(r, torch.Tensor):
             r = torch.from_numpy(np.ascontiguousarray(r)).to(y.device)
         return r
+    if callable(getattr(f, "eval_combine", None)):
+        g.eval_combine = f.eval_combine  # device operator: RHS + next accumulation in one call
     return g
+
+
+# srk_rhs_combine carries at most this many earlier stages on its fused path
+_FUSED_MAX_TERMS = 6
 
 
 def run_stages(f, y, t, h, pair, first_stage=None):
     """Stage loop of integrators.py:322-339 on the device.
 
     Returns (stages, y_new, evals).  For FSAL pairs y_new is the last stage's
-    input (identical arithmetic to y + sum h b_i F_i since A[-1] == b).
+    input (identical arithmetic to y + sum h b_i F_i since A[-1] == b).  When
+    ``f`` is a device operator with ``eval_combine`` (FlowRHS), each stage's
+    RHS call also forms the accumulation that consumes it -- the next stage
+    input (row i+1 of A) or, for non-FSAL pairs, y_new -- bitwise the same sums,
+    without reading the new stage back (srk_rhs_combine).
     """
     A, b, c, s = pair.A, pair.b, pair.c, pair.s
+    fused = getattr(f, "eval_combine", None)
     evals = 0
     stages = [None] * s
-    if first_stage is not None:
-        stages[0] = first_stage
-    else:
-        stages[0] = f(t, y)
-        evals += 1
+    pending = None  # input of stage i (or y_new) formed by the previous stage's call
     yi = None
-    for i in range(1, s):
-        terms = [(h * A[i, j], stages[j]) for j in range(i) if A[i, j] != 0.0]
-        yi = combine(y, terms)
-        stages[i] = f(t + c[i] * h, yi)
+    for i in range(s):
+        if i == 0:
+            if first_stage is not None:
+                stages[0] = first_stage
+                continue
+            xi = y
+        elif pending is not None:
+            xi, pending = pending, None
+        else:
+            xi = combine(y, [(h * A[i, j], stages[j]) for j in range(i) if A[i, j] != 0.0])
+        if i > 0:
+            yi = xi
+        row = A[i + 1] if i + 1 < s else (None if pair.fsal else b)
+        if fused is not None and row is not None and row[i] != 0.0:
+            terms = [(h * row[j], stages[j]) for j in range(i) if row[j] != 0.0]
+            if len(terms) <= _FUSED_MAX_TERMS:
+                stages[i], pending = fused(t + c[i] * h, xi, y, terms, h * row[i])
+                evals += 1
+                continue
+        stages[i] = f(t + c[i] * h, xi)
         evals += 1
     if pair.fsal and yi is not None:
         y_new = yi
+    elif pending is not None:
+        y_new = pending
     else:
         y_new = combine(y, [(h * b[i], stages[i]) for i in range(s) if b[i] != 0.0])
     return stages, y_new, evals

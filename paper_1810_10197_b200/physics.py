@@ -77,6 +77,28 @@ class FlowRHS:
         _native.count(pl.lib.srk_rhs_launch_count(pl.h))
         return from_device(f, was_np)
 
+    def eval_combine(self, t, fields, ybase, terms, coef_self):
+        """``f(t, fields)`` plus the rk_step accumulation that consumes it
+        (integrators.py:327-339): returns ``(f, ybase + sum c_j F_j + coef_self f)``,
+        summed in ascending stage order with f last -- bitwise the unfused
+        ``combine(ybase, terms + [(coef_self, f)])`` -- in one srk_rhs_combine call
+        (the 3D projection kernel forms the sum while f is in registers)."""
+        y, _ = to_device(fields, torch.complex128)
+        yb, _ = to_device(ybase, torch.complex128)
+        f = torch.empty_like(y)
+        ynext = torch.empty_like(y)
+        p = self.params
+        pl = self.plan
+        Fs = [F for _, F in terms]
+        _native.check(pl.lib.srk_rhs_combine(pl.bind(), _native.ptr(y), _native.ptr(f), 1.0 / p.reynolds,
+                                             float(p.richardson), float(p.reynolds) * float(p.prandtl),
+                                             _native.ptr(yb), len(Fs), _native.ptr_array(Fs),
+                                             _native.dbl_array([c for c, _ in terms]), float(coef_self),
+                                             _native.ptr(ynext), _native.stream_ptr()), "srk_rhs_combine")
+        self.calls += 1
+        _native.count(pl.lib.srk_rhs_launch_count(pl.h))
+        return f, ynext
+
     def launches_per_call(self):
         return int(self.plan.lib.srk_rhs_launch_count(self.plan.h))
 

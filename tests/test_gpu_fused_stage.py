@@ -1,0 +1,91 @@
+"""RHS + next-stage accumulation in one call (srk_rhs_combine, FlowRHS.eval_combine)
+must be bitwise what the unfused srk_rhs + srk_combine produce, and the stage loop
+(integrators.py:322-347) must give bitwise the same stages and y_new with and
+without the fusion.  Needs a B200."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+srk = pytest.importorskip("paper_1810_10197_b200")
+from paper_1810_10197_b200 import integrators  # noqa: E402
+
+
+def _state(g, ncomp, seed):
+    gen = torch.Generator(device="cuda").manual_seed(seed)
+    y = torch.randn((ncomp,) + g.kshape, dtype=torch.complex128, device="cuda", generator=gen)
+    return y * (float(np.prod(g.shape)) / torch.linalg.vector_norm(y).item())
+
+
+CASES = [((32, 32, 32), False), ((16, 32, 48), False), ((64, 64, 64), False), ((256, 256, 256), False),
+         ((64, 256), False), ((16, 32, 24), True), ((64, 128), True)]
+
+
+@pytest.mark.parametrize("shape,density", CASES)
+@pytest.mark.parametrize("nt", [0, 1, 3, 6])
+def test_rhs_combine_is_bitwise_rhs_then_combine(shape, density, nt):
+    g = srk.Grid(shape)
+    rhs = srk.FlowRHS(g, srk.PhysParams(800.0, 1.3, 0.7), density=density)
+    nc = g.dims + (1 if density else 0)
+    y = _state(g, nc, 1)
+    yb = _state(g, nc, 2)
+    Fs = [_state(g, nc, 10 + j) for j in range(nt)]
+    cs = [0.013 * (j + 1) - 0.004 for j in range(nt)]
+    terms = list(zip(cs, Fs))
+    f_ref = rhs(0.0, y)
+    yn_ref = integrators.combine(yb, terms + [(0.0271, f_ref)])
+    f, yn = rhs.eval_combine(0.0, y, yb, terms, 0.0271)
+    assert torch.equal(f, f_ref)
+    assert torch.equal(yn, yn_ref)
+
+
+def _unfused(rhs):
+    return lambda t, y: rhs(t, y)  # plain callable: no eval_combine
+
+
+@pytest.mark.parametrize("name", ["bs5", "rk4", "dp5", "kcl5"])
+@pytest.mark.parametrize("shape", [(32, 32, 32), (128, 128, 128)])
+def test_stage_loop_fused_equals_unfused(name, shape):
+    g = srk.Grid(shape)
+    y = srk.hit_init(g, srk.ProblemSpec("hit", a=4.0, energy=0.5, seed=42)).fields
+    rhs = srk.FlowRHS(g, srk.PhysParams(1600.0))
+    pair = srk.make_pair(name)
+    h = 2e-3
+    for first in (None, rhs(0.0, y)):
+        st_a, yn_a, ev_a = integrators.run_stages(integrators._as_dev_fn(rhs), y, 0.0, h, pair, first)
+        st_b, yn_b, ev_b = integrators.run_stages(_unfused(rhs), y, 0.0, h, pair, first)
+        assert ev_a == ev_b
+        assert torch.equal(yn_a, yn_b)
+        for a, b in zip(st_a, st_b):
+            assert torch.equal(a, b)
+
+
+def test_adaptive_step_fused_equals_unfused_256():
+    g = srk.Grid((256, 256, 256))
+    y = srk.hit_init(g, srk.ProblemSpec("hit", a=4.0, energy=0.5, seed=42)).fields
+    rhs = srk.FlowRHS(g, srk.PhysParams(2000.0))
+    cfg = srk.ControllerConfig(tol_abs=1e-6, tol_rel=1e-6)
+    f0 = rhs(0.0, y)
+    outs = []
+    for fn in (rhs, _unfused(rhs)):
+        st = srk.ControllerState(h=1e-3)
+        outs.append(srk.adaptive_advance(y, 0.0, srk.make_bs5(), st, cfg, fn, first_stage=f0, grid=g))
+    a, b = outs
+    assert a.h_next == b.h_next and a.errs == b.errs and a.rhs_evals == b.rhs_evals
+    assert torch.equal(a.y_new, b.y_new) and torch.equal(a.last_stage, b.last_stage)
+
+
+def test_rhs_combine_rejects_aliasing():
+    g = srk.Grid((32, 32, 32))
+    rhs = srk.FlowRHS(g, srk.PhysParams(800.0))
+    y = _state(g, 3, 1)
+    lib = rhs.plan.lib
+    from paper_1810_10197_b200 import _native
+
+    with pytest.raises(ValueError):  # SRK_ERR_INVALID -> ValueError (_native.check)
+        f = torch.empty_like(y)
+        _native.check(lib.srk_rhs_combine(rhs.plan.bind(), _native.ptr(y), _native.ptr(f), 1e-3, 1.0, 1.0,
+                                          _native.ptr(y), 0, _native.ptr_array([]), _native.dbl_array([]), 0.5,
+                                          _native.ptr(y), _native.stream_ptr()))
