@@ -951,3 +951,201 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_xfwd_proj
   }
   cluster.sync();  // peers may still be reading this CTA's tile
 }
+
+
+// ---------------------------------------------------------------------------
+// Stages after a caller-run prefix with the thread -> (column, butterfly) map
+// redone per stage and NCOL * M/R butterflies looped over the CTA (each
+// thread keeps ceil(NCOL*M/R / NT) butterflies live across the barrier).
+// ---------------------------------------------------------------------------
+template <int M, class L, int SIGN, int NCOL, int NT, int Ls, int R, int... Rest>
+struct LoopStageZ {
+  template <class ST>
+  __device__ __forceinline__ static void go(cplx* sm, const cplx* tw, ST& st) {
+    constexpr int STRIDE = M / R;
+    constexpr int TOT = NCOL * STRIDE;
+    constexpr int NB = (TOT + NT - 1) / NT;
+    constexpr bool LAST = (sizeof...(Rest) == 0);
+    const int tid = threadIdx.x;
+    cplx v[NB][R];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int u = tid + b * NT;
+      if (TOT % NT == 0 || u < TOT) {
+        const int col = u / STRIDE, j = u - col * STRIDE;
+        if constexpr (STRIDE % 8 == 0) {
+          const int a0 = L::idx(j, col);
+#pragma unroll
+          for (int t = 0; t < R; ++t) v[b][t] = sm[a0 + t * (STRIDE / 8) * L::STEP8];
+        } else {
+#pragma unroll
+          for (int t = 0; t < R; ++t) v[b][t] = sm[L::idx(j + t * STRIDE, col)];
+        }
+        const unsigned k = (unsigned)j % (unsigned)Ls;
+        stage_twiddle<M, R, SIGN>(v[b], tw, k * (unsigned)(M / (Ls * R)));
+        DFT<R, SIGN>::run(v[b]);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int u = tid + b * NT;
+      if (TOT % NT == 0 || u < TOT) {
+        const int col = u / STRIDE, j = u - col * STRIDE;
+        const unsigned k = (unsigned)j % (unsigned)Ls;
+        const int base = (int)(((unsigned)j - k) * (unsigned)R + k);
+        if constexpr (LAST) {
+#pragma unroll
+          for (int q = 0; q < R; ++q) st(base + q * Ls, col, v[b][q]);
+        } else if constexpr (Ls % 8 == 0) {
+          const int a0 = L::idx(base, col);
+#pragma unroll
+          for (int q = 0; q < R; ++q) sm[a0 + q * (Ls / 8) * L::STEP8] = v[b][q];
+        } else {
+#pragma unroll
+          for (int q = 0; q < R; ++q) sm[L::idx(base + q * Ls, col)] = v[b][q];
+        }
+      }
+    }
+    if constexpr (!LAST) {
+      __syncthreads();
+      LoopStageZ<M, L, SIGN, NCOL, NT, Ls * R, Rest...>::go(sm, tw, st);
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// NS3 z-pass, one pencil per CTA (SRK_ZP1): 3 inverse complex columns
+// (two-for-one: [u0 u1][u2 w0][w1 w2]), fused middle stage (last inverse
+// radix-4 | u x w | first forward radix-4, two butterfly rows per thread),
+// forward suffix on 2 columns [P0 + i P1][P2] looped over the CTA, extraction
+// (two-for-one for P0/P1, P2 read directly).  A third of the pencil-pair
+// kernel's shared memory and half its threads per CTA: 5 CTAs (15 warps) per
+// SM with independent phases instead of 2 CTAs (12 warps) -- at the price of
+// one extra 768-point forward transform per two pencils (P2 rides alone).
+// ---------------------------------------------------------------------------
+template <int M, class L, class EngI, int... FR>
+__global__ void __launch_bounds__(M / 8, 5) k_zpass_ns3p(const ZArgs a, int, int) {
+  extern __shared__ __align__(16) cplx smraw[];
+  cplx* const sm = smraw + EngI::TWN;  // [twiddle table][tile]
+  const cplx* const twp = smraw;
+  tw_fill<M>(smraw, a.tw);
+  constexpr int S = 3, NT = M / 8, K = M / 3 + 1, Q = M / 4;
+  static_assert(EngI::NT == NT, "inverse prefix must use M/8 threads");
+  static_assert(L::C == 3, "three tile columns");
+  const int pen = blockIdx.x;
+  const int tid = threadIdx.x;
+  // ---- staging: 6 real-signal rows of K modes via 1D TMA bulk copies ----
+  cplx* stg = sm;
+  __shared__ __align__(8) unsigned long long mbar;
+  if (tid == 0) {
+    mbar_init(&mbar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    mbar_expect_tx(&mbar, (unsigned)(2 * S * K * 16));
+    for (int s = 0; s < 2 * S; ++s)
+      bulk_g2s(stg + s * K, a.in + s * a.in_sig_stride + (long long)pen * K, (unsigned)(K * 16), &mbar);
+    if (a.pf_dist) {
+      const int q0 = pen + a.pf_dist;
+      if (q0 < a.P)
+        for (int s = 0; s < 2 * S; ++s)
+          bulk_prefetch_l2(a.in + s * a.in_sig_stride + (long long)q0 * K, (unsigned)(K * 16));
+    }
+  }
+  mbar_wait(&mbar, 0);
+  cp_async_wait_all();
+  __syncthreads();
+  auto hs = [&](int g, int k) -> cplx {
+    const bool head = k < K;
+    const bool tail = k >= M - (K - 1);
+    const int kk = head ? k : (tail ? M - k : 0);
+    cplx X = stg[g * K + kk];
+    X.y = tail ? -X.y : X.y;
+    if (k == 0) X.y = 0.0;  // irfft ignores Im of DC
+    return (head || tail) ? X : cmk(0.0, 0.0);
+  };
+  {
+    auto ld = [&](int k, int c) -> cplx {
+      cplx A = hs(2 * c, k), B = hs(2 * c + 1, k);
+      return cmk(A.x - B.y, A.y + B.x);
+    };
+    auto st = [&](int n, int c, cplx v) { sm[L::idx(n, c)] = v; };
+    EngI::template run_ws<+1, true, true>(a.gp, sm, twp, S, ld, st);
+  }
+  __syncthreads();
+  // ---- fused: last inverse radix-4 | u x w | first forward radix-4; rows j, j + NT ----
+  {
+    cplx v[2][S][4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = tid + h * NT;
+#pragma unroll
+      for (int c = 0; c < S; ++c) {
+        if constexpr (Q % 8 == 0) {
+          const int a0 = L::idx(j, c);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) v[h][c][t] = sm[a0 + t * (Q / 8) * L::STEP8];
+        } else {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) v[h][c][t] = sm[L::idx(j + t * Q, c)];
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = tid + h * NT;
+      cplx w[4];
+#pragma unroll
+      for (int t = 1; t < 4; ++t) {
+        w[t] = tw_get<M>(twp, (unsigned)(t * j));
+        w[t].y = -w[t].y;  // inverse sign
+      }
+#pragma unroll
+      for (int c = 0; c < S; ++c) {
+#pragma unroll
+        for (int t = 1; t < 4; ++t) v[h][c][t] = cmul(v[h][c][t], w[t]);
+        DFT<4, +1>::run(v[h][c]);
+      }
+      cplx F0[4], F1[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double r[6] = {v[h][0][q].x, v[h][0][q].y, v[h][1][q].x, v[h][1][q].y, v[h][2][q].x, v[h][2][q].y};
+        double o[3];
+        zphys<ZOP_NS3>(r, o);
+        F0[q] = cmk(o[0], o[1]);
+        F1[q] = cmk(o[2], 0.0);
+      }
+      DFT<4, -1>::run(F0);
+      DFT<4, -1>::run(F1);
+      const int a0 = L::idx(4 * j, 0), a1 = L::idx(4 * j, 1);  // Stockham stage-1 outputs: rows 4j + q
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        sm[a0 + q * L::ROWSTEP] = F0[q];
+        sm[a1 + q * L::ROWSTEP] = F1[q];
+      }
+    }
+  }
+  __syncthreads();
+  // ---- forward suffix (Ls = 4 ...) on the 2 packed columns ----
+  {
+    auto st = [&](int n, int c, cplx v) {
+      if (n < K - 1 || n > M - K + 1) sm[L::idx(n, c)] = v;
+    };
+    LoopStageZ<M, L, -1, 2, NT, 4, FR...>::go(sm, twp, st);
+  }
+  __syncthreads();
+  // ---- extraction: P0, P1 from column 0 (two-for-one), P2 = column 1; kz = n/2 zeroed ----
+  for (int k = tid; k < K; k += NT) {
+    const bool live = k != K - 1;
+    const cplx Zk = live ? sm[L::idx(k, 0)] : cmk(0.0, 0.0);
+    const cplx Zm = live ? sm[L::idx(k == 0 ? 0 : M - k, 0)] : cmk(0.0, 0.0);
+    const cplx P2 = live ? sm[L::idx(k, 1)] : cmk(0.0, 0.0);
+    cplx* o = a.out + (long long)pen * K + k;
+    o[0] = cmk(0.5 * (Zk.x + Zm.x), 0.5 * (Zk.y - Zm.y));
+    o[a.out_sig_stride] = cmk(0.5 * (Zk.y + Zm.y), -0.5 * (Zk.x - Zm.x));
+    o[2 * a.out_sig_stride] = (k == 0) ? cmk(P2.x, 0.0) : P2;
+  }
+}

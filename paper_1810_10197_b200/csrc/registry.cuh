@@ -36,6 +36,7 @@ struct KEntry {
   int cols;  // columns per block (strided) / complex columns capacity (z)
   int smem;  // dynamic shared memory bytes
   int persistent = 0;  // z pass: grid-stride over pencil pairs (grid = resident CTAs)
+  int ppc = 2;         // z pass: pencils per CTA (k_zpass_ns3p: 1)
 };
 
 // plain z ops process up to this many real signals per pencil per launch
@@ -164,6 +165,15 @@ struct GenCols {
 // NS3 z-pass with the fused middle stage: inverse prefix (IR..., product M/4),
 // forward suffix (FR..., product M/4), E = 24.
 // Pitch >= 4K so that tile columns 3..5 hold the 12 staged rows of K modes.
+// NS3 z-pass, one pencil per CTA (k_zpass_ns3p): inverse prefix (IR..., product
+// M/4) on 3 columns with E = 24 (M/8 threads), forward suffix FR... looped.
+#define SRK_NS3P(M, IR, FR)                                                                        \
+  {                                                                                                \
+    using ZL = ColTile<M, 3>;                                                                      \
+    using EI = FastFFT<M, 24, ZL, SRK_UNPAREN IR>;                                                 \
+    t[KK_Z_NS3] = KEntry{(const void*)(k_zpass_ns3p<M, ZL, EI, SRK_UNPAREN FR>), M / 8, 3,          \
+                         (int)(ZL::SIZE * 16) + EI::TWN * 16, 0, 1};                               \
+  }
 #define SRK_NS3F(M, IR, EF, FR)                                                                     \
   {                                                                                                \
     using ZL = ColTile<M, 6>;                                                                           \

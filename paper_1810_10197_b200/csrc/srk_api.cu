@@ -394,7 +394,18 @@ int launch_z(srk_plan* p, int kind, ZArgs a, int S_rt, int So_rt, cudaStream_t s
   if (rc) return rc;
   if ((rc = get_tw(p, a.M, &a.tw))) return rc;
   if ((rc = ensure_smem(e))) return rc;
-  int grid = (a.P + 1) / 2;
+  int grid = e.ppc == 1 ? a.P : (a.P + 1) / 2;
+  if (e.ppc == 1 && a.pf_dist) {  // L2 warm-up one wave of resident CTAs ahead (in pencils)
+    static const int d1 = [&] {
+      if (const char* s = getenv("SRK_ZPF1")) return atoi(s);
+      int per_sm = 0, dev = 0, nsm = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, e.fn, e.nt, e.smem);
+      return std::max(1, per_sm) * nsm;
+    }();
+    a.pf_dist = d1;
+  }
   if (e.persistent && !getenv("SRK_NOPERSIST")) {
     int per_sm = 0, dev = 0, nsm = 148;
     cudaGetDevice(&dev);
