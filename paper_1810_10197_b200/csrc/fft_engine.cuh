@@ -38,23 +38,27 @@ struct RowTile {
   // rows 8j+q and 8(j+1)+q in opposite halves, so the stride-R stores of the
   // first Stockham stage and the consecutive-row accesses of later stages
   // both split 4/4 over the halves (conflict free).
+  // C == 2 (one 32 B row per 16 B bank pair): the same pad row every 8 rows
+  // makes the stride-24 stores of the first Stockham stage (rows 24j + q) and
+  // the consecutive-row accesses of later stages conflict free per 8-lane
+  // wavefront (tj 0..3 land in slots 0, 6, 4, 2 of 8).
   static constexpr int SIZE = (C_ >= 8) ? M_ * C_ : (M_ + M_ / 8 + 1) * C_;  // in cplx
   // idx(row + 8m) = idx(row) + m*STEP8; within an aligned group of 8 rows
   // idx(row + 1) = idx(row) + ROWSTEP  (lets the stages hoist index math)
-  static constexpr int STEP8 = (C_ >= 8) ? 8 * C_ : 36;
-  static constexpr int ROWSTEP = (C_ >= 8) ? C_ : 4;
+  static constexpr int STEP8 = (C_ >= 8) ? 8 * C_ : 9 * C_;
+  static constexpr int ROWSTEP = C_;
   __device__ __forceinline__ static int idx(int row, int col) {
     if constexpr (C_ >= 8) {
       return row * C_ + col;
     } else {
-      static_assert(C_ == 4, "RowTile supports C = 4 or C >= 8");
-      return (row + (row >> 3)) * 4 + col;
+      static_assert(C_ == 4 || C_ == 2, "RowTile supports C = 2, 4 or C >= 8");
+      return (row + (row >> 3)) * C_ + col;
     }
   }
   SRK_DEV static int col_of(int tid, int) { return tid % C_; }
   SRK_DEV static int tj_of(int tid, int) { return tid / C_; }
   // idx(base + q, c) - idx(base, c) for base a multiple of 8
-  static constexpr int roff(int q) { return C_ >= 8 ? q * C_ : (q + (q >> 3)) * 4; }
+  static constexpr int roff(int q) { return C_ >= 8 ? q * C_ : (q + (q >> 3)) * C_; }
 };
 
 template <int M_, int C_, int MINPITCH = 0>

@@ -4,7 +4,10 @@
 #ifdef SRK_OLD768
 SRK_DEFINE_SIZE(srk_reg_768_base, 768, 24, 4, 8, 8, 12)
 #else
-SRK_DEFINE_SIZE_1(srk_reg_768_base, 768, 4, (24, 32), 24, 24, (8, 8, 12), 8, 8, 12)
+#ifndef SRK_C768
+#define SRK_C768 4  // strided-pass tile columns
+#endif
+SRK_DEFINE_SIZE_1(srk_reg_768_base, 768, SRK_C768, (24, 32), 24, 24, (8, 8, 12), 8, 8, 12)
 #endif
 void srk_reg_768(KEntry* t) {
   srk_reg_768_base(t);

@@ -179,7 +179,7 @@ __device__ __forceinline__ void tma_stage(cplx* sm, const CUtensorMap* tm, int w
 }
 
 template <class Eng, int KIND, int SIGN, int FL = 0>
-__global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : (Eng::NT <= 192 ? 2 : 1))) k_colpass(const PassArgs a, const __grid_constant__ CUtensorMap tm,
+__global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 ? 3 : (Eng::NT <= 192 ? 2 : 1)))) k_colpass(const PassArgs a, const __grid_constant__ CUtensorMap tm,
                                                                   const __grid_constant__ CUtensorMap tmo) {
   extern __shared__ __align__(128) cplx smraw[];
   cplx* const sm = smraw + Eng::TWN;
