@@ -17,6 +17,7 @@ Needs a B200 (about 40 GB of device memory at 512^3).
 
 import math
 
+import numpy as np
 import pytest
 import torch
 
@@ -28,53 +29,66 @@ N = 512
 RE = 1000.0
 
 
-def _kvecs(n, dev):
-    """Mode labels (grid.py:75-82): full axes fftfreq with n/2 relabelled +n/2, r2c axis 0..n/2."""
-    full = torch.cat([torch.arange(0, n // 2 + 1), torch.arange(-(n // 2) + 1, 0)]).to(dev, torch.float64)
-    half = torch.arange(0, n // 2 + 1, device=dev, dtype=torch.float64)
-    return full.view(n, 1, 1), full.view(1, n, 1), half.view(1, 1, n // 2 + 1)
+def _kvecs(n, dev, lengths=None):
+    """Wavenumbers (grid.py:75-93): full axes fftfreq with n/2 relabelled +n/2, r2c axis 0..n/2,
+    times 2 pi / L.  n: an int (cube) or (n0, n1, n2)."""
+    ns = (n, n, n) if isinstance(n, int) else tuple(n)
+    ls = lengths or (2 * math.pi,) * 3
+
+    def full(m):
+        return torch.cat([torch.arange(0, m // 2 + 1), torch.arange(-(m // 2) + 1, 0)]).to(dev, torch.float64)
+
+    k0 = full(ns[0]).view(-1, 1, 1) * (2 * math.pi / ls[0])
+    k1 = full(ns[1]).view(1, -1, 1) * (2 * math.pi / ls[1])
+    k2 = torch.arange(0, ns[2] // 2 + 1, device=dev, dtype=torch.float64).view(1, 1, -1) * (2 * math.pi / ls[2])
+    return k0, k1, k2
 
 
 def _widen(s, n):
     """One component: x pad (x 1.5^3) + ifft, y pad + ifft, irfft(n=m) along z (spectral.py:215-261)."""
-    m, h = 3 * n // 2, n // 2
-    b = torch.zeros((m, n, h + 1), dtype=torch.complex128, device=s.device)
-    b[: h + 1] = s[: h + 1] * 1.5 ** 3
-    b[m - (h - 1):] = s[h + 1:] * 1.5 ** 3
+    n0, n1, n2 = (n, n, n) if isinstance(n, int) else n
+    m0, m1, m2 = 3 * n0 // 2, 3 * n1 // 2, 3 * n2 // 2
+    h0, h1 = n0 // 2, n1 // 2
+    kz = n2 // 2 + 1
+    b = torch.zeros((m0, n1, kz), dtype=torch.complex128, device=s.device)
+    b[: h0 + 1] = s[: h0 + 1] * 1.5 ** 3
+    b[m0 - (h0 - 1):] = s[h0 + 1:] * 1.5 ** 3
     a = torch.fft.ifft(b, dim=0)
     del b
-    b = torch.zeros((m, m, h + 1), dtype=torch.complex128, device=s.device)
-    b[:, : h + 1] = a[:, : h + 1]
-    b[:, m - (h - 1):] = a[:, h + 1:]
+    b = torch.zeros((m0, m1, kz), dtype=torch.complex128, device=s.device)
+    b[:, : h1 + 1] = a[:, : h1 + 1]
+    b[:, m1 - (h1 - 1):] = a[:, h1 + 1:]
     del a
     b = torch.fft.ifft(b, dim=1)
-    return torch.fft.irfft(b, n=m, dim=2)
+    return torch.fft.irfft(b, n=m2, dim=2)
 
 
 def _narrow(p, n):
     """One component: rfft along z keeping n/2+1, fft + truncation on y then x (x (1/1.5)^3),
     Nyquist rows zeroed (spectral.py:263-304)."""
-    m, h = 3 * n // 2, n // 2
-    a = torch.fft.rfft(p, dim=2)[:, :, : h + 1]
+    n0, n1, n2 = (n, n, n) if isinstance(n, int) else n
+    m0, m1 = 3 * n0 // 2, 3 * n1 // 2
+    h0, h1, kz = n0 // 2, n1 // 2, n2 // 2 + 1
+    a = torch.fft.rfft(p, dim=2)[:, :, :kz]
     a = torch.fft.fft(a, dim=1)
-    o = torch.zeros((m, n, h + 1), dtype=torch.complex128, device=p.device)
-    o[:, :h] = a[:, :h]
-    o[:, h + 1:] = a[:, m - (h - 1):]
+    o = torch.zeros((m0, n1, kz), dtype=torch.complex128, device=p.device)
+    o[:, :h1] = a[:, :h1]
+    o[:, h1 + 1:] = a[:, m1 - (h1 - 1):]
     del a
     a = torch.fft.fft(o, dim=0)
     del o
     s = (1.0 / 1.5) ** 3
-    o = torch.zeros((n, n, h + 1), dtype=torch.complex128, device=p.device)
-    o[:h] = a[:h] * s
-    o[h + 1:] = a[m - (h - 1):] * s
-    o[:, :, h] = 0.0
+    o = torch.zeros((n0, n1, kz), dtype=torch.complex128, device=p.device)
+    o[:h0] = a[:h0] * s
+    o[h0 + 1:] = a[m0 - (h0 - 1):] * s
+    o[:, :, kz - 1] = 0.0
     o.imag[0, 0, 0] = 0.0
     return o
 
 
-def torch_ns_rhs(u, n, re):
+def torch_ns_rhs(u, n, re, lengths=None):
     """Independent device restatement of ns_rhs (physics.py:105-129) on torch.fft."""
-    k0, k1, k2 = _kvecs(n, u.device)
+    k0, k1, k2 = _kvecs(n, u.device, lengths)
     ks = (k0, k1, k2)
     w = torch.empty_like(u)
     w[0] = 1j * (k1 * u[2] - k2 * u[1])
@@ -167,3 +181,17 @@ def test_rhs_512_bitwise_repeatable(state):
     g, u, f = state
     f2 = srk.FlowRHS(g, srk.PhysParams(RE))(0.0, u)
     assert torch.equal(f, f2)
+
+
+@pytest.mark.parametrize("shape,lengths", [((64, 128, 512), (2 * math.pi, 3.0, 5.0)),
+                                           ((128, 32, 512), (1.0, 2 * math.pi, 2 * math.pi))])
+def test_rhs_anisotropic_z512_matches_cufft_restatement(shape, lengths):
+    """The one-pencil z-pass (M = 768) on non-cubic grids / non-2 pi boxes."""
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    g = srk.Grid(shape, lengths)
+    u = torch.randn((3,) + g.kshape, dtype=torch.complex128, device="cuda", generator=gen)
+    u *= float(np.prod(shape)) / torch.linalg.vector_norm(u).item()
+    f = srk.FlowRHS(g, srk.PhysParams(700.0))(0.0, u)
+    ref = torch_ns_rhs(u, shape, 700.0, lengths)
+    rel = (torch.linalg.vector_norm(f - ref) / torch.linalg.vector_norm(ref)).item()
+    assert rel <= 1e-12, f"{shape}: rel L2 {rel:.3e}"
