@@ -297,6 +297,15 @@ def run_native(args, rank, world, local_rank):
             traffic = json.load(fh).get(str(n), {}).get(kn[dom])
     except Exception:
         pass
+    # The FFT passes are bound by fp64 issue latency, not HBM (DESIGN.md §6,
+    # tools/l2_probe.py): the ncu fp64-pipe activity of the dominant kernel from
+    # the committed profile, when one exists for this size.
+    fp64 = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_fp64_pipe.json")) as fh:
+            fp64 = json.load(fh).get(str(n), {}).get(kn[dom])
+    except Exception:
+        pass
 
     # ---- e2e: through the public API with pinned host buffers ----
     # The state crosses PCIe every step: y is copied host->device, the cached
@@ -362,7 +371,8 @@ def run_native(args, rank, world, local_rank):
                      "peak_source": peak_src,
                      "kernel_ms": {k: round(float(v), 4) for k, v in zip(kn, kms)},
                      "kernel_share": {k: round(float(v), 4) for k, v in zip(kn, shares)},
-                     "algorithmic_bytes_per_launch": mb["per_kernel"][kn[dom]]},
+                     "algorithmic_bytes_per_launch": mb["per_kernel"][kn[dom]],
+                     "fp64_pipe_active": fp64},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
