@@ -114,7 +114,9 @@ __device__ __forceinline__ KVec kvec32(unsigned idx, const GeomArgs& g) {
 // k_combine produces from the stored f, without reading f back.  ybase and the
 // F_t ride in the same ring; chunks shrink to 128 modes to keep two CTAs/SM.
 #define SRK_PT_CH 256
-#define SRK_PC_CH 128
+#ifndef SRK_PC_CH
+#define SRK_PC_CH 256  // modes per chunk (and threads) of the fused K6 + stage-sum kernel; ncu: 128 -> 256 is 1-7% faster
+#endif
 template <int DIMS, bool DENS, int NTC = -1>
 __global__ void __launch_bounds__(NTC < 0 ? SRK_PT_CH : SRK_PC_CH) k_project_tma(const ProjArgs a) {
   extern __shared__ __align__(128) cplx psm[];
