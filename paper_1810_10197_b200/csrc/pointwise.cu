@@ -112,7 +112,8 @@ __device__ __forceinline__ KVec kvec32(unsigned idx, const GeomArgs& g) {
 // ascending in the stage index with f = the tendency just computed (the last,
 // highest-index term), one rounding per multiply and add -- bitwise what
 // k_combine produces from the stored f, without reading f back.  ybase and the
-// F_t ride in the same ring; chunks shrink to 128 modes to keep two CTAs/SM.
+// F_t ride in the same ring (256-mode chunks: one CTA per SM from 4 earlier
+// stages on, still faster than 128-mode chunks at two CTAs per SM).
 #define SRK_PT_CH 256
 #ifndef SRK_PC_CH
 #define SRK_PC_CH 256  // modes per chunk (and threads) of the fused K6 + stage-sum kernel; ncu: 128 -> 256 is 1-7% faster
