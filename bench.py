@@ -116,6 +116,8 @@ class ClockSampler:
         return [c.strip() for c in out.split(",")] if out else None
 
     def _run(self):
+        if os.environ.get("SRK_BENCH_NO_CLOCKS"):  # diagnostics only: no sampling
+            return
         while not self._stop.is_set():
             try:
                 row = self._sample()
@@ -252,11 +254,21 @@ def run_native(args, rank, world, local_rank):
     l0 = _native.LAUNCHES
     with ClockSampler(local_rank) as clk:
         e0.record(st)
+        per_step = []  # diagnostics (SRK_BENCH_STEPS=1): device time and RHS count of every step
         for _ in range(args.steps):
+            if os.environ.get("SRK_BENCH_STEPS"):
+                es = torch.cuda.Event(enable_timing=True)
+                es.record(st)
             ev, diag = step(s)
             evals += ev
+            if os.environ.get("SRK_BENCH_STEPS"):
+                ee = torch.cuda.Event(enable_timing=True)
+                ee.record(st)
+                per_step.append((es, ee, ev))
         e1.record(st)
         torch.cuda.synchronize()
+        if per_step:
+            print("per-step ms/evals:", [(round(a.elapsed_time(b), 1), e) for a, b, e in per_step], file=sys.stderr)
     launches = _native.LAUNCHES - l0
     barrier()
     torch.cuda.synchronize()
