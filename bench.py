@@ -232,7 +232,7 @@ def run_native(args, rank, world, local_rank):
     def step(s):
         out = srk.adaptive_advance(s["y"], s["t"], pair, s["ctrl"], cfg, rhs, first_stage=s["f"], grid=g)
         y = out.y_new
-        srk.apply_forcing(y, g, energy, k_f)
+        srk.apply_forcing(y, g, energy, k_f, energy_sum=out.diag_sums[4])
         f = rhs(out.t_new, y)
         q = srk.diagnostics.reduce_sums(g, y, fl=f, flags=2, ncomp=3).tolist()
         s.update(y=y, t=out.t_new, f=f)
@@ -343,7 +343,7 @@ def run_native(args, rank, world, local_rank):
             fd = rhs(t2_, yd)
             q = srk.diagnostics.reduce_sums(g, yd, fl=fd, flags=2, ncomp=3).tolist()
             out = srk.adaptive_advance(yd, t2_, pair, s2["ctrl"], cfg, rhs, first_stage=fd, grid=g)
-            srk.apply_forcing(out.y_new, g, energy, k_f)
+            srk.apply_forcing(out.y_new, g, energy, k_f, energy_sum=out.diag_sums[4])
             ev2 += out.rhs_evals + 1
             t2_ = out.t_new
             y_h.copy_(out.y_new, non_blocking=True)
@@ -425,7 +425,8 @@ def run_slab(args, rank, world, local_rank):
         out = srk.adaptive_advance(s["y"], s["t"], pair, s["ctrl"], cfg, rhs, first_stage=s["f"], grid=g,
                                    allreduce=red, plan=plan)
         y = out.y_new
-        srk.apply_forcing(y, g, energy, k_f, plan=plan, allreduce=red, slab=(rank, world))
+        srk.apply_forcing(y, g, energy, k_f, plan=plan, allreduce=red, slab=(rank, world),
+                          energy_sum=out.diag_sums[4])
         f = rhs(out.t_new, y)
         q = red(reduce_sums(g, y, fl=f, flags=2, ncomp=3, plan=plan))
         s.update(y=y, t=out.t_new, f=f)

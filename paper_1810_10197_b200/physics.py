@@ -149,11 +149,16 @@ def forcing_band_slab(grid: Grid, k_f, device, rank, nranks):
     return _BANDS[key]
 
 
-def apply_forcing(u_hat, grid: Grid, target_energy, k_f, plan=None, allreduce=None, slab=None):
+def apply_forcing(u_hat, grid: Grid, target_energy, k_f, plan=None, allreduce=None, slab=None,
+                  energy_sum=None):
     """Rescale 0<|k|<=k_f in place to restore ``target_energy`` (physics.py:209-239).
 
     Slab runs pass the slab ``plan``, ``slab=(rank, nranks)`` and the rank-order
-    ``allreduce``; E_total and E_band are then global sums."""
+    ``allreduce``; E_total and E_band are then global sums.  ``energy_sum``: the
+    (global) weighted sum sum_w |u|^2 of ``u_hat`` when the caller already has it
+    -- e.g. ``AdvanceOutcome.diag_sums[4]`` of the step that produced u_hat, which
+    the fused step reduction computes with the same arithmetic as the full pass
+    this function would otherwise make -- so only the band is read."""
     from .diagnostics import reduce_sums
 
     u = u_hat
@@ -168,16 +173,17 @@ def apply_forcing(u_hat, grid: Grid, target_energy, k_f, plan=None, allreduce=No
     lib = _native.load()
     ncomp = u.shape[0]
     pts2 = 2.0 * float(grid.points) ** 2
-    q = reduce_sums(grid, u, flags=2, ncomp=ncomp, plan=plan)
+    q = reduce_sums(grid, u, flags=2, ncomp=ncomp, plan=plan) if energy_sum is None else None
     eb = torch.zeros(1, dtype=torch.float64, device=u.device)
     if nb > 0:
         _native.check(lib.srk_band_energy(ph, _native.ptr(u), ncomp, _native.ptr(idx), _native.ptr(w), nb,
                                           _native.ptr(eb), _native.stream_ptr()))
     if allreduce is not None:
-        s = allreduce([q[4].item(), eb.item()])
-        e_total, e_band = s[0] / pts2, s[1] / pts2
+        s = allreduce([q[4].item() if q is not None else 0.0, eb.item()])
+        e_total = (s[0] if q is not None else float(energy_sum)) / pts2
+        e_band = s[1] / pts2
     else:
-        e_total = q[4].item() / pts2
+        e_total = (q[4].item() if q is not None else float(energy_sum)) / pts2
         e_band = eb.item() / pts2
     e_rest = e_total - e_band
     if e_band <= 0.0:

@@ -222,12 +222,14 @@ class _Driver:
         self.records.append(DiagnosticsRecord(t=self.t, h=h, e_kin=e, eps=eps, rhs_evals=self.evals,
                                               rejections=self.rejections, enstrophy=z))
 
-    def after_accept(self, last_stage, fsal_ok):
-        """simulation.py:165-182. Returns True when f_now is the FSAL stage."""
+    def after_accept(self, last_stage, fsal_ok, energy_sum=None):
+        """simulation.py:165-182. Returns True when f_now is the FSAL stage.
+        energy_sum: sum_w |u|^2 of the new state from the step reduction, if known."""
         cfg = self.config
         forced = False
         if cfg.forcing:
-            apply_forcing(self.y[: self.grid.dims], self.grid, cfg.problem.energy, cfg.k_f)
+            apply_forcing(self.y[: self.grid.dims], self.grid, cfg.problem.energy, cfg.k_f,
+                          energy_sum=energy_sum)
             forced = True
         self.steps += 1
         if fsal_ok and not forced and last_stage is not None:
@@ -348,7 +350,8 @@ def _run_adaptive(drv, max_steps=None):
         drv.h_ctrl = ctrl.h
         drv.prev_rejected = ctrl.prev_rejected
         drv.errs.append(out.errs)
-        fsal_used = drv.after_accept(out.last_stage, fsal_ok=pair.fsal)
+        fsal_used = drv.after_accept(out.last_stage, fsal_ok=pair.fsal,
+                                     energy_sum=out.diag_sums[4] if out.diag_sums is not None else None)
         drv.record(out.h_used, sums=out.diag_sums if fsal_used else None)
         drv.maybe_checkpoint()
         n += 1

@@ -89,3 +89,19 @@ def test_rhs_combine_rejects_aliasing():
         _native.check(lib.srk_rhs_combine(rhs.plan.bind(), _native.ptr(y), _native.ptr(f), 1e-3, 1.0, 1.0,
                                           _native.ptr(y), 0, _native.ptr_array([]), _native.dbl_array([]), 0.5,
                                           _native.ptr(y), _native.stream_ptr()))
+
+
+def test_forcing_with_step_energy_sum_is_bitwise_the_full_pass():
+    """apply_forcing(energy_sum=AdvanceOutcome.diag_sums[4]) skips its own energy pass;
+    the fused step reduction computes the same sum with the same arithmetic."""
+    g = srk.Grid((64, 64, 64))
+    y = srk.hit_init(g, srk.ProblemSpec("hit", a=4.0, energy=0.5, seed=42)).fields
+    rhs = srk.FlowRHS(g, srk.PhysParams(2000.0))
+    st = srk.ControllerState(h=1e-3)
+    out = srk.adaptive_advance(y, 0.0, srk.make_bs5(), st, srk.ControllerConfig(), rhs, first_stage=rhs(0.0, y),
+                               grid=g)
+    a, b = out.y_new.clone(), out.y_new.clone()
+    ga = srk.apply_forcing(a, g, 0.5, 2.0)
+    gb = srk.apply_forcing(b, g, 0.5, 2.0, energy_sum=out.diag_sums[4])
+    assert ga == gb
+    assert torch.equal(a, b)
