@@ -1038,6 +1038,8 @@ __global__ void __launch_bounds__(M / 8, SRK_ZP1_MINB) k_zpass_ns3p(const ZArgs 
   static_assert(L::C == 3, "three tile columns");
   const int pen = blockIdx.x;
   const int tid = threadIdx.x;
+  SRK_TS_INIT(a.dbg, 6)
+  SRK_TS(0)
   // ---- staging: 6 real-signal rows of K modes via 1D TMA bulk copies ----
   cplx* stg = sm;
   __shared__ __align__(8) unsigned long long mbar;
@@ -1060,6 +1062,7 @@ __global__ void __launch_bounds__(M / 8, SRK_ZP1_MINB) k_zpass_ns3p(const ZArgs 
   mbar_wait(&mbar, 0);
   cp_async_wait_all();
   __syncthreads();
+  SRK_TS(1)
   auto hs = [&](int g, int k) -> cplx {
     const bool head = k < K;
     const bool tail = k >= M - (K - 1);
@@ -1078,6 +1081,7 @@ __global__ void __launch_bounds__(M / 8, SRK_ZP1_MINB) k_zpass_ns3p(const ZArgs 
     EngI::template run_ws<+1, true, true>(a.gp, sm, twp, S, ld, st);
   }
   __syncthreads();
+  SRK_TS(2)
   // ---- fused: last inverse radix-4 | u x w | first forward radix-4; rows j, j + NT ----
   {
     cplx v[2][S][4];
@@ -1132,6 +1136,7 @@ __global__ void __launch_bounds__(M / 8, SRK_ZP1_MINB) k_zpass_ns3p(const ZArgs 
     }
   }
   __syncthreads();
+  SRK_TS(3)
   // ---- forward suffix (Ls = 4 ...) on the 2 packed columns ----
   {
     auto st = [&](int n, int c, cplx v) {
@@ -1140,6 +1145,7 @@ __global__ void __launch_bounds__(M / 8, SRK_ZP1_MINB) k_zpass_ns3p(const ZArgs 
     LoopStageZ<M, L, -1, 2, NT, 4, FR...>::go(sm, twp, st);
   }
   __syncthreads();
+  SRK_TS(4)
   // ---- extraction: P0, P1 from column 0 (two-for-one), P2 = column 1; kz = n/2 zeroed ----
   for (int k = tid; k < K; k += NT) {
     const bool live = k != K - 1;
@@ -1150,5 +1156,9 @@ __global__ void __launch_bounds__(M / 8, SRK_ZP1_MINB) k_zpass_ns3p(const ZArgs 
     o[0] = cmk(0.5 * (Zk.x + Zm.x), 0.5 * (Zk.y - Zm.y));
     o[a.out_sig_stride] = cmk(0.5 * (Zk.y + Zm.y), -0.5 * (Zk.x - Zm.x));
     o[2 * a.out_sig_stride] = (k == 0) ? cmk(P2.x, 0.0) : P2;
+  }
+  if (a.dbg) {
+    __syncthreads();
+    SRK_TS(5)
   }
 }
