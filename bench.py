@@ -319,34 +319,49 @@ def run_native(args, rank, world, local_rank):
     except Exception:
         pass
 
-    # ---- e2e: through the public API with pinned host buffers ----
-    # The state crosses PCIe every step: y is copied host->device, the cached
-    # tendency f = rhs(t, y) (the refresh the device-resident loop does at the
-    # end of the previous step, same count) and the diagnostics record are
-    # computed from it, one adaptive step + forcing runs, and y_new is copied
-    # back to the host buffer the next step reads.
+    # ---- e2e: through the public API with the state resident on the host ----
+    # The state crosses PCIe every step (hostio.HostMirror, pinned): y is copied
+    # host->device, the cached tendency f = rhs(t, y) (the refresh the
+    # device-resident loop does at the end of the previous step, same count) and
+    # the diagnostics record are computed from it, one adaptive step + forcing
+    # runs, and y_new goes back to the host copy the next step reads -- issued as
+    # soon as y_new exists, and the next step's host->device chunks follow the
+    # device->host ones on the other PCIe direction, both under the FSAL stage and
+    # the error reduction (a rejected attempt redoes both); after the accept and
+    # the forcing rescale only the band's x-planes go down and up again.
     e2e = None
     if not args.no_e2e:
         s2 = new_state()
-        y_h = torch.empty(s2["y"].shape, dtype=s2["y"].dtype, pin_memory=True)
-        y_h.copy_(s2["y"])
+        mirror = srk.HostMirror(s2["y"])
+        mirror.load_host(s2["y"].cpu())
+        fplanes = srk.forcing_planes(g, k_f)
         torch.cuda.synchronize()
-        nbytes = y_h.numel() * y_h.element_size()
         barrier()
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev2 = 0
-        yd = torch.empty_like(s2["y"])
         t2_ = s2["t"]
+        n_e2e = max(2, args.steps // 2)
+        b_in0, b_out0 = mirror.h2d_bytes, mirror.d2h_bytes
+        spec = {}
+
+        def on_y_new(v):  # every attempt: y_new -> host, and the host copy -> the next input
+            mirror.push(v)
+            spec["next"] = mirror.pull(wait=False)
+
         a0.record(st)
-        for _ in range(max(2, args.steps // 2)):
-            yd.copy_(y_h, non_blocking=True)
+        yd = mirror.pull()
+        for _ in range(n_e2e):
             fd = rhs(t2_, yd)
             q = srk.diagnostics.reduce_sums(g, yd, fl=fd, flags=2, ncomp=3).tolist()
-            out = srk.adaptive_advance(yd, t2_, pair, s2["ctrl"], cfg, rhs, first_stage=fd, grid=g)
+            out = srk.adaptive_advance(yd, t2_, pair, s2["ctrl"], cfg, rhs, first_stage=fd, grid=g,
+                                       on_y_new=on_y_new)
             srk.apply_forcing(out.y_new, g, energy, k_f, energy_sum=out.diag_sums[4])
+            mirror.push(out.y_new, planes=fplanes)
             ev2 += out.rhs_evals + 1
             t2_ = out.t_new
-            y_h.copy_(out.y_new, non_blocking=True)
+            del yd, fd, out
+            yd = mirror.pull(into=spec.pop("next"), planes=fplanes)  # the re-sent planes, then wait
+        mirror.wait()
         a1.record(st)
         torch.cuda.synchronize()
         t2 = torch.tensor([a0.elapsed_time(a1) / 1e3], dtype=torch.float64, device=dev)
@@ -354,10 +369,13 @@ def run_native(args, rank, world, local_rank):
         if world > 1:
             dist.all_reduce(t2, op=dist.ReduceOp.MAX)
             dist.all_reduce(e2t, op=dist.ReduceOp.SUM)
-        e2e = {"value": e2t.item() / t2.item(), "unit": "stages/s", "h2d_bytes_per_step": nbytes,
-               "d2h_bytes_per_step": nbytes + 9 * 8,
-               "path": "per step: y host->device (pinned), cached tendency rhs(t, y) + diagnostics record, "
-                       "adaptive_advance (BS5) + forcing through the Python API, y_new device->host; "
+        e2e = {"value": e2t.item() / t2.item(), "unit": "stages/s",
+               "h2d_bytes_per_step": (mirror.h2d_bytes - b_in0) // n_e2e,
+               "d2h_bytes_per_step": (mirror.d2h_bytes - b_out0) // n_e2e + 9 * 8,
+               "path": "per step: y host->device (pinned HostMirror), cached tendency rhs(t, y) + diagnostics "
+                       "record, adaptive_advance (BS5) + forcing through the Python API, y_new device->host "
+                       "(every attempt's y_new, issued before its FSAL stage, the next step's host->device behind it; "
+                       "forcing band planes re-sent both ways); "
                        "same RHS count as the device-resident step"}
 
     if rank != 0:

@@ -25,6 +25,7 @@ from .simulation import (ADAPTIVE_CAPABLE, INTEGRATORS, ConfigError, RunConfig, 
 from .checkpoint import (CheckpointData, CheckpointError, read_checkpoint, read_diagnostics_csv,
                          write_checkpoint, write_diagnostics_csv)
 from .workprec import WorkPrecisionPoint, cell_config, work_precision, write_work_precision_csv
+from .hostio import HostMirror, forcing_planes, plane_runs
 from . import _native
 
 __version__ = "0.1.0"

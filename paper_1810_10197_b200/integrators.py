@@ -175,7 +175,7 @@ def _as_dev_fn(f):
 _FUSED_MAX_TERMS = 6
 
 
-def run_stages(f, y, t, h, pair, first_stage=None):
+def run_stages(f, y, t, h, pair, first_stage=None, on_y_new=None):
     """Stage loop of integrators.py:322-339 on the device.
 
     Returns (stages, y_new, evals).  For FSAL pairs y_new is the last stage's
@@ -184,6 +184,10 @@ def run_stages(f, y, t, h, pair, first_stage=None):
     RHS call also forms the accumulation that consumes it -- the next stage
     input (row i+1 of A) or, for non-FSAL pairs, y_new -- bitwise the same sums,
     without reading the new stage back (srk_rhs_combine).
+
+    ``on_y_new(y_new)`` is called once y_new is queued: for FSAL pairs before the
+    last stage's RHS (whose input it is), so a consumer such as
+    ``HostMirror.push`` overlaps that evaluation.
     """
     A, b, c, s = pair.A, pair.b, pair.c, pair.s
     fused = getattr(f, "eval_combine", None)
@@ -203,6 +207,8 @@ def run_stages(f, y, t, h, pair, first_stage=None):
             xi = combine(y, [(h * A[i, j], stages[j]) for j in range(i) if A[i, j] != 0.0])
         if i > 0:
             yi = xi
+            if on_y_new is not None and pair.fsal and i == s - 1:
+                on_y_new(xi)
         row = A[i + 1] if i + 1 < s else (None if pair.fsal else b)
         if fused is not None and row is not None and row[i] != 0.0:
             terms = [(h * row[j], stages[j]) for j in range(i) if row[j] != 0.0]
@@ -218,6 +224,8 @@ def run_stages(f, y, t, h, pair, first_stage=None):
         y_new = pending
     else:
         y_new = combine(y, [(h * b[i], stages[i]) for i in range(s) if b[i] != 0.0])
+    if on_y_new is not None and not (pair.fsal and yi is not None):
+        on_y_new(y_new)
     return stages, y_new, evals
 
 

@@ -263,3 +263,64 @@ def test_invariants_over_200_adaptive_bs5_steps():
         fd = (srk.kinetic_energy(y + d * f_now, g) - srk.kinetic_energy(y - d * f_now, g)) / (2 * d)
         worst_probe = max(worst_probe, abs(fd + eps) / abs(eps))
     assert worst_div <= 1e-11 and worst_neu <= 1e-8 and worst_probe <= 1e-6
+
+
+# ---------------------------------------------------------------- host-resident state (hostio)
+@pytest.mark.parametrize("chunk_bytes", [1 << 30, 48 * 1024])
+def test_host_mirror_loop_is_bitwise_the_device_loop(chunk_bytes):
+    """Forced-HIT BS5 steps with the state kept on the host (HostMirror: y_new pushed
+    before its FSAL stage, forcing planes re-sent, chunked pull) == the device-resident
+    loop, bit for bit; h0 = 0.5 forces rejected attempts (each pushes again)."""
+    g = srk.Grid((32, 32, 32))
+    rhs = srk.FlowRHS(g, srk.PhysParams(2000.0))
+    pair = srk.make_bs5()
+    cfg = srk.ControllerConfig(tol_abs=1e-6, tol_rel=1e-6)
+    y0 = _hit(g, seed=42, energy=0.5)
+    planes = srk.forcing_planes(g, 2.0)
+
+    def run(host_state):
+        st = srk.ControllerState(h=0.5)
+        t, y, pushes, rej = 0.0, y0.clone(), [], 0
+        m, spec = None, {}
+        if host_state:
+            m = srk.HostMirror(y, chunk_bytes=chunk_bytes)
+            m.load_host(y.cpu())
+            y = m.pull()
+
+        def hook(v):  # every attempt: push y_new, pull it back as the next input (speculative)
+            pushes.append(1)
+            m.push(v)
+            spec["next"] = m.pull(wait=False)
+
+        hist = []
+        for _ in range(4):
+            f = rhs(t, y)
+            out = srk.adaptive_advance(y, t, pair, st, cfg, rhs, first_stage=f, grid=g,
+                                       on_y_new=hook if host_state else None)
+            srk.apply_forcing(out.y_new, g, 0.5, 2.0, energy_sum=out.diag_sums[4])
+            rej += out.rejections
+            t, y = out.t_new, out.y_new
+            if host_state:
+                m.push(out.y_new, planes=planes)
+                y = m.pull(into=spec.pop("next"), planes=planes)
+            hist.append((out.h_used, out.h_next))
+        if host_state:
+            m.synchronize()
+            assert torch.equal(y.cpu(), m.host)  # the pulled input is the host copy
+            return m.host.clone(), hist, len(pushes), rej
+        return y.cpu(), hist, None, rej
+
+    yh, hh, pushes, rej = run(True)
+    yd, hd, _, rej_d = run(False)
+    assert rej >= 1 and rej == rej_d
+    assert pushes == 4 + rej  # one push per attempt
+    assert hh == hd
+    assert torch.equal(yh, yd)
+
+
+def test_host_mirror_rejects_mismatched_tensors():
+    m = srk.HostMirror(torch.zeros((2, 4, 4, 3), dtype=torch.complex128, device="cuda"))
+    with pytest.raises(ValueError):
+        m.push(torch.zeros((2, 4, 4, 2), dtype=torch.complex128, device="cuda"))
+    with pytest.raises(TypeError):
+        srk.HostMirror(torch.zeros(3))

@@ -114,3 +114,19 @@ def test_compute_without_cuda_fails_loudly():
         pytest.skip("has a GPU")
     with pytest.raises(RuntimeError, match="CUDA"):
         srk.FlowRHS(srk.Grid((8, 8, 8)), srk.PhysParams(10.0))
+
+
+def test_plane_runs_and_forcing_planes():
+    from paper_1810_10197_b200.hostio import forcing_planes, plane_runs
+
+    assert plane_runs([]) == []
+    assert plane_runs([5, 0, 1, 2, 7, 6, 2]) == [(0, 3), (5, 8)]
+    g = srk.Grid((16, 16, 16))
+    # k_f = 2 on L = 2pi: |k_x| <= 2 -> x-planes 0, 1, 2, 14, 15
+    assert forcing_planes(g, 2.0) == [(0, 3), (14, 16)]
+    og = O.OGrid((16, 12, 8), (2 * np.pi, 3.0, 4.0))
+    g2 = srk.Grid((16, 12, 8), (2 * np.pi, 3.0, 4.0))
+    band = (og.k2 > 0) & (og.k2 <= 2.5 ** 2 * (1 + 1e-12))
+    want = sorted(set(np.nonzero(band)[0].tolist()))
+    got = [i for a, b in forcing_planes(g2, 2.5) for i in range(a, b)]
+    assert got == want
