@@ -234,7 +234,7 @@ def run_native(args, rank, world, local_rank):
         y = out.y_new
         srk.apply_forcing(y, g, energy, k_f, energy_sum=out.diag_sums[4])
         f = rhs(out.t_new, y)
-        q = srk.diagnostics.reduce_sums(g, y, fl=f, flags=2, ncomp=3).tolist()
+        q = srk.diagnostics.reduce_sums(g, y, fl=f, flags=2, ncomp=3, host=True).tolist()
         s.update(y=y, t=out.t_new, f=f)
         return out.rhs_evals + 1, diag_from_sums(q, g)
 
@@ -352,7 +352,7 @@ def run_native(args, rank, world, local_rank):
         yd = mirror.pull()
         for _ in range(n_e2e):
             fd = rhs(t2_, yd)
-            q = srk.diagnostics.reduce_sums(g, yd, fl=fd, flags=2, ncomp=3).tolist()
+            q = srk.diagnostics.reduce_sums(g, yd, fl=fd, flags=2, ncomp=3, host=True).tolist()
             out = srk.adaptive_advance(yd, t2_, pair, s2["ctrl"], cfg, rhs, first_stage=fd, grid=g,
                                        on_y_new=on_y_new)
             srk.apply_forcing(out.y_new, g, energy, k_f, energy_sum=out.diag_sums[4])

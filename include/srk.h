@@ -119,7 +119,8 @@ int srk_combine(int64_t n, const void* y, int nterms, const void* const* F, cons
  *              out[8] = sum_k w_k |k|^2 sum_{j<d} |y1_kj|^2  (enstrophy)
  *   always:    out[6] = number of non-finite entries in Delta and y1
  *              (integrators.py:348-351), out[7] = count(sc <= 0).
- * out_dev: DEVICE array of 9 doubles.  Needs no bound workspace. */
+ * out_dev: 9 doubles in device memory or in pinned (UVA-mapped) host memory,
+ *          stored by the last kernel.  Needs no bound workspace. */
 int srk_step_reduce(srk_plan* plan, const void* y0, const void* y1, int nterms, const void* const* F,
                     const double* coef, const void* fl, int ncomp, double tol_abs, double tol_rel, int flags,
                     double* out_dev, void* stream);

@@ -122,6 +122,24 @@ def stream_ptr(stream=None):
     return ctypes.c_void_p(s.cuda_stream)
 
 
+def host_result(n):
+    """Pinned host float64[n] a kernel can store into directly (UVA-mapped), for
+    small results read by the host: no cudaMemcpy, so nothing queues behind bulk
+    copies on the copy engines."""
+    import torch
+
+    return torch.empty(n, dtype=torch.float64, pin_memory=True)
+
+
+def wait_stream_point(stream=None):
+    """Block the host until the work queued so far on ``stream`` (default: current) is done."""
+    import torch
+
+    ev = torch.cuda.Event()
+    ev.record(stream if stream is not None else torch.cuda.current_stream())
+    ev.synchronize()
+
+
 def ptr_array(tensors):
     arr = (ctypes.c_void_p * max(1, len(tensors)))()
     for i, t in enumerate(tensors):

@@ -33,15 +33,18 @@ class DiagnosticsRecord:
 
 
 def reduce_sums(grid: Grid, y1, fl=None, y0=None, terms=(), tol_abs=0.0, tol_rel=0.0, flags=2, ncomp=None,
-                stream=None, plan=None):
+                stream=None, plan=None, host=False):
     """Launch srk_step_reduce; returns the 9 device sums as a CUDA float64 tensor (no sync).
 
     ``plan``: a slab plan handle (paper_1810_10197_b200.slab) when y1 is a y-slab;
-    the sums are then this rank's partials."""
+    the sums are then this rank's partials.  ``host=True``: the finishing kernel
+    stores the sums straight into pinned host memory (no copy-engine transfer that
+    could queue behind a large HostMirror copy); the call then waits for the
+    stream and returns a CPU tensor."""
     lib = _native.load()
     h = get_plan(grid).h if plan is None else plan
     ncomp = y1.shape[0] if ncomp is None else ncomp
-    out = torch.empty(9, dtype=torch.float64, device=y1.device)
+    out = _native.host_result(9) if host else torch.empty(9, dtype=torch.float64, device=y1.device)
     Fs = [t for _, t in terms]
     cs = [c for c, _ in terms]
     _native.check(lib.srk_step_reduce(
@@ -49,6 +52,8 @@ def reduce_sums(grid: Grid, y1, fl=None, y0=None, terms=(), tol_abs=0.0, tol_rel
         _native.ptr(fl if fl is not None else y1), ncomp, float(tol_abs), float(tol_rel), int(flags),
         _native.ptr(out), _native.stream_ptr(stream)), "srk_step_reduce")
     _native.count(2)
+    if host:
+        _native.wait_stream_point(stream)
     return out
 
 
@@ -61,7 +66,7 @@ def diag_from_sums(q, grid: Grid):
 def kinetic_energy(u_hat, grid: Grid):
     """E = sum_k w_k sum_j |u_kj|^2 / (2 points^2) (diagnostics.py:48-50)."""
     u, _ = to_device(u_hat, torch.complex128)
-    q = reduce_sums(grid, u, flags=2, ncomp=u.shape[0]).tolist()
+    q = reduce_sums(grid, u, flags=2, ncomp=u.shape[0], host=True).tolist()
     return q[4] / (2.0 * float(grid.points) ** 2)
 
 
@@ -72,14 +77,14 @@ def dissipation_rate(u_hat, f_hat, grid: Grid):
     if tuple(u.shape[1:]) != grid.kshape or tuple(f.shape) != tuple(u.shape):
         raise ValueError(f"shape mismatch: fields {tuple(u.shape)}, tendency {tuple(f.shape)}, "
                          f"grid modes {grid.kshape}")
-    q = reduce_sums(grid, u, fl=f, flags=2, ncomp=min(u.shape[0], grid.dims)).tolist()
+    q = reduce_sums(grid, u, fl=f, flags=2, ncomp=min(u.shape[0], grid.dims), host=True).tolist()
     return -q[5] / float(grid.points) ** 2
 
 
 def enstrophy(u_hat, grid: Grid):
     """Z = sum_k w_k |k|^2 sum_{j<d} |u_kj|^2 / (2 points^2)."""
     u, _ = to_device(u_hat, torch.complex128)
-    q = reduce_sums(grid, u, flags=2, ncomp=min(u.shape[0], grid.dims)).tolist()
+    q = reduce_sums(grid, u, flags=2, ncomp=min(u.shape[0], grid.dims), host=True).tolist()
     return q[8] / (2.0 * float(grid.points) ** 2)
 
 

@@ -251,7 +251,7 @@ def rk_step(f, y, t, h, pair, first_stage=None):
     kshape = tuple(yd.shape[1:])
     grid = Grid(kshape[:-1] + (2 * (kshape[-1] - 1),))
     q = reduce_sums(grid, y_new, y0=yd, terms=terms, tol_abs=1.0, tol_rel=0.0,
-                    flags=1 if terms else 0, ncomp=yd.shape[0]).tolist()
+                    flags=1 if terms else 0, ncomp=yd.shape[0], host=True).tolist()
     if q[6] > 0:
         raise NonFiniteStateError(f"non-finite state at t={t}")
     return StepOutcome(y_new=from_device(y_new, was_np), error_vector=None if err is None else from_device(err, was_np),

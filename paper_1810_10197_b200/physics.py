@@ -173,11 +173,13 @@ def apply_forcing(u_hat, grid: Grid, target_energy, k_f, plan=None, allreduce=No
     lib = _native.load()
     ncomp = u.shape[0]
     pts2 = 2.0 * float(grid.points) ** 2
-    q = reduce_sums(grid, u, flags=2, ncomp=ncomp, plan=plan) if energy_sum is None else None
-    eb = torch.zeros(1, dtype=torch.float64, device=u.device)
+    q = reduce_sums(grid, u, flags=2, ncomp=ncomp, plan=plan, host=True) if energy_sum is None else None
+    eb = _native.host_result(1)  # written by the kernel (pinned, mapped)
+    eb.zero_()
     if nb > 0:
         _native.check(lib.srk_band_energy(ph, _native.ptr(u), ncomp, _native.ptr(idx), _native.ptr(w), nb,
                                           _native.ptr(eb), _native.stream_ptr()))
+    _native.wait_stream_point()
     if allreduce is not None:
         s = allreduce([q[4].item() if q is not None else 0.0, eb.item()])
         e_total = (s[0] if q is not None else float(energy_sum)) / pts2

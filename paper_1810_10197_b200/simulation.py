@@ -215,7 +215,7 @@ class _Driver:
     def record(self, h, sums=None):
         d = self.grid.dims
         if sums is None:
-            sums = reduce_sums(self.grid, self.y, fl=self.f_now, flags=2, ncomp=min(d, self.y.shape[0])).tolist()
+            sums = reduce_sums(self.grid, self.y, fl=self.f_now, flags=2, ncomp=min(d, self.y.shape[0]), host=True).tolist()
             if sums[6] > 0:
                 raise NonFiniteStateError(f"non-finite state at t={self.t}")
         e, eps, z = diag_from_sums(sums, self.grid)
