@@ -498,10 +498,14 @@ SRK_DEV void zphys(const double* r, double* o) {
   }
 }
 
-// Eng runs the inverse transforms (S complex columns); EngF the forward ones
-// (So columns) -- a different plan when So < S so all threads stay busy.
-template <class Eng, class L, int OP, class EngF = Eng>
-__global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 192 ? 2 : 1)) k_zpass(const ZArgs a, int S_rt, int So_rt) {
+// Eng runs the inverse transforms (PPC*S/2 complex columns); EngF the forward
+// ones (PPC*So/2 columns) -- a different plan when So < S so all threads stay
+// busy.  PPC = pencils per CTA: 2 (real signals paired across the two pencils)
+// or 1 (S and So even: paired within the pencil; half the tile, twice the CTAs
+// per SM -- the 2D Boussinesq pass at 1024^2, where one CTA per SM left each
+// SM waiting on one tile at a time).
+template <class Eng, class L, int OP, class EngF = Eng, int PPC = 2>
+__global__ void __launch_bounds__(Eng::NT, (PPC == 1 && Eng::NT <= 128 ? 3 : (Eng::NT <= 192 ? 2 : 1))) k_zpass(const ZArgs a, int S_rt, int So_rt) {
   extern __shared__ __align__(16) cplx smraw[];
   cplx* const sm = smraw + Eng::TWN;  // [twiddle table][tile]
   const cplx* const twp = Eng::kFast ? smraw : a.tw;
@@ -509,7 +513,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 192 ? 2 : 1)) k_zpass(con
     tw_fill<Eng::M>(smraw, a.tw);  // first use is after a CTA barrier
     cp_async_wait_all();
   }
-  const int p0 = 2 * blockIdx.x;
+  const int p0 = PPC * blockIdx.x;
   const int S = (OP >= ZOP_NS3) ? ZSig<OP>::S : S_rt;
   const int So = (OP >= ZOP_NS3) ? ZSig<OP>::So : So_rt;
   // physics ops always run on the 3/2-padded axis: M = 3n/2, K = n/2 + 1 = M/3 + 1,
@@ -534,21 +538,21 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 192 ? 2 : 1)) k_zpass(con
       __syncthreads();
       if (threadIdx.x == 0) {
         unsigned bytes = 0;
-        for (int g = 0; g < 2 * S; ++g) bytes += (p0 + g / S < a.P) ? (unsigned)(K * 16) : 0u;
+        for (int g = 0; g < PPC * S; ++g) bytes += (p0 + g / S < a.P) ? (unsigned)(K * 16) : 0u;
         mbar_expect_tx(&mbar, bytes);
-        for (int g = 0; g < 2 * S; ++g) {
+        for (int g = 0; g < PPC * S; ++g) {
           const int pp = g / S, s = g - pp * S, pen = p0 + pp;
           if (pen < a.P)
             bulk_g2s(stg + g * K, a.in + s * a.in_sig_stride + (long long)pen * K, (unsigned)(K * 16), &mbar);
         }
       }
       // rows of a missing second pencil (odd P) are zero
-      if (p0 + 1 >= a.P)
+      if (PPC == 2 && p0 + 1 >= a.P)
         for (int i = threadIdx.x; i < S * K; i += blockDim.x) stg[S * K + i] = cmk(0.0, 0.0);
       mbar_wait(&mbar, 0);
       __syncthreads();
     } else {
-      for (int g = 0; g < 2 * S; ++g) {
+      for (int g = 0; g < PPC * S; ++g) {
         const int pp = g / S, s = g - pp * S, pen = p0 + pp;
         const cplx* __restrict__ src = a.in + s * a.in_sig_stride + (long long)pen * K;
         for (int k = threadIdx.x; k < K; k += blockDim.x) stg[g * K + k] = (pen < a.P) ? src[k] : cmk(0.0, 0.0);
@@ -565,7 +569,8 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 192 ? 2 : 1)) k_zpass(con
       if (k == 0 || 2 * k == M) X.y = 0.0;  // irfft ignores Im of DC / Nyquist
       return (head || tail) ? X : cmk(0.0, 0.0);
     };
-    // ---- inverse: S complex columns, column c carries real signals 2c, 2c+1 ----
+    // ---- inverse: PPC*S/2 complex columns, column c carries real signals 2c, 2c+1 ----
+    const int NCI = PPC * S / 2 + (PPC * S) % 2;
     auto ld = [&](int k, int c) -> cplx {
       cplx A = hs(2 * c, k), B = hs(2 * c + 1, k);
       return cmk(A.x - B.y, A.y + B.x);
@@ -577,36 +582,37 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 192 ? 2 : 1)) k_zpass(con
           const int pp = g0 / S, s = g0 - pp * S, pen = p0 + pp;
           if (pen < a.P) a.out_real[s * a.out_sig_stride + (long long)pen * M + n] = v.x;
         }
-        if (g1 < 2 * S) {
+        if (g1 < PPC * S) {
           const int pp = g1 / S, s = g1 - pp * S, pen = p0 + pp;
           if (pen < a.P) a.out_real[s * a.out_sig_stride + (long long)pen * M + n] = v.y;
         }
       };
-      Eng::template run<+1, true, false>(a.gp, sm, twp, S, ld, st);
+      Eng::template run<+1, true, false>(a.gp, sm, twp, NCI, ld, st);
       return;
     } else {
       auto st = [&](int n, int c, cplx v) { sm[L::idx(n, c)] = v; };
-      Eng::template run<+1, true, true>(a.gp, sm, twp, S, ld, st);
+      Eng::template run<+1, true, true>(a.gp, sm, twp, NCI, ld, st);
       __syncthreads();
       // ---- physical space: per row n, both pencils ----
       for (int n = threadIdx.x; n < M; n += blockDim.x) {
         double r[2 * 7];
 #pragma unroll
-        for (int c = 0; c < ZSig<OP>::S; ++c) {
+        for (int c = 0; c < PPC * ZSig<OP>::S / 2; ++c) {
           cplx z = sm[L::idx(n, c)];
           r[2 * c] = z.x;
           r[2 * c + 1] = z.y;
         }
         double o[2 * 6];
         zphys<OP>(r, o);
-        zphys<OP>(r + ZSig<OP>::S, o + ZSig<OP>::So);
+        if constexpr (PPC == 2) zphys<OP>(r + ZSig<OP>::S, o + ZSig<OP>::So);
 #pragma unroll
-        for (int c = 0; c < ZSig<OP>::So; ++c) sm[L::idx(n, c)] = cmk(o[2 * c], o[2 * c + 1]);
+        for (int c = 0; c < PPC * ZSig<OP>::So / 2; ++c) sm[L::idx(n, c)] = cmk(o[2 * c], o[2 * c + 1]);
       }
       __syncthreads();
     }
   }
-  // ---- forward: So complex columns ----
+  // ---- forward: PPC*So/2 complex columns ----
+  const int NCO = PPC * So / 2 + (PPC * So) % 2;
   if constexpr (OP == ZOP_R2C) {
     auto ld = [&](int n, int c) -> cplx {
       double v[2];
@@ -614,24 +620,24 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 192 ? 2 : 1)) k_zpass(con
       for (int h = 0; h < 2; ++h) {
         const int g = 2 * c + h;
         const int pp = g / So, s = g - pp * So, pen = p0 + pp;
-        v[h] = (g < 2 * So && pen < a.P) ? a.in_real[s * a.in_sig_stride + (long long)pen * M + n] : 0.0;
+        v[h] = (g < PPC * So && pen < a.P) ? a.in_real[s * a.in_sig_stride + (long long)pen * M + n] : 0.0;
       }
       return cmk(v[0], v[1]);
     };
     auto st = [&](int n, int c, cplx v) { sm[L::idx(n, c)] = v; };
-    Eng::template run<-1, false, true>(a.gp, sm, twp, So, ld, st);
+    Eng::template run<-1, false, true>(a.gp, sm, twp, NCO, ld, st);
   } else {
     auto ld = [&](int n, int c) -> cplx { return sm[L::idx(n, c)]; };
     // only rows [0, K-1) and (M-K+1, M) feed the kept modes (kz = n/2 is zeroed)
     auto st = [&](int n, int c, cplx v) {
       if (n < K - 1 || n > M - K + 1) sm[L::idx(n, c)] = v;
     };
-    EngF::template run<-1, true, true>(a.gp, sm, twp, So, ld, st);
+    EngF::template run<-1, true, true>(a.gp, sm, twp, NCO, ld, st);
   }
   __syncthreads();
   // ---- extraction: two real spectra from each complex column, keep K modes ----
   const bool zn = a.zero_nyq != 0;
-  for (int i = threadIdx.x; i < So * K; i += blockDim.x) {
+  for (int i = threadIdx.x; i < NCO * K; i += blockDim.x) {
     const int c = i / K, k = i - (i / K) * K;
     const bool live = !(zn && k == K - 1);
     const cplx Zk = live ? sm[L::idx(k, c)] : cmk(0.0, 0.0);
@@ -645,7 +651,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 192 ? 2 : 1)) k_zpass(con
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int g = 2 * c + h;
-      if (g >= 2 * So) break;
+      if (g >= PPC * So) break;
       const int pp = g / So, s = g - pp * So, pen = p0 + pp;
       if (pen < a.P) a.out[s * a.out_sig_stride + (long long)pen * K + k] = h ? B : A;
     }

@@ -27,7 +27,8 @@ enum KernelKind {
   KK_INV_CURLY_SLAB = 18,  // 3D K2 from the all-to-all #1 receive layout
   KK_FWD_PROJ = 19,        // K5 + K6 fused over a cluster of So CTAs (DSMEM)
   KK_FWD_PROJ_SLAB = 20,   // same, reading the all-to-all #2 receive layout
-  KK_COUNT = 21
+  KK_FWD_P2D = 21,         // 2D x-forward + truncation (K5) when a narrower tile is registered
+  KK_COUNT = 22
 };
 
 struct KEntry {

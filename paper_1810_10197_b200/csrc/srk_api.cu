@@ -254,7 +254,8 @@ void setup_tma(int kind, int cols, PassArgs& a, CUtensorMap* tm) {
   a.tma = 0;
   const bool inv = kind == KK_INV || kind == KK_INV_P || kind == KK_INV_KX || kind == KK_INV_KX_SLAB ||
                    kind == KK_INV_CURLY;
-  const bool fwd = kind == KK_FWD || kind == KK_FWD_P || kind == KK_FWD_P_SLABO || kind == KK_FWD_P_SLABI;
+  const bool fwd = kind == KK_FWD || kind == KK_FWD_P || kind == KK_FWD_P_SLABO || kind == KK_FWD_P_SLABI ||
+                   kind == KK_FWD_P2D;
   const bool slab_in = kind == KK_INV_CURLY_SLAB || kind == KK_INV_P_SLAB;  // blocked input rows
   if (!(inv || fwd || slab_in) || !g_fast->count(a.M)) return;
   static const int skip_mask = getenv("SRK_TMA_SKIP") ? atoi(getenv("SRK_TMA_SKIP")) : 0;  // experiments
@@ -812,7 +813,13 @@ int rhs_impl(srk_plan* p, const void* y_, void* f_, double nu, double ri, double
     if ((rc = launch_fwd_proj(p, KK_FWD_PROJ, c5, st))) return rc;
     return cs ? comb_after(p, cs, f, st) : SRK_OK;
   }
-  if ((rc = launch_col(p, KK_FWD_P, c5, st))) return rc;
+  int k5 = KK_FWD_P;
+  if (d == 2) {  // 2D: a narrower x-forward tile where one is registered (more CTAs per SM)
+    init_registry();
+    auto it = g_fast->find(p->m0);
+    if (it != g_fast->end() && it->second.e[KK_FWD_P2D].fn) k5 = KK_FWD_P2D;
+  }
+  if ((rc = launch_col(p, k5, c5, st))) return rc;
   // K6: projection + viscous (+ Boussinesq terms)
   ProjArgs pa{};
   pa.g = geom(p);
