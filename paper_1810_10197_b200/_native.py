@@ -122,13 +122,25 @@ def stream_ptr(stream=None):
     return ctypes.c_void_p(s.cuda_stream)
 
 
+_HOST_RESULT = {}
+NO_HOST_RESULT = bool(os.environ.get("SRK_NO_HOST_RESULT"))  # A/B experiments: device result + cudaMemcpy
+
+
 def host_result(n):
     """Pinned host float64[n] a kernel can store into directly (UVA-mapped), for
     small results read by the host: no cudaMemcpy, so nothing queues behind bulk
-    copies on the copy engines."""
+    copies on the copy engines.  One cached buffer per (thread, size): callers
+    wait for the stream (``wait_stream_point``) and copy the values out before the
+    next call reuses it (a fresh pinned allocation per call cost ~1 ms)."""
+    import threading
+
     import torch
 
-    return torch.empty(n, dtype=torch.float64, pin_memory=True)
+    key = (threading.get_ident(), int(n))
+    buf = _HOST_RESULT.get(key)
+    if buf is None:
+        buf = _HOST_RESULT[key] = torch.empty(int(n), dtype=torch.float64, pin_memory=True)
+    return buf
 
 
 def wait_stream_point(stream=None):

@@ -180,6 +180,7 @@ def apply_forcing(u_hat, grid: Grid, target_energy, k_f, plan=None, allreduce=No
         _native.check(lib.srk_band_energy(ph, _native.ptr(u), ncomp, _native.ptr(idx), _native.ptr(w), nb,
                                           _native.ptr(eb), _native.stream_ptr()))
     _native.wait_stream_point()
+    eb = eb.clone()  # the pinned buffer is reused by the next call
     if allreduce is not None:
         s = allreduce([q[4].item() if q is not None else 0.0, eb.item()])
         e_total = (s[0] if q is not None else float(energy_sum)) / pts2
