@@ -512,6 +512,51 @@ def run_slab(args, rank, world, local_rank):
     achieved = grp_bytes[dom] / (grp_ms[dom] * 1e-3) / 1e9
     a2a_bytes = (geo["send1"] + geo["send2"]) * 16 * (world - 1) / world
     a2a_ms = ph[1] + ph[3]
+    # ---- e2e: each rank's slab resident on its host, as in run_native ----
+    e2e = None
+    if not args.no_e2e:
+        s2 = new_state()
+        mirror = srk.HostMirror(s2["y"])
+        mirror.load_host(s2["y"].cpu())
+        fplanes = srk.forcing_planes(g, k_f)
+        spec = {}
+
+        def on_y_new(v):
+            mirror.push(v)
+            spec["next"] = mirror.pull(wait=False)
+
+        torch.cuda.synchronize()
+        dist.barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev2, t2_ = 0, s2["t"]
+        n_e2e = max(2, args.steps // 2)
+        b_in0, b_out0 = mirror.h2d_bytes, mirror.d2h_bytes
+        a0.record(st)
+        yd = mirror.pull()
+        for _ in range(n_e2e):
+            fd = rhs(t2_, yd)
+            red(reduce_sums(g, yd, fl=fd, flags=2, ncomp=3, plan=plan))
+            out = srk.adaptive_advance(yd, t2_, pair, s2["ctrl"], cfg, rhs, first_stage=fd, grid=g,
+                                       allreduce=red, plan=plan, on_y_new=on_y_new)
+            srk.apply_forcing(out.y_new, g, energy, k_f, plan=plan, allreduce=red, slab=(rank, world),
+                              energy_sum=out.diag_sums[4])
+            mirror.push(out.y_new, planes=fplanes)
+            ev2 += out.rhs_evals + 1
+            t2_ = out.t_new
+            del yd, fd, out
+            yd = mirror.pull(into=spec.pop("next"), planes=fplanes)
+        mirror.wait()
+        a1.record(st)
+        torch.cuda.synchronize()
+        t2 = torch.tensor([a0.elapsed_time(a1) / 1e3], dtype=torch.float64, device=dev)
+        dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+        e2e = {"value": ev2 / t2.item(), "unit": "stages/s",
+               "h2d_bytes_per_step": (mirror.h2d_bytes - b_in0) // n_e2e,
+               "d2h_bytes_per_step": (mirror.d2h_bytes - b_out0) // n_e2e + 9 * 8,
+               "path": "per rank: y-slab host->device (pinned HostMirror), cached tendency + diagnostics, "
+                       "adaptive_advance (BS5, rank-order sums) + forcing, y_new slab device->host overlapped "
+                       "with the FSAL stage; bytes are per rank"}
+
     if rank != 0:
         return
     names = ["K1 (forward)", "K2-K4 (middle)", "K5-K6 (finish)"]
@@ -533,7 +578,7 @@ def run_slab(args, rank, world, local_rank):
                                   "pipelined_rhs": ph[5], "kz_chunks": len(rhs.chunks)}},
         "nvlink": {"bytes_per_rhs_per_gpu": a2a_bytes, "achieved_GBps": a2a_bytes / (a2a_ms * 1e-3) / 1e9
                    if world > 1 else None, "peak_GBps": 770.0, "peak_source": "B200_PROFILING.md peer copy"},
-        "cpu_baseline": None, "e2e": None, "gpu_launches": launches, "clocks": clk.summary(),
+        "cpu_baseline": None, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
 

@@ -134,6 +134,13 @@ int srk_band_energy(srk_plan* plan, const void* u, int ncomp, const int64_t* idx
 int srk_band_scale(srk_plan* plan, void* u, int ncomp, const int64_t* idx_dev, int nb, double gamma,
                    void* stream);
 
+/* Small-result store: dst[i] = src[i], i < n, by a kernel on ``stream``; dst is
+ * pinned (UVA-mapped) host memory, so the host reads the values after a stream
+ * sync without a cudaMemcpy that could queue behind bulk host copies on the
+ * copy engines (the reference reads its sums as numpy scalars,
+ * control.py:72-79; the slab path's rank-order sums come back through this). */
+int srk_store_mapped(const double* src_dev, double* dst_mapped, int n, void* stream);
+
 /* srk_rhs with a CUDA event after every kernel (synchronises): writes the
  * per-kernel device times [ms] in launch order to ms_out and returns
  * -(number of kernels) on success, a positive error code otherwise.

@@ -28,7 +28,7 @@ EXPORTS = (
     "srk_band_scale", "srk_rhs_launch_count", "srk_rhs_timed", "srk_plan_create_slab", "srk_slab_sizes",
     "srk_slab_forward", "srk_slab_middle", "srk_slab_finish", "srk_debug_phase_buffer",
     "srk_slab_forward_kz", "srk_slab_inverse_y_kz", "srk_slab_zpass", "srk_slab_forward_y_kz",
-    "srk_slab_forward_x_kz", "srk_slab_project",
+    "srk_slab_forward_x_kz", "srk_slab_project", "srk_store_mapped",
 )
 
 _lib = None
@@ -78,6 +78,7 @@ def load():
         "srk_step_reduce": (c_int, [vp, vp, vp, c_int, P(vp), P(c_dbl), vp, c_int, c_dbl, c_dbl, c_int, vp, vp]),
         "srk_band_energy": (c_int, [vp, vp, c_int, vp, vp, c_int, vp, vp]),
         "srk_band_scale": (c_int, [vp, vp, c_int, vp, c_int, c_dbl, vp]),
+        "srk_store_mapped": (c_int, [vp, vp, c_int, vp]),
         "srk_rhs_launch_count": (c_int, [vp]),
         "srk_rhs_timed": (c_int, [vp, vp, vp, c_dbl, c_dbl, c_dbl, vp, P(ctypes.c_float), c_int]),
         "srk_plan_create_slab": (c_int, [P(vp), P(i64), P(c_dbl), c_int, c_int, c_int]),
@@ -141,6 +142,23 @@ def host_result(n):
     if buf is None:
         buf = _HOST_RESULT[key] = torch.empty(int(n), dtype=torch.float64, pin_memory=True)
     return buf
+
+
+def fetch_small(t, stream=None):
+    """Small CUDA float64 tensor -> CPU tensor through a kernel store into mapped
+    pinned memory (srk_store_mapped) instead of a cudaMemcpy (which would queue
+    behind a large HostMirror copy on the copy engine)."""
+    import torch
+
+    t = t.to(torch.float64).contiguous()
+    if NO_HOST_RESULT:
+        return t.cpu()
+    buf = host_result(t.numel())
+    check(load().srk_store_mapped(ptr(t), ctypes.c_void_p(buf.data_ptr()), t.numel(), stream_ptr(stream)),
+          "srk_store_mapped")
+    count(1)
+    wait_stream_point(stream)
+    return buf.clone()
 
 
 def wait_stream_point(stream=None):

@@ -630,6 +630,12 @@ void srk_launch_band_energy(const cplx* u, const long long* idx, const double* w
                             long long modes, double* out, cudaStream_t st) {
   k_band_energy<<<1, 256, 0, st>>>(u, idx, w, nb, ncomp, modes, out);
 }
+__global__ void k_store_mapped(const double* __restrict__ src, double* dst, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+void srk_launch_store_mapped(const double* src, double* dst, int n, cudaStream_t st) {
+  if (n > 0) k_store_mapped<<<1, 32, 0, st>>>(src, dst, n);
+}
 void srk_launch_band_scale(cplx* u, const long long* idx, int nb, int ncomp, long long modes, double gamma,
                            cudaStream_t st) {
   const int tot = nb * ncomp;

@@ -67,5 +67,6 @@ void srk_launch_combine(const CombArgs& a, cudaStream_t st);
 void srk_launch_reduce(const RedArgs& a, double* out, cudaStream_t st);
 void srk_launch_band_energy(const cplx* u, const long long* idx, const double* w, int nb, int ncomp,
                             long long modes, double* out, cudaStream_t st);
+void srk_launch_store_mapped(const double* src, double* dst, int n, cudaStream_t st);
 void srk_launch_band_scale(cplx* u, const long long* idx, int nb, int ncomp, long long modes, double gamma,
                            cudaStream_t st);

@@ -988,6 +988,13 @@ int srk_band_scale(srk_plan* p, void* u, int ncomp, const int64_t* idx, int nb, 
   return check_launch("k_band_scale");
 }
 
+int srk_store_mapped(const double* src, double* dst, int n, void* stream) {
+  if ((!src || !dst) && n > 0) return fail(SRK_ERR_INVALID, "null pointer");
+  if (n < 0) return fail(SRK_ERR_INVALID, "negative count");
+  srk_launch_store_mapped(src, dst, n, (cudaStream_t)stream);
+  return check_launch("k_store_mapped");
+}
+
 // ---------------------------------------------------------------------------
 // Slab decomposition over y: rank r owns y-slab [r*Ny, (r+1)*Ny)
 // of the spectral state.  srk_slab_forward (K1) writes the x-padded signals

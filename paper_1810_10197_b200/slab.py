@@ -180,7 +180,8 @@ def dist_sum_in_rank_order(group=None):
         acc = parts[0].clone()
         for p in parts[1:]:
             acc += p
-        return acc.cpu().tolist()
+        # kernel store into mapped host memory (no cudaMemcpy behind HostMirror copies)
+        return (_native.fetch_small(acc) if acc.is_cuda else acc).tolist()
 
     return reduce
 
