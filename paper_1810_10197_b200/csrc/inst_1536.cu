@@ -8,7 +8,11 @@ void srk_reg_1536(KEntry* t) {
   // 2D Boussinesq z-pass, one pencil per CTA (2 columns, 128 threads, 3 CTAs/SM)
   {
     using Z2 = ColTile<1536, 2>;
+#ifdef SRK_B2E12
+    using E2 = FastFFT<1536, 12, Z2, 4, 4, 4, 4, 6>;
+#else
     using E2 = FastFFT<1536, 24, Z2, 8, 8, 24>;
+#endif
     t[KK_Z_B2] = KEntry{(const void*)(k_zpass<E2, Z2, ZOP_B2, E2, 1>), E2::NT, 2, (int)(Z2::SIZE * 16) + E2::TWN * 16, 0, 1};
   }
 #endif
@@ -18,7 +22,11 @@ void srk_reg_1536(KEntry* t) {
   // little; 3D keeps the four-column tiles of the base plan)
   {
     using SL2 = RowTile<1536, 2>;
+#ifdef SRK_X2E12
+    using SE2 = FastFFT<1536, 12, SL2, 4, 4, 4, 4, 6>;
+#else
     using SE2 = FastFFT<1536, 24, SL2, 8, 8, 24>;
+#endif
     constexpr int rhs_smem = (SL2::SIZE > 2 * 1024 * 2 ? SL2::SIZE : 2 * 1024 * 2) * 16;
     t[KK_INV_RHS] = SRK_ENTRY((k_colpass<SE2, PK_INV_RHS, +1, PF_CTN>), SE2, rhs_smem);
     t[KK_FWD_P2D] = SRK_ENTRY((k_colpass<SE2, PK_FWD, -1, PF_CTN>), SE2, SL2::SIZE * 16);
