@@ -1,9 +1,38 @@
 // Fast compile-time FFT plan instantiations (see registry.cuh).
 #include "registry.cuh"
-SRK_DEFINE_SIZE_F(srk_reg_1536_base, 1536, 24, 4, 12, (4, 4, 4, 4, 6), 8, 8, 24)
+#ifndef SRK_C1536
+// strided-pass tile columns at 1536 (3D 1024^3 slabs): two columns, 128 threads,
+// 3 CTAs per SM instead of one 256-thread CTA (140+ registers): one 1024^3/8 rank,
+// K1 4.69 -> 3.58, K2 10.77 -> 6.43, K4 4.64 -> 3.06 ms (tools/slab_rank_probe.py)
+#define SRK_C1536 2
+#endif
+SRK_DEFINE_SIZE_F(srk_reg_1536_base, 1536, 24, SRK_C1536, 12, (4, 4, 4, 4, 6), 8, 8, 24)
 void srk_reg_1536(KEntry* t) {
   srk_reg_1536_base(t);
   SRK_NS3F(1536, (8, 8, 6), 12, (4, 4, 2, 12))
+#ifndef SRK_NS3P1536
+#define SRK_NS3P1536 3
+#endif
+  // one z-pencil per CTA (192 threads, 89 KB, 2 CTAs per SM) instead of the pencil
+  // pair (384 threads, 166 KB, 1 CTA per SM): K3 of one 1024^3/8 rank 13.75 ->
+  // 10.66 ms with the forward suffix (24, 16); (16, 24) 11.55, (8, 8, 6) 11.72
+#if SRK_NS3P1536 == 1
+  SRK_NS3P(1536, (8, 8, 6), (16, 24))
+#elif SRK_NS3P1536 == 2
+  SRK_NS3P(1536, (8, 8, 6), (8, 8, 6))
+#elif SRK_NS3P1536 == 3
+  SRK_NS3P(1536, (8, 8, 6), (24, 16))
+#elif SRK_NS3P1536 == 4
+  SRK_NS3P(1536, (24, 8, 2), (24, 16))
+#elif SRK_NS3P1536 == 5
+  SRK_NS3P(1536, (12, 8, 4), (24, 16))
+#elif SRK_NS3P1536 == 6
+  SRK_NS3P(1536, (6, 8, 8), (24, 16))
+#elif SRK_NS3P1536 == 7
+  SRK_NS3P(1536, (8, 8, 6), (32, 12))
+#elif SRK_NS3P1536 == 8
+  SRK_NS3P(1536, (8, 8, 6), (12, 32))
+#endif
 #ifndef SRK_B2PAIR
   // 2D Boussinesq z-pass, one pencil per CTA (2 columns, 128 threads, 3 CTAs/SM)
   {

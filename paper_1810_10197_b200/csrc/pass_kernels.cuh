@@ -1034,7 +1034,7 @@ struct LoopStageZ {
 #define SRK_ZP1_MINB 5  // CTAs per SM the register budget targets (shared memory allows 5)
 #endif
 template <int M, class L, class EngI, int... FR>
-__global__ void __launch_bounds__(M / 8, SRK_ZP1_MINB) k_zpass_ns3p(const ZArgs a, int, int) {
+__global__ void __launch_bounds__(M / 8, (M <= 768 ? SRK_ZP1_MINB : 2)) k_zpass_ns3p(const ZArgs a, int, int) {
   extern __shared__ __align__(16) cplx smraw[];
   cplx* const sm = smraw + EngI::TWN;  // [twiddle table][tile]
   const cplx* const twp = smraw;

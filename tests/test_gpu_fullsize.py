@@ -195,3 +195,16 @@ def test_rhs_anisotropic_z512_matches_cufft_restatement(shape, lengths):
     ref = torch_ns_rhs(u, shape, 700.0, lengths)
     rel = (torch.linalg.vector_norm(f - ref) / torch.linalg.vector_norm(ref)).item()
     assert rel <= 1e-12, f"{shape}: rel L2 {rel:.3e}"
+
+
+@pytest.mark.parametrize("shape", [(32, 48, 1024), (1024, 32, 16), (16, 1024, 32), (64, 64, 1024)])
+def test_rhs_1536_axes_match_cufft_restatement(shape):
+    """M = 1536 passes (the 1024^3 slab configs' lengths) on each axis vs the torch.fft restatement."""
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    g = srk.Grid(shape)
+    u = torch.randn((3,) + g.kshape, dtype=torch.complex128, device="cuda", generator=gen)
+    u *= float(np.prod(shape)) / torch.linalg.vector_norm(u).item()
+    f = srk.FlowRHS(g, srk.PhysParams(700.0))(0.0, u)
+    ref = torch_ns_rhs(u, shape, 700.0, g.lengths)
+    rel = (torch.linalg.vector_norm(f - ref) / torch.linalg.vector_norm(ref)).item()
+    assert rel <= 1e-12, f"{shape}: rel L2 {rel:.3e}"
