@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--chunks", type=int, default=None,
                     help="slab mode: kz chunks of the pipelined RHS (exchange of chunk c overlaps chunk c+1); "
                          "default 4 for N > 1, 1 on a single GPU (nothing to overlap)")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
+                    help="slab mode: nccl = all_to_all_single (kz-chunk pipelined); peer = the exchange fused "
+                         "into K1 / K4 (row blocks stored into the peers' receive buffers over CUDA IPC)")
     ap.add_argument("--mode", default="auto", choices=["auto", "single", "slab", "replicas"],
                     help="auto: single GPU at N=1, slab decomposition (strong scaling) for N>1")
     return ap.parse_args()
@@ -429,7 +432,7 @@ def run_slab(args, rank, world, local_rank):
     energy, k_f = 0.5, 2.0
     red = dist_sum_in_rank_order()
     chunks = args.chunks if args.chunks is not None else (4 if world > 1 else 1)
-    rhs = SlabFlowRHS(g, params, rank, world, chunks=chunks)
+    rhs = SlabFlowRHS(g, params, rank, world, chunks=chunks, peer=args.exchange == "peer")
     plan = rhs.backend.h
     y0 = hit_slab(g, rank, world, a=4.0, energy=energy, seed=42, allreduce=red)
     pair = srk.make_bs5()
@@ -484,16 +487,31 @@ def run_slab(args, rank, world, local_rank):
         if w is not None:
             w.wait()
 
+    K = g.kshape[2]
     ev[0].record(st)
-    b.forward(yk, rhs.send1)
-    ev[1].record(st)
-    xchg(rhs.recv1, rhs.send1)
-    ev[2].record(st)
-    b.middle(rhs.recv1, rhs.send2)
-    ev[3].record(st)
-    xchg(rhs.recv2, rhs.send2)
-    ev[4].record(st)
-    b.finish(rhs.recv2, yk, fk)
+    if rhs.peer:  # K1 with its peer stores | barrier | K2-K4 (K4 with peer stores) | barrier | K5-K6
+        b.forward_kz_peer(yk, 0, K)
+        ev[1].record(st)
+        rhs.barrier()
+        ev[2].record(st)
+        b.inverse_y_kz(rhs.recv1, 0, K)
+        b.zpass()
+        b.forward_y_kz_peer(0, K)
+        ev[3].record(st)
+        rhs.barrier()
+        ev[4].record(st)
+        b.forward_x_kz(rhs.recv2, 0, K)
+        b.project(yk, fk)
+    else:
+        b.forward(yk, rhs.send1)
+        ev[1].record(st)
+        xchg(rhs.recv1, rhs.send1)
+        ev[2].record(st)
+        b.middle(rhs.recv1, rhs.send2)
+        ev[3].record(st)
+        xchg(rhs.recv2, rhs.send2)
+        ev[4].record(st)
+        b.finish(rhs.recv2, yk, fk)
     ev[5].record(st)
     # the pipelined RHS as the steps run it (exchanges overlapped with kernels)
     rhs(0.0, yk, out=fk)
@@ -566,7 +584,9 @@ def run_slab(args, rank, world, local_rank):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (device-side seeded HIT-spectrum slabs, E=0.5)",
         "config": {"workload": f"forced_hit_bs5_{n}^3", "n": n, "nu": 5e-4, "tol": 1e-6, "k_f": 2.0,
-                   "parallelism": f"y-slab x{world}, NCCL all-to-all, {len(rhs.chunks)} kz chunks pipelined",
+                   "parallelism": (f"y-slab x{world}, exchange fused into K1/K4 (peer stores over CUDA IPC)"
+                                   if rhs.peer else
+                                   f"y-slab x{world}, NCCL all-to-all, {len(rhs.chunks)} kz chunks pipelined"),
                    "l2": "inputs larger than L2"},
         "gpts_stage_per_s": value * n ** 3 / 1e9,
         "rhs_evals": evals,

@@ -187,6 +187,32 @@ int srk_slab_forward_y_kz(srk_plan* plan, void* send2_chunk, int k0, int kc, voi
 int srk_slab_forward_x_kz(srk_plan* plan, const void* recv2_chunk, int k0, int kc, void* stream);
 int srk_slab_project(srk_plan* plan, const void* y, void* f, double nu, double ri, double re_pr, void* stream);
 
+/* Exchange fused into the passes (P <= 8 ranks): K1 and K4 store
+ * their output row blocks straight into the peers' receive buffers over NVLink
+ * (peer pointers from CUDA IPC, srk_ipc_*), so the two all-to-alls ride on the
+ * passes' own stores, tile by tile, instead of separate NCCL collectives.
+ * srk_slab_set_peers: recv1[r] / recv2[r] = rank r's all-to-all #1 / #2
+ * receive buffer (sizes from srk_slab_sizes), n = nranks, r = this rank included.
+ * srk_slab_forward_kz_peer / srk_slab_forward_y_kz_peer: srk_slab_forward_kz /
+ * srk_slab_forward_y_kz writing rank d's block into rank d's receive chunk
+ * region at this rank's source block -- the layout srk_slab_inverse_y_kz /
+ * srk_slab_forward_x_kz read.  Ordering is the caller's: every rank's K1 (K4)
+ * must complete before any rank reads its recv1 (recv2), e.g. a one-element
+ * NCCL all-reduce on the compute streams between them.
+ * Replaces the all_to_all_single exchanges of slab.py (the reference has no
+ * multi-GPU path). */
+int srk_slab_set_peers(srk_plan* plan, const void* const recv1[], const void* const recv2[], int n);
+int srk_slab_forward_kz_peer(srk_plan* plan, const void* y, int k0, int kc, void* stream);
+int srk_slab_forward_y_kz_peer(srk_plan* plan, int k0, int kc, void* stream);
+
+/* CUDA IPC of a device buffer between the ranks' processes: export writes the
+ * 64-byte cudaIpcMemHandle of the allocation holding dev_ptr and dev_ptr's
+ * offset in it; import opens a peer's handle (lazy peer access) and returns the
+ * peer's buffer address in this process; close releases an imported mapping. */
+int srk_ipc_export(const void* dev_ptr, void* handle64_out, int64_t* offset_out);
+int srk_ipc_import(const void* handle64, int64_t offset, void** dev_ptr_out);
+int srk_ipc_close(void* dev_ptr, int64_t offset);
+
 /* Diagnostics: when dev_buf (u64) is non-NULL, launch number launch_index of
  * the next srk_rhs chain (0 = K1) records clock64() phase timestamps of every
  * 97th CTA into it (3 per CTA for the axis passes, 6 for the NS3 z-pass;

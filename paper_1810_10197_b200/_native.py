@@ -28,7 +28,8 @@ EXPORTS = (
     "srk_band_scale", "srk_rhs_launch_count", "srk_rhs_timed", "srk_plan_create_slab", "srk_slab_sizes",
     "srk_slab_forward", "srk_slab_middle", "srk_slab_finish", "srk_debug_phase_buffer",
     "srk_slab_forward_kz", "srk_slab_inverse_y_kz", "srk_slab_zpass", "srk_slab_forward_y_kz",
-    "srk_slab_forward_x_kz", "srk_slab_project", "srk_store_mapped",
+    "srk_slab_forward_x_kz", "srk_slab_project", "srk_store_mapped", "srk_slab_set_peers",
+    "srk_slab_forward_kz_peer", "srk_slab_forward_y_kz_peer", "srk_ipc_export", "srk_ipc_import", "srk_ipc_close",
 )
 
 _lib = None
@@ -79,6 +80,12 @@ def load():
         "srk_band_energy": (c_int, [vp, vp, c_int, vp, vp, c_int, vp, vp]),
         "srk_band_scale": (c_int, [vp, vp, c_int, vp, c_int, c_dbl, vp]),
         "srk_store_mapped": (c_int, [vp, vp, c_int, vp]),
+        "srk_slab_set_peers": (c_int, [vp, P(vp), P(vp), c_int]),
+        "srk_slab_forward_kz_peer": (c_int, [vp, vp, c_int, c_int, vp]),
+        "srk_slab_forward_y_kz_peer": (c_int, [vp, c_int, c_int, vp]),
+        "srk_ipc_export": (c_int, [vp, vp, P(i64)]),
+        "srk_ipc_import": (c_int, [vp, i64, P(vp)]),
+        "srk_ipc_close": (c_int, [vp, i64]),
         "srk_rhs_launch_count": (c_int, [vp]),
         "srk_rhs_timed": (c_int, [vp, vp, vp, c_dbl, c_dbl, c_dbl, vp, P(ctypes.c_float), c_int]),
         "srk_plan_create_slab": (c_int, [P(vp), P(i64), P(c_dbl), c_int, c_int, c_int]),

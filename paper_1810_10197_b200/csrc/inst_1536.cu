@@ -6,7 +6,13 @@
 // K1 4.69 -> 3.58, K2 10.77 -> 6.43, K4 4.64 -> 3.06 ms (tools/slab_rank_probe.py)
 #define SRK_C1536 2
 #endif
+#if defined(SRK_R1536) && SRK_R1536 == 1
+SRK_DEFINE_SIZE_F(srk_reg_1536_base, 1536, 24, SRK_C1536, 12, (4, 4, 4, 4, 6), 24, 8, 8)
+#elif defined(SRK_R1536) && SRK_R1536 == 2
+SRK_DEFINE_SIZE_F(srk_reg_1536_base, 1536, 24, SRK_C1536, 12, (4, 4, 4, 4, 6), 8, 24, 8)
+#else
 SRK_DEFINE_SIZE_F(srk_reg_1536_base, 1536, 24, SRK_C1536, 12, (4, 4, 4, 4, 6), 8, 8, 24)
+#endif
 void srk_reg_1536(KEntry* t) {
   srk_reg_1536_base(t);
   SRK_NS3F(1536, (8, 8, 6), 12, (4, 4, 2, 12))

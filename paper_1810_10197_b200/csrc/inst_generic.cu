@@ -16,6 +16,8 @@ void srk_reg_generic(KEntry* t) {
   t[KK_FWD_P_SLABI] = SRK_ENTRY((k_colpass<SE, PK_FWD, -1, PF_BIN>), SE, 0);
   t[KK_INV_KX] = SRK_ENTRY((k_colpass<SE, PK_INV_KX, +1, 0>), SE, 0);
   t[KK_INV_KX_SLAB] = SRK_ENTRY((k_colpass<SE, PK_INV_KX, +1, PF_BOUT>), SE, 0);
+  t[KK_INV_KX_PEER] = SRK_ENTRY((k_colpass<SE, PK_INV_KX, +1, PF_BOUT | PF_PEER>), SE, 0);
+  t[KK_FWD_P_PEER] = SRK_ENTRY((k_colpass<SE, PK_FWD, -1, PF_BOUT | PF_PEER>), SE, 0);
   t[KK_INV_CURLY] = SRK_ENTRY((k_colpass<SE, PK_INV_CURLY, +1, 0>), SE, 0);
   t[KK_INV_CURLY_SLAB] = SRK_ENTRY((k_colpass<SE, PK_INV_CURLY, +1, PF_BIN>), SE, 0);
   using Z4 = ColTile<SRK_GEN_MAXM, 4>;

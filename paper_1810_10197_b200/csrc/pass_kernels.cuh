@@ -20,6 +20,8 @@
 
 #include "fft_engine.cuh"
 
+#define SRK_MAX_PEERS 8
+
 enum PassKind {
   PK_INV = 0,      // plain padded / unpadded inverse
   PK_INV_RHS = 1,  // x inverse with the full curl on load (2D K1)
@@ -84,6 +86,10 @@ struct PassArgs {
   int kc, ngrp, tpg, in_k0, out_k0, kz0;
   long long in_kst, out_kst;
   long long in_rs, out_rs;  // row strides of input / output (0 -> row_stride)
+  // PF_PEER (slab all-to-all fused into the pass): output row block b goes to
+  // peer[b] (rank b's receive buffer at this rank's source block, UVA / CUDA IPC
+  // pointer) instead of out + b * out_bstride
+  cplx* peer[SRK_MAX_PEERS];
 };
 
 // Phase timestamps of every 97th CTA (diagnostics only; dbg == nullptr in
@@ -121,7 +127,9 @@ __device__ __forceinline__ void stage_rows(cplx* dst, const cplx* __restrict__ s
 // FL bits: PF_CTN -- padded pass with n = 2M/3 known at compile time (lets the
 // pad / truncate maps resolve statically); PF_BIN / PF_BOUT -- blocked input /
 // output rows (slab all-to-all layouts).
-enum PassFlags { PF_CTN = 1, PF_BIN = 2, PF_BOUT = 4 };
+// PF_PEER -- with PF_BOUT: output row blocks go straight to the peers' receive
+// buffers (PassArgs::peer), the exchange rides on the pass's own stores.
+enum PassFlags { PF_CTN = 1, PF_BIN = 2, PF_BOUT = 4, PF_PEER = 8 };
 
 // Block -> (plane, column group, first local column) of a strided pass.
 template <int KIND, int C>
@@ -199,6 +207,30 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
   const unsigned rso = (unsigned)a.out_rs;
   const cplx* __restrict__ inp = a.in + plane * a.in_plane_stride + w_in;
   cplx* __restrict__ outp = a.out + plane * a.out_plane_stride + w_out;
+  // output element (row, col): rows in blocks of out_rpb; PF_PEER sends block b to
+  // peer b (one shared-memory table lookup per store instead of a dynamically
+  // indexed kernel parameter)
+  __shared__ cplx* s_peer[(FL & PF_PEER) ? SRK_MAX_PEERS : 1];
+  if constexpr ((FL & PF_PEER) != 0) {
+    if (threadIdx.x < SRK_MAX_PEERS) {
+      cplx* q = a.peer[0];
+#pragma unroll
+      for (int i = 1; i < SRK_MAX_PEERS; ++i)
+        if ((int)threadIdx.x == i) q = a.peer[i];
+      s_peer[threadIdx.x] = q ? q + plane * a.out_plane_stride + w_out : nullptr;
+    }
+    __syncthreads();
+  }
+  const unsigned rso_ = (unsigned)a.out_rs;
+  const int orpb_ = (FL & PF_BOUT) ? a.out_rpb : 0;
+  auto oel = [&](int row, int col) -> cplx& {
+    if constexpr ((FL & PF_PEER) != 0) {
+      const int blk = row / orpb_;
+      return s_peer[blk][(unsigned)(row - blk * orpb_) * rso_ + (unsigned)col];
+    } else {
+      return outp[row_off(row, rso_, orpb_, a.out_bstride) + (unsigned)col];
+    }
+  };
   const int M = CTN ? Eng::M : a.M;
   const int n = CTN ? 2 * Eng::M / 3 : a.n;
   const int in_rpb = (FL & PF_BIN) ? a.in_rpb : 0;
@@ -260,7 +292,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
       if (use_tmo)
         sm[row * C + col] = v;
       else
-        outp[row_off(row, rso, out_rpb, a.out_bstride) + (unsigned)col] = v;
+        oel(row, col) = v;
     };
     Eng::template run<SIGN, Eng::kFast, kTMAO>(a.gp, sm, twp, ncols, ld, st);
     flush_out();
@@ -323,7 +355,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
       const double f = ok ? sc : 0.0;
       return cmk(v.x * f, v.y * f);
     };
-    auto st = [&](int row, int col, cplx v) { outp[row_off(row, rso, out_rpb, a.out_bstride) + (unsigned)col] = v; };
+    auto st = [&](int row, int col, cplx v) { oel(row, col) = v; };
     Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, twp, ncols, ld, st);
   } else if constexpr (KIND == PK_INV_KX) {
     // 3D K1.  k_y and k_z are constant along x, so the x inverse commutes with
@@ -357,7 +389,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
       if (use_tmo)
         sm[row * C + col] = v;
       else
-        outp[row_off(row, rso, out_rpb, a.out_bstride) + (unsigned)col] = v;
+        oel(row, col) = v;
     };
     Eng::template run<SIGN, Eng::kFast, kTMAO>(a.gp, sm, twp, ncols, ld, st);
     flush_out();
@@ -408,7 +440,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
       if (use_tmo)
         sm[row * C + col] = v;
       else
-        outp[row_off(row, rso, out_rpb, a.out_bstride) + (unsigned)col] = v;
+        oel(row, col) = v;
     };
     Eng::template run<SIGN, Eng::kFast, kTMAO>(a.gp, sm, twp, ncols, ld, st);
     flush_out();
@@ -434,7 +466,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
       cplx o = cmk(v.x * sc, v.y * sc);
       if (c == -2) o = cmk(0.0, 0.0);
       if (zdc && c == 0 && col == 0) o.y = 0.0;
-      outp[row_off(c == -2 ? (n >> 1) : c, rso, out_rpb, a.out_bstride) + (unsigned)col] = o;
+      oel(c == -2 ? (n >> 1) : c, col) = o;
     };
     Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, twp, ncols, ld, st);
   }

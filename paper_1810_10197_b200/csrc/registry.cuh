@@ -28,7 +28,9 @@ enum KernelKind {
   KK_FWD_PROJ = 19,        // K5 + K6 fused over a cluster of So CTAs (DSMEM)
   KK_FWD_PROJ_SLAB = 20,   // same, reading the all-to-all #2 receive layout
   KK_FWD_P2D = 21,         // 2D x-forward + truncation (K5) when a narrower tile is registered
-  KK_COUNT = 22
+  KK_INV_KX_PEER = 22,     // 3D K1, rows stored straight into the peers' all-to-all #1 receive buffers
+  KK_FWD_P_PEER = 23,      // K4, rows stored straight into the peers' all-to-all #2 receive buffers
+  KK_COUNT = 24
 };
 
 struct KEntry {
@@ -70,6 +72,8 @@ struct GenCols {
     t[KK_FWD_P_SLABI] = SRK_ENTRY((k_colpass<SE, PK_FWD, -1, PF_CTN | PF_BIN>), SE, SL::SIZE * 16); \
     t[KK_INV_KX] = SRK_ENTRY((k_colpass<SE, PK_INV_KX, +1, PF_CTN>), SE, SL::SIZE * 16);           \
     t[KK_INV_KX_SLAB] = SRK_ENTRY((k_colpass<SE, PK_INV_KX, +1, PF_CTN | PF_BOUT>), SE, SL::SIZE * 16); \
+    t[KK_INV_KX_PEER] = SRK_ENTRY((k_colpass<SE, PK_INV_KX, +1, PF_CTN | PF_BOUT | PF_PEER>), SE, SL::SIZE * 16); \
+    t[KK_FWD_P_PEER] = SRK_ENTRY((k_colpass<SE, PK_FWD, -1, PF_CTN | PF_BOUT | PF_PEER>), SE, SL::SIZE * 16); \
     t[KK_INV_CURLY] = SRK_ENTRY((k_colpass<SE, PK_INV_CURLY, +1, PF_CTN>), SE, SRK_RHS_SMEM(M, CS)); \
     t[KK_INV_CURLY_SLAB] = SRK_ENTRY((k_colpass<SE, PK_INV_CURLY, +1, PF_CTN | PF_BIN>), SE,       \
                                      SRK_RHS_SMEM(M, CS));                                         \

@@ -153,6 +153,11 @@ struct srk_plan {
   cudaEvent_t ev[16];
   int nev = 0;
   cudaStream_t tstream = nullptr;
+  // slab exchange fused into K1 / K4 (srk_slab_set_peers): every rank's
+  // all-to-all #1 / #2 receive buffer, indexed by rank (UVA / CUDA IPC pointers)
+  cplx* peer1[SRK_MAX_PEERS] = {};
+  cplx* peer2[SRK_MAX_PEERS] = {};
+  bool peers_set = false;
 };
 
 namespace {
@@ -253,15 +258,18 @@ bool encode_pass_map(CUtensorMap* tm, const cplx* base, const PassArgs& a, long 
 void setup_tma(int kind, int cols, PassArgs& a, CUtensorMap* tm) {
   a.tma = 0;
   const bool inv = kind == KK_INV || kind == KK_INV_P || kind == KK_INV_KX || kind == KK_INV_KX_SLAB ||
+                   kind == KK_INV_KX_PEER ||
                    kind == KK_INV_CURLY;
   const bool fwd = kind == KK_FWD || kind == KK_FWD_P || kind == KK_FWD_P_SLABO || kind == KK_FWD_P_SLABI ||
+                   kind == KK_FWD_P_PEER ||
                    kind == KK_FWD_P2D;
   const bool slab_in = kind == KK_INV_CURLY_SLAB || kind == KK_INV_P_SLAB;  // blocked input rows
   if (!(inv || fwd || slab_in) || !g_fast->count(a.M)) return;
   static const int skip_mask = getenv("SRK_TMA_SKIP") ? atoi(getenv("SRK_TMA_SKIP")) : 0;  // experiments
   if (a.in_rpb > 0 && getenv("SRK_NO_TMA5")) return;
   if (skip_mask & (1 << kind)) return;
-  if ((kind == KK_INV_KX || kind == KK_INV_KX_SLAB) && a.comp_stride != a.in_plane_stride) return;
+  if ((kind == KK_INV_KX || kind == KK_INV_KX_SLAB || kind == KK_INV_KX_PEER) && a.comp_stride != a.in_plane_stride)
+    return;
   const int rows = fwd ? a.M : a.n;
   const int rb = a.in_rpb > 0 ? a.in_rpb : rows;  // boxes must not straddle row blocks
   if (rows % rb) return;
@@ -1268,6 +1276,132 @@ int srk_slab_forward_y_kz(srk_plan* p, void* send2, int k0, int kc, void* stream
   c.out_bstride = (long long)p->So * Mx * Ny * kc;
   c.zero_nyq = 1;
   return launch_col(p, KK_FWD_P_SLABO, c, (cudaStream_t)stream);
+}
+
+int srk_slab_set_peers(srk_plan* p, const void* const* recv1, const void* const* recv2, int n) {
+  if (!p || !p->Mx) return fail(SRK_ERR_INVALID, "not a slab plan");
+  if (n != p->nranks || n > SRK_MAX_PEERS)
+    return fail(SRK_ERR_INVALID, "peer tables need one entry per rank (at most " +
+                                     std::to_string(SRK_MAX_PEERS) + ")");
+  for (int r = 0; r < n; ++r) {
+    if (!recv1[r] || !recv2[r]) return fail(SRK_ERR_INVALID, "null peer receive buffer");
+    p->peer1[r] = (cplx*)recv1[r];
+    p->peer2[r] = (cplx*)recv2[r];
+  }
+  p->peers_set = true;
+  return SRK_OK;
+}
+
+// K1 of kz chunk (k0, kc) with its output row blocks stored straight into the
+// peers' receive buffers: block d -> rank d's recv1 chunk region at this rank's
+// source block (the layout srk_slab_inverse_y_kz reads), so all-to-all #1 is the
+// pass's own NVLink stores.  Ordering: every rank's K1 must complete before any
+// rank's K2 reads its recv1 (a stream-ordered barrier between the two).
+int srk_slab_forward_kz_peer(srk_plan* p, const void* y, int k0, int kc, void* stream) {
+  if (bad_chunk(p, k0, kc)) return fail(SRK_ERR_INVALID, "not a slab plan / bad kz chunk");
+  if (!p->peers_set) return fail(SRK_ERR_INVALID, "srk_slab_set_peers not called");
+  const long long Ny = p->n1, Mx = p->Mx;
+  const long long per_kz = (long long)p->S1 * p->m0 * Ny;  // recv1 elements per kz
+  const long long bs = (long long)p->S1 * Mx * Ny * kc;     // source-block stride of the chunk
+  PassArgs a = x_pass(p, (const cplx*)y, p->peer1[p->rank], p->S1, p->n0, p->m0, p->m0, p->n0);
+  a.kc = kc;
+  a.ngrp = (int)Ny;
+  a.in_kst = p->K;
+  a.in_k0 = k0;
+  a.out_kst = kc;
+  a.out_k0 = 0;
+  a.kz0 = k0;
+  a.in_rs = Ny * p->K;
+  a.out_rs = Ny * kc;
+  a.out_plane_stride = Mx * Ny * kc;
+  a.out_rpb = (int)Mx;
+  a.out_bstride = bs;
+  for (int r = 0; r < p->nranks; ++r) a.peer[r] = p->peer1[r] + per_kz * k0 + (long long)p->rank * bs;
+  a.scale = std::pow(1.5, p->dims) / ((double)p->m0 * p->m1 * p->m2);
+  a.dims = p->dims;
+  a.n1 = p->n1;
+  a.K = p->K;
+  a.ck0 = p->ck0;
+  a.ck1 = p->ck1;
+  a.ck2 = p->ck2;
+  a.comp_stride = p->modes;
+  a.y0 = p->y0;
+  a.n1g = p->n1g;
+  return launch_col(p, KK_INV_KX_PEER, a, (cudaStream_t)stream);
+}
+
+// K4 of kz chunk (k0, kc) storing into the peers' recv2 chunk regions (all-to-all #2).
+int srk_slab_forward_y_kz_peer(srk_plan* p, int k0, int kc, void* stream) {
+  if (bad_chunk(p, k0, kc)) return fail(SRK_ERR_INVALID, "not a slab plan / bad kz chunk");
+  if (!p->peers_set) return fail(SRK_ERR_INVALID, "srk_slab_set_peers not called");
+  int rc = need_ws(p);
+  if (rc) return rc;
+  const long long K = p->K, Ny = p->n1, Mx = p->Mx, m1 = p->m1;
+  const long long per_kz = (long long)p->So * Mx * p->n1g;  // recv2 elements per kz
+  const long long bs = (long long)p->So * Mx * Ny * kc;
+  PassArgs c = base_pass();
+  c.in = p->A;
+  c.out = p->peer2[p->rank];
+  c.M = p->m1;
+  c.n = p->n1g;
+  c.planes = p->So * p->Mx;
+  c.Qp = kc;
+  c.kc = kc;
+  c.ngrp = 1;
+  c.in_k0 = k0;
+  c.out_k0 = 0;
+  c.kz0 = k0;
+  c.in_rs = K;
+  c.out_rs = kc;
+  c.in_plane_stride = m1 * K;
+  c.out_plane_stride = Ny * kc;
+  c.out_rpb = (int)Ny;
+  c.out_bstride = bs;
+  for (int r = 0; r < p->nranks; ++r) c.peer[r] = p->peer2[r] + per_kz * k0 + (long long)p->rank * bs;
+  c.zero_nyq = 1;
+  return launch_col(p, KK_FWD_P_PEER, c, (cudaStream_t)stream);
+}
+
+// ---- CUDA IPC of receive buffers between the ranks' processes ---------------
+typedef CUresult (*srk_get_range_fn)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+int srk_ipc_export(const void* dev_ptr, void* handle_out, int64_t* offset_out) {
+  if (!dev_ptr || !handle_out || !offset_out) return fail(SRK_ERR_INVALID, "null argument");
+  static srk_get_range_fn range = nullptr;
+  if (!range) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+      return fail(SRK_ERR_CUDA, "cuMemGetAddressRange entry point unavailable");
+    range = (srk_get_range_fn)fn;
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, (CUdeviceptr)dev_ptr) != CUDA_SUCCESS) return fail(SRK_ERR_CUDA, "cuMemGetAddressRange failed");
+  cudaIpcMemHandle_t h;
+  cudaError_t err = cudaIpcGetMemHandle(&h, (void*)base);
+  if (err != cudaSuccess) return fail(SRK_ERR_CUDA, std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(err));
+  memcpy(handle_out, &h, sizeof(h));
+  *offset_out = (int64_t)((const char*)dev_ptr - (const char*)base);
+  return SRK_OK;
+}
+
+int srk_ipc_import(const void* handle, int64_t offset, void** dev_ptr_out) {
+  if (!handle || !dev_ptr_out) return fail(SRK_ERR_INVALID, "null argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  void* base = nullptr;
+  cudaError_t err = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+  if (err != cudaSuccess) return fail(SRK_ERR_CUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(err));
+  *dev_ptr_out = (char*)base + offset;
+  return SRK_OK;
+}
+
+int srk_ipc_close(void* dev_ptr, int64_t offset) {
+  if (!dev_ptr) return SRK_OK;
+  cudaError_t err = cudaIpcCloseMemHandle((char*)dev_ptr - offset);
+  if (err != cudaSuccess) return fail(SRK_ERR_CUDA, std::string("cudaIpcCloseMemHandle: ") + cudaGetErrorString(err));
+  return SRK_OK;
 }
 
 int srk_slab_forward_x_kz(srk_plan* p, const void* recv2, int k0, int kc, void* stream) {

@@ -130,11 +130,91 @@ class CudaSlabBackend:
                                                 _native.stream_ptr()))
         _native.count(1)
 
+    # ---- exchange fused into K1 / K4 (peer stores, srk_slab_*_peer) ----
+    def set_peers(self, recv1_ptrs, recv2_ptrs):
+        n = len(recv1_ptrs)
+        a1 = (ctypes.c_void_p * n)(*[ctypes.c_void_p(int(q)) for q in recv1_ptrs])
+        a2 = (ctypes.c_void_p * n)(*[ctypes.c_void_p(int(q)) for q in recv2_ptrs])
+        _native.check(self.lib.srk_slab_set_peers(self.h, a1, a2, n), "srk_slab_set_peers")
+
+    def forward_kz_peer(self, y, k0, kc):
+        _native.check(self.lib.srk_slab_forward_kz_peer(self.h, _native.ptr(y), k0, kc, _native.stream_ptr()))
+        _native.count(1)
+
+    def forward_y_kz_peer(self, k0, kc):
+        _native.check(self.lib.srk_slab_forward_y_kz_peer(self.h, k0, kc, _native.stream_ptr()))
+        _native.count(1)
+
     def __del__(self):
         try:
             self.lib.srk_plan_destroy(self.h)
         except Exception:
             pass
+
+
+def ipc_export(t):
+    """(64-byte CUDA IPC handle, offset) of a CUDA tensor's storage (srk_ipc_export)."""
+    lib = _native.load()
+    h = (ctypes.c_char * 64)()
+    off = ctypes.c_int64()
+    _native.check(lib.srk_ipc_export(_native.ptr(t), h, ctypes.byref(off)), "srk_ipc_export")
+    return bytes(h), off.value
+
+
+def ipc_import(handle, offset):
+    """Address of a peer process's buffer in this process (srk_ipc_import)."""
+    lib = _native.load()
+    buf = ctypes.create_string_buffer(bytes(handle), 64)
+    out = ctypes.c_void_p()
+    _native.check(lib.srk_ipc_import(buf, int(offset), ctypes.byref(out)), "srk_ipc_import")
+    return out.value
+
+
+def ipc_close(ptr, offset):
+    _native.check(_native.load().srk_ipc_close(ctypes.c_void_p(int(ptr)), int(offset)), "srk_ipc_close")
+
+
+def exchange_peer_tables(recv1, recv2, group=None):
+    """All ranks' recv1 / recv2 addresses in this process: own buffers directly,
+    the others through CUDA IPC (handles all-gathered over torch.distributed).
+    Returns (recv1_ptrs, recv2_ptrs, imported) -- ``imported`` lists the (ptr,
+    offset) mappings to close."""
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    mine = (ipc_export(recv1), ipc_export(recv2))
+    allh = [None] * world
+    dist.all_gather_object(allh, mine, group=group)
+    p1, p2, imported = [], [], []
+    for r in range(world):
+        if r == rank:
+            p1.append(recv1.data_ptr())
+            p2.append(recv2.data_ptr())
+            continue
+        (h1, o1), (h2, o2) = allh[r]
+        a, b = ipc_import(h1, o1), ipc_import(h2, o2)
+        p1.append(a)
+        p2.append(b)
+        imported += [(a, o1), (b, o2)]
+    return p1, p2, imported
+
+
+def dist_stream_barrier(group=None):
+    """Stream-ordered barrier for the peer-store exchange: a one-element NCCL
+    all-reduce on the compute stream completes on a rank only after every rank
+    has reached it, i.e. after every rank's preceding K1 / K4 (and its NVLink
+    stores) finished."""
+    import torch.distributed as dist
+
+    flag = {}
+
+    def barrier():
+        t = flag.get("t")
+        if t is None:
+            t = flag["t"] = torch.zeros(1, dtype=torch.float32, device=torch.device("cuda", torch.cuda.current_device()))
+        dist.all_reduce(t, group=group)
+
+    return barrier
 
 
 def dist_all_to_all(group=None, async_op=False):
@@ -197,10 +277,18 @@ class SlabFlowRHS:
     """``f(t, y_slab)`` for one rank of a slab-decomposed grid (drop-in for FlowRHS)."""
 
     def __init__(self, grid: Grid, params: PhysParams, rank: int, nranks: int, density=False, backend=None,
-                 exchange=None, chunks=1):
+                 exchange=None, chunks=1, peer=False, barrier=None):
         """``chunks`` > 1 pipelines the RHS over kz chunks: the exchange of
         chunk c (asynchronous, ``exchange`` must then return a handle with
-        ``wait()``) overlaps the kernels of the neighbouring chunks."""
+        ``wait()``) overlaps the kernels of the neighbouring chunks.
+
+        ``peer=True`` fuses the two all-to-alls into K1 / K4: their row blocks
+        are stored straight into the ranks' receive buffers (CUDA IPC peer
+        pointers over NVLink, srk_slab_*_peer) and a stream-ordered ``barrier``
+        (default: one-element NCCL all-reduce) separates them from the readers;
+        no NCCL data movement, the transfer rides on the passes' stores tile by
+        tile.  ``peer_tables`` may be given instead of torch.distributed (one
+        process driving several emulated ranks)."""
         self.grid, self.params, self.rank, self.nranks = grid, params, rank, nranks
         self.density = bool(density)
         self.geo = slab_geometry(grid, nranks, density)
@@ -211,8 +299,23 @@ class SlabFlowRHS:
             exchange = dist_all_to_all(async_op=self.pipelined)
         self.exchange = exchange
         g = self.geo
-        self.send1, self.recv1 = self.backend.empty(g["send1"]), self.backend.empty(g["send1"])
-        self.send2, self.recv2 = self.backend.empty(g["send2"]), self.backend.empty(g["send2"])
+        self.peer = bool(peer)
+        self._imported = []
+        if self.peer:
+            self.send1 = self.send2 = None
+            self.recv1, self.recv2 = self.backend.empty(g["send1"]), self.backend.empty(g["send2"])
+            if nranks == 1:
+                p1, p2 = [self.recv1.data_ptr()], [self.recv2.data_ptr()]
+            else:
+                p1, p2, self._imported = exchange_peer_tables(self.recv1, self.recv2)
+            self.backend.set_peers(p1, p2)
+            self.barrier = barrier if barrier is not None else \
+                (dist_stream_barrier() if nranks > 1 else (lambda: None))
+            self.chunks = [(0, g["K"])]
+            self.pipelined = False
+        else:
+            self.send1, self.recv1 = self.backend.empty(g["send1"]), self.backend.empty(g["send1"])
+            self.send2, self.recv2 = self.backend.empty(g["send2"]), self.backend.empty(g["send2"])
         self.calls = 0
 
     @property
@@ -225,6 +328,18 @@ class SlabFlowRHS:
 
     def __call__(self, t, y, out=None):
         f = out if out is not None else (torch.empty_like(y) if isinstance(y, torch.Tensor) else np.empty_like(y))
+        if self.peer:
+            be, K = self.backend, self.geo["K"]
+            be.forward_kz_peer(y, 0, K)        # K1 + all-to-all #1 (peer stores)
+            self.barrier()
+            be.inverse_y_kz(self.recv1, 0, K)  # K2
+            be.zpass()                         # K3
+            be.forward_y_kz_peer(0, K)         # K4 + all-to-all #2 (peer stores)
+            self.barrier()
+            be.forward_x_kz(self.recv2, 0, K)  # K5
+            be.project(y, f)                   # K6
+            self.calls += 1
+            return f
         if not self.pipelined:
             self.backend.forward(y, self.send1)
             self.exchange(self.recv1, self.send1)

@@ -45,3 +45,9 @@ def test_bench_slab_over_nccl():
     assert d["n_gpus"] == 1 and d["scaling"] == "strong" and d["value"] > 0
     assert d["roofline"]["phase_ms"]["serial_rhs"] > 0 and d["gpu_launches"] > 0
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] >= 3 * 64 * 64 * 33 * 16
+
+
+def test_bench_slab_peer_exchange():
+    d = run_bench("--mode", "slab", "--exchange", "peer", "--grid", "64", "--steps", "2", "--warmup", "3", "--no-e2e",
+                  env={"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(random.randint(20000, 40000))})
+    assert d["value"] > 0 and "peer stores" in d["config"]["parallelism"]

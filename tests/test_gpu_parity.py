@@ -481,3 +481,61 @@ def test_fused_cluster_projection_matches(monkeypatch):
     monkeypatch.setenv("SRK_FUSEPROJ", "1")
     f1 = srk.FlowRHS(g, srk.PhysParams(500.0))(0.0, y)
     assert rel(f1, f0) <= 1e-15
+
+
+@pytest.mark.parametrize("P,shape", [(2, (32, 32, 32)), (3, (32, 48, 16)), (4, (64, 64, 64)),
+                                     (8, (64, 64, 64)), (2, (256, 256, 256))])
+def test_slab_peer_stores_emulated_ranks_match_single_gpu(P, shape):
+    """All-to-alls fused into K1 / K4 (srk_slab_*_peer: row blocks stored straight
+    into every rank's receive buffer): P virtual ranks on one GPU whose peer tables
+    point at each other's receive buffers, vs the unsplit RHS -- and bitwise equal
+    to the NCCL-layout path with block-copy exchanges."""
+    from paper_1810_10197_b200.slab import CudaSlabBackend, scatter_slab, slab_geometry
+
+    g = srk.Grid(shape)
+    params = srk.PhysParams(321.0)
+    if shape[0] >= 256:
+        y = srk.hit_init(g, srk.ProblemSpec("hit", a=4.0, energy=0.5, seed=8)).fields
+    else:
+        y = dev(O.hit(O.OGrid(shape), a=4.0, energy=0.5, seed=8))
+    f_ref = srk.FlowRHS(g, params)(0.0, y)
+    geo = slab_geometry(g, P)
+    K = geo["K"]
+    backs = [CudaSlabBackend(g, params, r, P) for r in range(P)]
+    ys = [scatter_slab(y, r, P) for r in range(P)]
+    r1 = [b.empty(geo["send1"]).fill_(float("nan")) for b in backs]
+    r2 = [b.empty(geo["send2"]).fill_(float("nan")) for b in backs]
+    for b in backs:
+        b.set_peers([t.data_ptr() for t in r1], [t.data_ptr() for t in r2])
+    for r in range(P):
+        backs[r].forward_kz_peer(ys[r], 0, K)
+    for r in range(P):  # (every rank's K1 done: one stream)
+        backs[r].inverse_y_kz(r1[r], 0, K)
+        backs[r].zpass()
+        backs[r].forward_y_kz_peer(0, K)
+    fs = [torch.empty_like(ys[r]) for r in range(P)]
+    for r in range(P):
+        backs[r].forward_x_kz(r2[r], 0, K)
+        backs[r].project(ys[r], fs[r])
+    f = torch.cat(fs, dim=2)
+    assert float(torch.linalg.norm(f - f_ref) / torch.linalg.norm(f_ref)) <= 1e-14
+    # the same kernels with the exchange as block copies (send layouts) give the same bits
+    s1 = [b.empty(geo["send1"]) for b in backs]
+    for r in range(P):
+        backs[r].forward(ys[r], s1[r])
+    blk = s1[0].numel() // P
+    for r in range(P):
+        assert torch.equal(torch.cat([s1[q][r * blk:(r + 1) * blk] for q in range(P)]), r1[r])
+
+
+def test_slab_flowrhs_peer_world1_matches_flowrhs():
+    from paper_1810_10197_b200.slab import SlabFlowRHS
+
+    g = srk.Grid((64, 64, 64))
+    params = srk.PhysParams(400.0)
+    y = srk.hit_init(g, srk.ProblemSpec("hit", a=4.0, energy=0.5, seed=3)).fields
+    f_ref = srk.FlowRHS(g, params)(0.0, y)
+    rhs = SlabFlowRHS(g, params, 0, 1, peer=True)
+    f = rhs(0.0, y)
+    assert float(torch.linalg.norm(f - f_ref) / torch.linalg.norm(f_ref)) <= 1e-14
+    assert rhs.send1 is None  # no send buffers: K1 / K4 store into the receive buffers
