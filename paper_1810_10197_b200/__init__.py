@@ -19,7 +19,7 @@ from .control import (AdvanceOutcome, ControllerConfig, ControllerState, StepSiz
                       adaptive_advance, error_norm, error_norm_delta, propose_step, scale_vector)
 from .diagnostics import (DiagnosticsRecord, SpectrumRecord, compare_series, dissipation_rate, energy_spectrum,
                           enstrophy, field_error_norms, kinetic_energy)
-from .problems import ProblemSpec, hit_init, rayleigh_taylor_init, taylor_green_init
+from .problems import ProblemSpec, hit_init, rayleigh_taylor_init, rt_tanh_init, taylor_green_init
 from .simulation import (ADAPTIVE_CAPABLE, INTEGRATORS, ConfigError, RunConfig, SimulationResult,
                          default_lengths, make_initial_state, run_simulation)
 from .checkpoint import (CheckpointData, CheckpointError, read_checkpoint, read_diagnostics_csv,

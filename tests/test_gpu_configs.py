@@ -155,3 +155,10 @@ def test_c5_forced_hit64_window():
     c = cfg((64,) * 3, "hit", 2000.0, "bs5", "adaptive", 1e9, a=4.0, energy=0.5, forcing=True, k_f=2.0)
     res = srk.run_simulation(c, initial_state=y0, max_steps=5)
     compare(res, y_ref, recs)
+
+
+def test_c4_rt_tanh_init_matches_oracle():
+    """The product's config-4 IC generator (device transforms) vs the oracle's restatement."""
+    og, y0 = _c4()
+    st = srk.rt_tanh_init(srk.Grid((1024, 1024)), width=0.05, amp=1e-3, kmax=8, seed=4)
+    assert rel(st.fields, y0) <= 1e-13
