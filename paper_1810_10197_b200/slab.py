@@ -318,6 +318,12 @@ class SlabFlowRHS:
             self.send2, self.recv2 = self.backend.empty(g["send2"]), self.backend.empty(g["send2"])
         self.calls = 0
 
+    def close(self):
+        """Release the CUDA IPC mappings of the other ranks' receive buffers (peer mode)."""
+        for ptr, off in self._imported:
+            ipc_close(ptr, off)
+        self._imported = []
+
     @property
     def local_kshape(self):
         g = self.geo
