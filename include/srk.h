@@ -82,6 +82,19 @@ int srk_rhs_combine(srk_plan* plan, const void* y, void* f, double nu, double ri
                     const void* ybase, int nterms, const void* const* F, const double* coef, double coef_self,
                     void* ynext, void* stream);
 
+/* The refresh after a step's forcing (simulation.py:165-182 after_accept: the
+ * cached tendency and the diagnostics record of the new state) fused with the
+ * next step's first stage sum (integrators.py:327-333, row 2 of A):
+ *   f     = FlowRHS(y)
+ *   ynext = y + coef_self * f              (bitwise srk_rhs_combine(ybase = y))
+ *   diag_out[4] = sum_k w_k sum_j |y_jk|^2, diag_out[5] = sum w Re(y conj f),
+ *   diag_out[8] = sum w |k|^2 |y|^2, other entries 0 -- the srk_step_reduce
+ *   (flags = 2) layout, fixed-order (deterministic) sums; diag_out may be
+ *   mapped pinned host memory.
+ * One pass of the projection kernel (y is read once); 3D NS, unsplit plans. */
+int srk_rhs_refresh(srk_plan* plan, const void* y, void* f, double nu, double ri, double re_pr, double coef_self,
+                    void* ynext, double* diag_out, void* stream);
+
 /* DealiasWorkspace.widen (spectral.py:215-261): spec (ncomp, kshape) ->
  * phys (ncomp, 3n0/2, 3n1/2[, 3n2/2]) float64. */
 int srk_widen(srk_plan* plan, const void* spec, int ncomp, void* phys, void* stream);

@@ -30,6 +30,7 @@ EXPORTS = (
     "srk_slab_forward_kz", "srk_slab_inverse_y_kz", "srk_slab_zpass", "srk_slab_forward_y_kz",
     "srk_slab_forward_x_kz", "srk_slab_project", "srk_store_mapped", "srk_slab_set_peers",
     "srk_slab_forward_kz_peer", "srk_slab_forward_y_kz_peer", "srk_ipc_export", "srk_ipc_import", "srk_ipc_close",
+    "srk_rhs_refresh",
 )
 
 _lib = None
@@ -80,6 +81,7 @@ def load():
         "srk_band_energy": (c_int, [vp, vp, c_int, vp, vp, c_int, vp, vp]),
         "srk_band_scale": (c_int, [vp, vp, c_int, vp, c_int, c_dbl, vp]),
         "srk_store_mapped": (c_int, [vp, vp, c_int, vp]),
+        "srk_rhs_refresh": (c_int, [vp, vp, vp, c_dbl, c_dbl, c_dbl, c_dbl, vp, vp, vp]),
         "srk_slab_set_peers": (c_int, [vp, P(vp), P(vp), c_int]),
         "srk_slab_forward_kz_peer": (c_int, [vp, vp, c_int, c_int, vp]),
         "srk_slab_forward_y_kz_peer": (c_int, [vp, c_int, c_int, vp]),

@@ -118,16 +118,19 @@ __device__ __forceinline__ KVec kvec32(unsigned idx, const GeomArgs& g) {
 #ifndef SRK_PC_CH
 #define SRK_PC_CH 256  // modes per chunk (and threads) of the fused K6 + stage-sum kernel; ncu: 128 -> 256 is 1-7% faster
 #endif
-template <int DIMS, bool DENS, int NTC = -1>
+template <int DIMS, bool DENS, int NTC = -1, bool DIAG = false>
 __global__ void __launch_bounds__(NTC < 0 ? SRK_PT_CH : SRK_PC_CH) k_project_tma(const ProjArgs a) {
   extern __shared__ __align__(128) cplx psm[];
   constexpr int CH = NTC < 0 ? SRK_PT_CH : SRK_PC_CH;
   constexpr int d = DIMS;
   constexpr int NG = DENS ? 2 * d : d;  // G components
   constexpr int NY = DENS ? d + 1 : d;  // state components
-  constexpr int NC = NTC < 0 ? 0 : d * (NTC + 1);  // ybase + F_t components
+  // ybase + F_t components (DIAG: ybase is the state, already in the ring)
+  constexpr int NC = NTC < 0 ? 0 : (DIAG ? 0 : d) + d * NTC;
   constexpr int NS = NG + NY + NC;
   static_assert(NTC < 0 || (DIMS == 3 && !DENS), "fused stage combination: 3D NS only");
+  static_assert(!DIAG || NTC == 0, "refresh: the state's own next-stage input only");
+  double e_acc = 0.0, ep_acc = 0.0, z_acc = 0.0;  // DIAG: E, eps, Z partial sums of this thread
   __shared__ __align__(8) unsigned long long mb[2];
   const int tid = threadIdx.x;
   const long long n = a.modes;
@@ -149,7 +152,7 @@ __global__ void __launch_bounds__(NTC < 0 ? SRK_PT_CH : SRK_PC_CH) k_project_tma
     for (int j = 0; j < NG; ++j) bulk_g2s(st + j * CH, a.G + j * n + i0, cnt * 16u, &mb[b]);
 #pragma unroll
     for (int j = 0; j < NY; ++j) bulk_g2s(st + (NG + j) * CH, a.y + j * n + i0, cnt * 16u, &mb[b]);
-    if constexpr (NTC >= 0) {
+    if constexpr (NTC >= 0 && !DIAG) {
 #pragma unroll
       for (int j = 0; j < d; ++j) bulk_g2s(st + (NG + NY + j) * CH, a.yb + j * n + i0, cnt * 16u, &mb[b]);
 #pragma unroll
@@ -186,16 +189,28 @@ __global__ void __launch_bounds__(NTC < 0 ? SRK_PT_CH : SRK_PC_CH) k_project_tma
       for (int j = 1; j < d; ++j) kd = radd(kd, rmul(kv.k[j], Gv[j]));
       kd = rmul(kv.inv_k2, kd);
       const double nuk2 = DMUL(a.nu, kv.k2);
+      double wgt = 0.0;
+      if constexpr (DIAG) {  // Hermitian weight of the mode (diagnostics.py:39-45)
+        const int kz = (int)((unsigned)i % (unsigned)a.g.K);
+        wgt = (kz == 0 || kz == a.g.K - 1) ? 1.0 : 2.0;
+      }
 #pragma unroll
       for (int j = 0; j < d; ++j) {
+        const cplx u = st[(NG + j) * CH + tid];
         cplx o = rsub(Gv[j], rmul(kv.k[j], kd));
-        o = rsub(o, rmul(nuk2, st[(NG + j) * CH + tid]));
+        o = rsub(o, rmul(nuk2, u));
         a.f[j * n + i] = o;
+        if constexpr (DIAG) {  // same op order as k_reduce_tma's diagnostics
+          const double m2 = DADD(DMUL(u.x, u.x), DMUL(u.y, u.y));
+          e_acc = DADD(e_acc, DMUL(wgt, m2));
+          ep_acc = DADD(ep_acc, DMUL(wgt, DADD(DMUL(u.x, o.x), DMUL(u.y, o.y))));
+          z_acc = DADD(z_acc, DMUL(DMUL(wgt, kv.k2), m2));
+        }
         if constexpr (NTC >= 0) {
-          cplx acc = st[(NG + NY + j) * CH + tid];
+          cplx acc = DIAG ? u : st[(NG + NY + j) * CH + tid];
 #pragma unroll
           for (int t = 0; t < (NTC < 0 ? 0 : NTC); ++t)
-            acc = radd(acc, rmul(a.c[t], st[(NG + NY + d + t * d + j) * CH + tid]));
+            acc = radd(acc, rmul(a.c[t], st[(NG + NY + (DIAG ? 0 : d) + t * d + j) * CH + tid]));
           a.ynext[j * n + i] = radd(acc, rmul(a.cself, o));
         }
       }
@@ -210,6 +225,25 @@ __global__ void __launch_bounds__(NTC < 0 ? SRK_PT_CH : SRK_PC_CH) k_project_tma
     }
     __syncthreads();  // stage b consumed
     issue(k + 2LL * G, b);
+  }
+  if constexpr (DIAG) {  // fixed-order block reduction -> partials (deterministic)
+    __shared__ double red[3][CH / 32];
+    const int lane = tid & 31, warp = tid >> 5;
+    double v[3] = {e_acc, ep_acc, z_acc};
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v[q] += __shfl_down_sync(0xffffffffu, v[q], off);
+      if (lane == 0) red[q][warp] = v[q];
+    }
+    __syncthreads();
+    if (tid < SRK_NQ) {
+      double s = 0.0;
+      const int q = tid == 4 ? 0 : (tid == 5 ? 1 : (tid == 8 ? 2 : -1));
+      if (q >= 0)
+        for (int w = 0; w < CH / 32; ++w) s += red[q][w];
+      a.partial[tid * gridDim.x + blockIdx.x] = s;
+    }
   }
 }
 
@@ -571,22 +605,33 @@ __global__ void k_band_scale(cplx* __restrict__ u, const long long* __restrict__
   *p = rmul(gamma, *p);
 }
 
-template <int DIMS, bool DENS, int NTC = -1>
-static void launch_project_tma(const ProjArgs& a, cudaStream_t st) {
+template <int DIMS, bool DENS, int NTC = -1, bool DIAG = false>
+static int launch_project_tma(const ProjArgs& a, cudaStream_t st) {
   constexpr int CH = NTC < 0 ? SRK_PT_CH : SRK_PC_CH;
-  constexpr int NS = (DENS ? 2 * DIMS : DIMS) + (DENS ? DIMS + 1 : DIMS) + (NTC < 0 ? 0 : DIMS * (NTC + 1));
+  constexpr int NS = (DENS ? 2 * DIMS : DIMS) + (DENS ? DIMS + 1 : DIMS) +
+                     (NTC < 0 ? 0 : (DIAG ? 0 : DIMS) + DIMS * NTC);
   const int smem = 2 * NS * CH * 16;
   static int blocks = 0;
   if (!blocks) {
-    cudaFuncSetAttribute(k_project_tma<DIMS, DENS, NTC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_project_tma<DIMS, DENS, NTC, DIAG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int per_sm = 0, dev = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_project_tma<DIMS, DENS, NTC>, CH, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_project_tma<DIMS, DENS, NTC, DIAG>, CH, smem);
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     blocks = std::max(1, per_sm) * sms;
+    if (DIAG) blocks = std::min(blocks, SRK_RED_BLOCKS);  // partials buffer
   }
   const long long nch = (a.modes + CH - 1) / CH;
-  k_project_tma<DIMS, DENS, NTC><<<(int)std::min<long long>(blocks, nch), CH, smem, st>>>(a);
+  const int grid = (int)std::min<long long>(blocks, nch);
+  k_project_tma<DIMS, DENS, NTC, DIAG><<<grid, CH, smem, st>>>(a);
+  return grid;
+}
+
+bool srk_launch_project_refresh(const ProjArgs& a, double* out, cudaStream_t st) {
+  if (a.g.dims != 3 || a.density || a.modes >= (1LL << 32) || !a.partial) return false;
+  const int grid = launch_project_tma<3, false, 0, true>(a, st);
+  k_finalize<<<1, 256, 0, st>>>(a.partial, grid, out);
+  return true;
 }
 
 // K6 with the next stage input formed in the same pass (3D NS, modes < 2^32,

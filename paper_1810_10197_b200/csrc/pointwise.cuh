@@ -30,6 +30,10 @@ struct ProjArgs {
   int nt;
   double cself;
   cplx* ynext;
+  // k_project_tma<3, false, 0, true> (srk_rhs_refresh): ybase is the state itself
+  // (not streamed) and the block partials of E, eps, Z over the velocity
+  // components go to partial[q * gridDim.x + block] (q = 4, 5, 8; others 0)
+  double* partial;
 };
 
 struct CombArgs {
@@ -67,6 +71,9 @@ void srk_launch_combine(const CombArgs& a, cudaStream_t st);
 void srk_launch_reduce(const RedArgs& a, double* out, cudaStream_t st);
 void srk_launch_band_energy(const cplx* u, const long long* idx, const double* w, int nb, int ncomp,
                             long long modes, double* out, cudaStream_t st);
+// srk_rhs_refresh: K6 + ynext = y + cself f + the (E, eps, Z) sums of (y, f);
+// returns false when the fused kernel does not apply (2D, Boussinesq, >= 2^32 modes)
+bool srk_launch_project_refresh(const ProjArgs& a, double* out, cudaStream_t st);
 void srk_launch_store_mapped(const double* src, double* dst, int n, cudaStream_t st);
 void srk_launch_band_scale(cplx* u, const long long* idx, int nb, int ncomp, long long modes, double gamma,
                            cudaStream_t st);

@@ -691,6 +691,7 @@ struct CombSpec {
   double c[SRK_MAX_TERMS];
   double cself;
   cplx* ynext;
+  double* diag_out;  // srk_rhs_refresh: (E, eps, Z) sums of (y, f) -> out[4], [5], [8]
 };
 int rhs_impl(srk_plan* p, const void* y_, void* f_, double nu, double ri, double re_pr, void* stream,
              const CombSpec* cs);
@@ -716,6 +717,25 @@ int srk_rhs_combine(srk_plan* p, const void* y, void* f, double nu, double ri, d
   }
   cs.cself = coef_self;
   cs.ynext = (cplx*)ynext;
+  return rhs_impl(p, y, f, nu, ri, re_pr, stream, &cs);
+}
+
+int srk_rhs_refresh(srk_plan* p, const void* y, void* f, double nu, double ri, double re_pr, double coef_self,
+                    void* ynext, double* diag_out, void* stream) {
+  if (!p) return fail(SRK_ERR_INVALID, "null plan");
+  if (p->dims != 3 || p->density || p->nranks != 1)
+    return fail(SRK_ERR_UNSUPPORTED, "srk_rhs_refresh: 3D NS on an unsplit plan only");
+  if (!ynext || !diag_out || ynext == y || ynext == f) return fail(SRK_ERR_INVALID, "srk_rhs_refresh: bad outputs");
+  if (!p->partial) {
+    cudaError_t err = cudaMalloc(&p->partial, sizeof(double) * SRK_NQ * SRK_RED_BLOCKS);
+    if (err != cudaSuccess) return fail(SRK_ERR_CUDA, std::string("cudaMalloc(partials): ") + cudaGetErrorString(err));
+  }
+  CombSpec cs;
+  memset(&cs, 0, sizeof(cs));
+  cs.yb = (const cplx*)y;
+  cs.cself = coef_self;
+  cs.ynext = (cplx*)ynext;
+  cs.diag_out = diag_out;
   return rhs_impl(p, y, f, nu, ri, re_pr, stream, &cs);
 }
 
@@ -840,6 +860,15 @@ int rhs_impl(srk_plan* p, const void* y_, void* f_, double nu, double ri, double
   pa.ri = ri;
   pa.re_pr = re_pr;
   bool fused = false;
+  if (cs && cs->diag_out) {  // srk_rhs_refresh (ybase == y, no earlier terms)
+    pa.partial = p->partial;
+    pa.cself = cs->cself;
+    pa.ynext = cs->ynext;
+    if (!srk_launch_project_refresh(pa, cs->diag_out, st)) return fail(SRK_ERR_UNSUPPORTED, "srk_rhs_refresh: 3D NS only");
+    p->last_launches += 2;
+    if (p->timing && p->nev < 16) cudaEventRecord(p->ev[p->nev++], st);
+    return check_launch("k_project_tma (refresh)");
+  }
   if (cs && !getenv("SRK_NO_PCOMB")) {
     pa.yb = cs->yb;
     pa.nt = cs->nt;

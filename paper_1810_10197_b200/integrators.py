@@ -175,7 +175,7 @@ def _as_dev_fn(f):
 _FUSED_MAX_TERMS = 6
 
 
-def run_stages(f, y, t, h, pair, first_stage=None, on_y_new=None):
+def run_stages(f, y, t, h, pair, first_stage=None, on_y_new=None, second_input=None):
     """Stage loop of integrators.py:322-339 on the device.
 
     Returns (stages, y_new, evals).  For FSAL pairs y_new is the last stage's
@@ -188,6 +188,10 @@ def run_stages(f, y, t, h, pair, first_stage=None, on_y_new=None):
     ``on_y_new(y_new)`` is called once y_new is queued: for FSAL pairs before the
     last stage's RHS (whose input it is), so a consumer such as
     ``HostMirror.push`` overlaps that evaluation.
+
+    ``second_input``: the stage-2 input y + h a21 F1 already formed together with
+    ``first_stage`` (FlowRHS.refresh); used as is (bitwise what the combine
+    would give) -- the caller guarantees it was formed with this h.
     """
     A, b, c, s = pair.A, pair.b, pair.c, pair.s
     fused = getattr(f, "eval_combine", None)
@@ -203,6 +207,8 @@ def run_stages(f, y, t, h, pair, first_stage=None, on_y_new=None):
             xi = y
         elif pending is not None:
             xi, pending = pending, None
+        elif i == 1 and second_input is not None and stages[0] is first_stage:
+            xi = second_input
         else:
             xi = combine(y, [(h * A[i, j], stages[j]) for j in range(i) if A[i, j] != 0.0])
         if i > 0:

@@ -99,6 +99,36 @@ class FlowRHS:
         _native.count(pl.lib.srk_rhs_launch_count(pl.h))
         return f, ynext
 
+    def refresh(self, t, fields, coef_self):
+        """The after-accept refresh (simulation.py:165-182) fused with the next
+        step's first stage sum: returns ``(f, y + coef_self f, sums)`` with ``f =
+        self(t, y)`` and ``sums`` the 9 reduce_sums values of (y, f) for the
+        diagnostics record (entries 4, 5, 8 = E, eps, Z sums; diag_from_sums).
+        One projection pass on the 3D NS path (srk_rhs_refresh); elsewhere the
+        separate calls."""
+        from .diagnostics import reduce_sums
+        from .integrators import combine
+
+        y, _ = to_device(fields, torch.complex128)
+        g = self.grid
+        if g.dims != 3 or self.density:
+            f = self(t, y)
+            q = reduce_sums(g, y, fl=f, flags=2, ncomp=min(y.shape[0], g.dims), host=True).tolist()
+            return f, combine(y, [(coef_self, f)]), q
+        f = torch.empty_like(y)
+        ynext = torch.empty_like(y)
+        p = self.params
+        pl = self.plan
+        out = _native.host_result(9)
+        _native.check(pl.lib.srk_rhs_refresh(pl.bind(), _native.ptr(y), _native.ptr(f), 1.0 / p.reynolds,
+                                             float(p.richardson), float(p.reynolds) * float(p.prandtl),
+                                             float(coef_self), _native.ptr(ynext), _native.ptr(out),
+                                             _native.stream_ptr()), "srk_rhs_refresh")
+        self.calls += 1
+        _native.count(pl.lib.srk_rhs_launch_count(pl.h))
+        _native.wait_stream_point()
+        return f, ynext, out.clone().tolist()
+
     def launches_per_call(self):
         return int(self.plan.lib.srk_rhs_launch_count(self.plan.h))
 

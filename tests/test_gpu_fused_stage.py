@@ -105,3 +105,38 @@ def test_forcing_with_step_energy_sum_is_bitwise_the_full_pass():
     gb = srk.apply_forcing(b, g, 0.5, 2.0, energy_sum=out.diag_sums[4])
     assert ga == gb
     assert torch.equal(a, b)
+
+
+def test_refresh_matches_separate_calls():
+    """srk_rhs_refresh: f and y + c f bitwise the separate calls, the diagnostics
+    sums equal to srk_step_reduce's (different fixed summation order)."""
+    from paper_1810_10197_b200.diagnostics import reduce_sums
+    from paper_1810_10197_b200.integrators import combine
+
+    g = srk.Grid((64, 64, 64))
+    rhs = srk.FlowRHS(g, srk.PhysParams(700.0))
+    y = srk.hit_init(g, srk.ProblemSpec("hit", a=4.0, energy=0.5, seed=9)).fields
+    c = 1e-3 * 0.5
+    f, y2, q = rhs.refresh(0.0, y, c)
+    f_ref = rhs(0.0, y)
+    assert torch.equal(f, f_ref)
+    assert torch.equal(y2, combine(y, [(c, f_ref)]))
+    q_ref = reduce_sums(g, y, fl=f_ref, flags=2, ncomp=3, host=True).tolist()
+    for k in (4, 5, 8):
+        assert abs(q[k] - q_ref[k]) <= 1e-13 * abs(q_ref[k])
+    assert all(q[k] == 0.0 for k in (0, 1, 2, 3, 6, 7))
+
+
+def test_second_input_is_bitwise_the_stage_sum():
+    """adaptive_advance(second_input=(h, y + h a21 F1)) == the unfused first stage sum."""
+    g = srk.Grid((32, 32, 32))
+    rhs = srk.FlowRHS(g, srk.PhysParams(900.0))
+    pair = srk.make_bs5()
+    cfg = srk.ControllerConfig(tol_abs=1e-6, tol_rel=1e-6)
+    y = srk.hit_init(g, srk.ProblemSpec("hit", a=4.0, energy=0.5, seed=2)).fields
+    h = 2e-3
+    f, y2, _ = rhs.refresh(0.0, y, h * float(pair.A[1, 0]))
+    a = srk.adaptive_advance(y, 0.0, pair, srk.ControllerState(h=h), cfg, rhs, first_stage=f, grid=g,
+                             second_input=(h, y2))
+    b = srk.adaptive_advance(y, 0.0, pair, srk.ControllerState(h=h), cfg, rhs, first_stage=f, grid=g)
+    assert torch.equal(a.y_new, b.y_new) and a.h_next == b.h_next and a.rhs_evals == b.rhs_evals
