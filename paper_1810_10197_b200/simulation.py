@@ -186,6 +186,7 @@ class _Driver:
             self.evals += 1
         self.records = []
         self.errs = []
+        self.second_input = self.refresh_sums = None
         out_dir = getattr(config, "output_dir", None)
         self.out_dir = Path(out_dir) if out_dir else None
         if self.out_dir is not None:
@@ -222,9 +223,13 @@ class _Driver:
         self.records.append(DiagnosticsRecord(t=self.t, h=h, e_kin=e, eps=eps, rhs_evals=self.evals,
                                               rejections=self.rejections, enstrophy=z))
 
-    def after_accept(self, last_stage, fsal_ok, energy_sum=None):
+    def after_accept(self, last_stage, fsal_ok, energy_sum=None, next_coef=None):
         """simulation.py:165-182. Returns True when f_now is the FSAL stage.
-        energy_sum: sum_w |u|^2 of the new state from the step reduction, if known."""
+        energy_sum: sum_w |u|^2 of the new state from the step reduction, if known.
+        next_coef=(h, h a21): when f_now has to be recomputed, do it with
+        FlowRHS.refresh -- the same f_now, plus the diagnostics sums of the new
+        state (``refresh_sums``) and the next attempt's stage-2 input for step
+        size h (``second_input``) from the same pass."""
         cfg = self.config
         forced = False
         if cfg.forcing:
@@ -232,10 +237,17 @@ class _Driver:
                           energy_sum=energy_sum)
             forced = True
         self.steps += 1
+        self.second_input = self.refresh_sums = None
         if fsal_ok and not forced and last_stage is not None:
             self.f_now = last_stage
             return True
-        self.f_now = self.rhs(self.t, self.y)
+        if next_coef is not None:
+            self.f_now, y2, sums = self.rhs.refresh(self.t, self.y, next_coef[1])
+            if not all(np.isfinite(sums[k]) for k in (4, 5, 8)):
+                raise NonFiniteStateError(f"non-finite state at t={self.t}")
+            self.second_input, self.refresh_sums = (next_coef[0], y2), sums
+        else:
+            self.f_now = self.rhs(self.t, self.y)
         self.evals += 1
         return False
 
@@ -327,6 +339,7 @@ def _run_adaptive(drv, max_steps=None):
     pair = make_pair(cfg.integrator)
     t_end = cfg.t_end
     ctrl = ControllerState(h=drv.h_ctrl, prev_rejected=drv.prev_rejected, rejections=drv.rejections)
+    a21 = float(pair.A[1, 0])
     drv.record(drv.h_ctrl)
     n = 0
     while drv.t < t_end and (max_steps is None or n < max_steps):
@@ -336,7 +349,7 @@ def _run_adaptive(drv, max_steps=None):
         if clamped:
             ctrl.h = remaining
         out = adaptive_advance(drv.y, drv.t, pair, ctrl, cfg.controller, drv.rhs, first_stage=drv.f_now,
-                               grid=drv.grid)
+                               grid=drv.grid, second_input=drv.second_input)
         drv.evals += out.rhs_evals
         drv.rejections += out.rejections
         drv.y = out.y_new
@@ -351,8 +364,9 @@ def _run_adaptive(drv, max_steps=None):
         drv.prev_rejected = ctrl.prev_rejected
         drv.errs.append(out.errs)
         fsal_used = drv.after_accept(out.last_stage, fsal_ok=pair.fsal,
-                                     energy_sum=out.diag_sums[4] if out.diag_sums is not None else None)
-        drv.record(out.h_used, sums=out.diag_sums if fsal_used else None)
+                                     energy_sum=out.diag_sums[4] if out.diag_sums is not None else None,
+                                     next_coef=(ctrl.h, ctrl.h * a21))
+        drv.record(out.h_used, sums=out.diag_sums if fsal_used else drv.refresh_sums)
         drv.maybe_checkpoint()
         n += 1
 
