@@ -452,7 +452,8 @@ __global__ void __launch_bounds__(SRK_RT_CH) k_reduce_tma(const RedArgs a) {
     const bool vel = c < a.dvel;
     unsigned bytes = cnt * 16u;
     if (a.do_norm) bytes += cnt * 16u * (1u + NT);
-    if (a.do_diag && vel) bytes += cnt * 16u;
+    const bool fl_own = a.do_diag && vel && !(a.do_norm && a.fl_term >= 0);  // fl needs its own stream
+    if (fl_own) bytes += cnt * 16u;
     mbar_expect_tx(&mb[b], bytes);
     bulk_g2s(st, a.y1 + off, cnt * 16u, &mb[b]);
     if (a.do_norm) {
@@ -460,7 +461,7 @@ __global__ void __launch_bounds__(SRK_RT_CH) k_reduce_tma(const RedArgs a) {
 #pragma unroll
       for (int j = 0; j < NT; ++j) bulk_g2s(st + (2 + j) * CH, a.F[j] + off, cnt * 16u, &mb[b]);
     }
-    if (a.do_diag && vel) bulk_g2s(st + (2 + NT) * CH, a.fl + off, cnt * 16u, &mb[b]);
+    if (fl_own) bulk_g2s(st + (2 + NT) * CH, a.fl + off, cnt * 16u, &mb[b]);
   };
   issue(blockIdx.x, 0);
   issue(blockIdx.x + G, 1);
@@ -500,7 +501,8 @@ __global__ void __launch_bounds__(SRK_RT_CH) k_reduce_tma(const RedArgs a) {
         const double w = (kz == 0 || kz == a.K - 1) ? 1.0 : 2.0;
         const double m2 = DADD(DMUL(y1.x, y1.x), DMUL(y1.y, y1.y));
         acc[4] = DADD(acc[4], DMUL(w, m2));
-        const cplx fl = st[(2 + NT) * CH + tid];
+        const int fslot = (a.do_norm && a.fl_term >= 0) ? 2 + a.fl_term : 2 + NT;
+        const cplx fl = st[fslot * CH + tid];
         acc[5] = DADD(acc[5], DMUL(w, DADD(DMUL(y1.x, fl.x), DMUL(y1.y, fl.y))));
         const double k2 = k2_at(i, a.g, small);
         acc[8] = DADD(acc[8], DMUL(DMUL(w, k2), m2));

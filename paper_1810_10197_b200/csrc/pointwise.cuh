@@ -53,6 +53,7 @@ struct RedArgs {
   double c[SRK_MAX_TERMS];  // h*(b - b_hat) for the error vector
   int nt;
   const cplx* fl;  // tendency at y1 (diag)
+  int fl_term;     // >= 0: fl is F[fl_term] (the FSAL stage): streamed once, read from that slot
   int ncomp;
   int dvel;
   long long modes;

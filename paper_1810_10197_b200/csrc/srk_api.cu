@@ -1000,6 +1000,9 @@ int srk_step_reduce(srk_plan* p, const void* y0, const void* y1, int nterms, con
     a.c[j] = coef[j];
   }
   a.fl = (const cplx*)fl;
+  a.fl_term = -1;
+  for (int j = 0; j < a.nt; ++j)
+    if (a.F[j] == a.fl) a.fl_term = j;  // the FSAL stage is also an error term: stream it once
   a.ncomp = ncomp;
   a.dvel = std::min(p->dims, ncomp);
   a.modes = p->modes;
