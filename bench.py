@@ -390,11 +390,12 @@ def run_native(args, rank, world, local_rank):
         e2e = {"value": e2t.item() / t2.item(), "unit": "stages/s",
                "h2d_bytes_per_step": (mirror.h2d_bytes - b_in0) // n_e2e,
                "d2h_bytes_per_step": (mirror.d2h_bytes - b_out0) // n_e2e + 9 * 8,
-               "path": "per step: y host->device (pinned HostMirror), cached tendency rhs(t, y) + diagnostics "
-                       "record, adaptive_advance (BS5) + forcing through the Python API, y_new device->host "
+               "path": "per step: y host->device (pinned HostMirror), cached tendency + diagnostics record + "
+                       "first stage sum (FlowRHS.refresh), adaptive_advance (BS5) + forcing through the Python "
+                       "API, y_new device->host "
                        "(every attempt's y_new, issued before its FSAL stage, the next step's host->device behind it; "
                        "forcing band planes re-sent both ways); "
-                       "same RHS count as the device-resident step"}
+                       "same RHS count as the device-resident step; bytes include every attempt's copies"}
 
     if rank != 0:
         return
