@@ -183,6 +183,24 @@ def test_rhs_512_bitwise_repeatable(state):
     assert torch.equal(f, f2)
 
 
+def test_refresh_512_is_bitwise_the_separate_calls(state):
+    """srk_rhs_refresh at the config-5 grid: f bitwise the plain RHS, y + c f bitwise
+    the stage-sum kernel, the diagnostics sums equal to the step reduction's."""
+    from paper_1810_10197_b200.diagnostics import reduce_sums
+    from paper_1810_10197_b200.integrators import combine
+
+    g, u, f = state
+    rhs = srk.FlowRHS(g, srk.PhysParams(RE))
+    c = 1.7e-3 * 0.2
+    f2, y2, q = rhs.refresh(0.0, u, c)
+    assert torch.equal(f2, f)
+    assert torch.equal(y2, combine(u, [(c, f)]))
+    del y2, f2
+    q_ref = reduce_sums(g, u, fl=f, flags=2, ncomp=3, host=True).tolist()
+    for k in (4, 5, 8):
+        assert abs(q[k] - q_ref[k]) <= 1e-12 * abs(q_ref[k]), (k, q[k], q_ref[k])
+
+
 @pytest.mark.parametrize("shape,lengths", [((64, 128, 512), (2 * math.pi, 3.0, 5.0)),
                                            ((128, 32, 512), (1.0, 2 * math.pi, 2 * math.pi))])
 def test_rhs_anisotropic_z512_matches_cufft_restatement(shape, lengths):
