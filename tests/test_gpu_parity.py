@@ -528,6 +528,41 @@ def test_slab_peer_stores_emulated_ranks_match_single_gpu(P, shape):
         assert torch.equal(torch.cat([s1[q][r * blk:(r + 1) * blk] for q in range(P)]), r1[r])
 
 
+def test_slab_peer_stores_boussinesq_emulated_ranks():
+    """Peer-store exchange with a density field (3D Boussinesq: 6 K1 signals, 6 products)."""
+    from paper_1810_10197_b200.slab import CudaSlabBackend, scatter_slab, slab_geometry
+
+    P, shape = 2, (32, 32, 32)
+    g = srk.Grid(shape)
+    params = srk.PhysParams(200.0, 1.0, 1.0)
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    y = torch.randn((4,) + g.kshape, dtype=torch.complex128, device="cuda", generator=gen)
+    y[:3] = srk.leray_project(y[:3], g)
+    srk.symmetrize_real_planes(y, g)
+    srk.zero_nyquist(y, g)
+    f_ref = srk.FlowRHS(g, params, density=True)(0.0, y)
+    geo = slab_geometry(g, P, density=True)
+    K = geo["K"]
+    backs = [CudaSlabBackend(g, params, r, P, density=True) for r in range(P)]
+    ys = [scatter_slab(y, r, P) for r in range(P)]
+    r1 = [b.empty(geo["send1"]) for b in backs]
+    r2 = [b.empty(geo["send2"]) for b in backs]
+    for b in backs:
+        b.set_peers([t.data_ptr() for t in r1], [t.data_ptr() for t in r2])
+    for r in range(P):
+        backs[r].forward_kz_peer(ys[r], 0, K)
+    for r in range(P):
+        backs[r].inverse_y_kz(r1[r], 0, K)
+        backs[r].zpass()
+        backs[r].forward_y_kz_peer(0, K)
+    fs = [torch.empty_like(ys[r]) for r in range(P)]
+    for r in range(P):
+        backs[r].forward_x_kz(r2[r], 0, K)
+        backs[r].project(ys[r], fs[r])
+    f = torch.cat(fs, dim=2)
+    assert float(torch.linalg.norm(f - f_ref) / torch.linalg.norm(f_ref)) <= 1e-13
+
+
 def test_slab_flowrhs_peer_world1_matches_flowrhs():
     from paper_1810_10197_b200.slab import SlabFlowRHS
 
