@@ -73,3 +73,66 @@ def test_peer_store_exchange_across_processes(tmp_path):
     f = np.concatenate([np.load(tmp_path / f"f{r}.npy") for r in range(world)], axis=2)
     ref = np.load(tmp_path / "ref.npy")
     assert np.linalg.norm(f - ref) / np.linalg.norm(ref) <= 1e-14
+
+
+def _bs5_worker(rank, world, port, out_dir):
+    """10 adaptive BS5 steps of a y-slab-decomposed 64^3 HIT over two processes:
+    peer-store exchanges, rank-order sums over gloo, identical accept/reject
+    decisions on both ranks."""
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    import paper_1810_10197_b200 as srk
+    from paper_1810_10197_b200.slab import SlabFlowRHS, dist_sum_in_rank_order, scatter_slab
+
+    g = srk.Grid(SHAPE)
+    params = srk.PhysParams(500.0)
+    y = srk.hit_init(g, srk.ProblemSpec("hit", a=4.0, energy=0.5, seed=11)).fields
+
+    def barrier():
+        torch.cuda.synchronize()
+        dist.barrier()
+
+    rhs = SlabFlowRHS(g, params, rank, world, peer=True, barrier=barrier)
+    red = dist_sum_in_rank_order()
+    ys = scatter_slab(y, rank, world)
+    pair, cfg = srk.make_bs5(), srk.ControllerConfig(tol_abs=1e-6, tol_rel=1e-6)
+    st = srk.ControllerState(h=1e-3)
+    t, f, hs = 0.0, rhs(0.0, ys), []
+    for _ in range(10):
+        out = srk.adaptive_advance(ys, t, pair, st, cfg, rhs, first_stage=f, grid=g, allreduce=red,
+                                   plan=rhs.backend.h)
+        ys, t, f = out.y_new, out.t_new, out.last_stage
+        hs.append(out.h_used)
+    torch.cuda.synchronize()
+    np.save(os.path.join(out_dir, f"y{rank}.npy"), ys.cpu().numpy())
+    np.save(os.path.join(out_dir, f"h{rank}.npy"), np.array(hs))
+    rhs.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_peer_slab_bs5_run_across_processes_matches_single_gpu(tmp_path):
+    import paper_1810_10197_b200 as srk
+
+    world = 2
+    mp.start_processes(_bs5_worker, args=(world, random.randint(20000, 40000), str(tmp_path)), nprocs=world,
+                       start_method="spawn", join=True)
+    g = srk.Grid(SHAPE)
+    y = srk.hit_init(g, srk.ProblemSpec("hit", a=4.0, energy=0.5, seed=11)).fields
+    rhs = srk.FlowRHS(g, srk.PhysParams(500.0))
+    pair, cfg = srk.make_bs5(), srk.ControllerConfig(tol_abs=1e-6, tol_rel=1e-6)
+    st = srk.ControllerState(h=1e-3)
+    t, f, hs = 0.0, rhs(0.0, y), []
+    for _ in range(10):
+        out = srk.adaptive_advance(y, t, pair, st, cfg, rhs, first_stage=f, grid=g)
+        y, t, f = out.y_new, out.t_new, out.last_stage
+        hs.append(out.h_used)
+    h0, h1 = np.load(tmp_path / "h0.npy"), np.load(tmp_path / "h1.npy")
+    assert np.array_equal(h0, h1)  # both ranks took the same decisions
+    np.testing.assert_allclose(h0, np.array(hs), rtol=1e-12)
+    ys = np.concatenate([np.load(tmp_path / f"y{r}.npy") for r in range(world)], axis=2)
+    yr = y.cpu().numpy()
+    assert np.linalg.norm(ys - yr) / np.linalg.norm(yr) <= 1e-12
