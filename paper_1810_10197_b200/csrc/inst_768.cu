@@ -24,6 +24,14 @@ void srk_reg_768(KEntry* t) {
 #ifndef SRK_ZPAIR
   // one pencil per CTA, forward suffix (8, 24): K3 9.02 -> 8.53 ms at 512^3
   // (forward (16, 12) 8.67, (12, 16) 8.84, (24, 8) 8.64; inverse (8, 24) 8.69)
+#if defined(SRK_K3E12) && SRK_K3E12 == 1
+  SRK_NS3P12(768, (12, 4, 4), (8, 24))
+#elif defined(SRK_K3E12) && SRK_K3E12 == 2
+  SRK_NS3P12(768, (4, 4, 12), (8, 24))
+#elif defined(SRK_K3E12) && SRK_K3E12 == 3
+  SRK_NS3P12(768, (12, 4, 4), (16, 12))
+#else
   SRK_NS3P(768, (24, 8), (8, 24))
+#endif
 #endif
 }

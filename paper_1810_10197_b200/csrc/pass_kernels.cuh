@@ -1065,14 +1065,19 @@ struct LoopStageZ {
 #ifndef SRK_ZP1_MINB
 #define SRK_ZP1_MINB 5  // CTAs per SM the register budget targets (shared memory allows 5)
 #endif
+#ifndef SRK_ZP1_MINB12
+#define SRK_ZP1_MINB12 5  // CTAs per SM for the E = 12 (M/4-thread) variant
+#endif
 template <int M, class L, class EngI, int... FR>
-__global__ void __launch_bounds__(M / 8, (M <= 768 ? SRK_ZP1_MINB : 2)) k_zpass_ns3p(const ZArgs a, int, int) {
+__global__ void __launch_bounds__(EngI::NT, (EngI::NT == M / 8 ? (M <= 768 ? SRK_ZP1_MINB : 2) : SRK_ZP1_MINB12))
+    k_zpass_ns3p(const ZArgs a, int, int) {
   extern __shared__ __align__(16) cplx smraw[];
   cplx* const sm = smraw + EngI::TWN;  // [twiddle table][tile]
   const cplx* const twp = smraw;
   tw_fill<M>(smraw, a.tw);
-  constexpr int S = 3, NT = M / 8, K = M / 3 + 1, Q = M / 4;
-  static_assert(EngI::NT == NT, "inverse prefix must use M/8 threads");
+  // NT = M/8 (E = 24: two fused-middle rows per thread) or M/4 (E = 12: one)
+  constexpr int S = 3, NT = EngI::NT, K = M / 3 + 1, Q = M / 4, RPT = Q / NT;
+  static_assert(NT == M / 8 || NT == M / 4, "inverse prefix must use M/8 or M/4 threads");
   static_assert(L::C == 3, "three tile columns");
   const int pen = blockIdx.x;
   const int tid = threadIdx.x;
@@ -1122,9 +1127,9 @@ __global__ void __launch_bounds__(M / 8, (M <= 768 ? SRK_ZP1_MINB : 2)) k_zpass_
   SRK_TS(2)
   // ---- fused: last inverse radix-4 | u x w | first forward radix-4; rows j, j + NT ----
   {
-    cplx v[2][S][4];
+    cplx v[RPT][S][4];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < RPT; ++h) {
       const int j = tid + h * NT;
 #pragma unroll
       for (int c = 0; c < S; ++c) {
@@ -1140,7 +1145,7 @@ __global__ void __launch_bounds__(M / 8, (M <= 768 ? SRK_ZP1_MINB : 2)) k_zpass_
     }
     __syncthreads();
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < RPT; ++h) {
       const int j = tid + h * NT;
       cplx w[4];
 #pragma unroll
