@@ -91,7 +91,8 @@ int srk_rhs_combine(srk_plan* plan, const void* y, void* f, double nu, double ri
  *   diag_out[8] = sum w |k|^2 |y|^2, other entries 0 -- the srk_step_reduce
  *   (flags = 2) layout, fixed-order (deterministic) sums; diag_out may be
  *   mapped pinned host memory.
- * One pass of the projection kernel (y is read once); 3D NS, unsplit plans. */
+ * One pass of the projection kernel (y is read once); 2D / 3D, NS or
+ * Boussinesq (E, eps, Z over the velocity components), unsplit plans. */
 int srk_rhs_refresh(srk_plan* plan, const void* y, void* f, double nu, double ri, double re_pr, double coef_self,
                     void* ynext, double* diag_out, void* stream);
 

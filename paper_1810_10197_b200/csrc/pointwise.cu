@@ -106,7 +106,7 @@ __device__ __forceinline__ KVec kvec32(unsigned idx, const GeomArgs& g) {
 // elected thread, mbarrier completion); f is stored straight from registers.
 // Same arithmetic as k_project.
 //
-// NTC >= 0 (3D NS): the next RK stage input is formed in the same pass
+// NTC >= 0 (2D / 3D, NS or Boussinesq): the next RK stage input is formed in the same pass
 // (integrators.py:327-339 / :336-339):
 //   ynext = ybase + sum_{t < NTC} c_t F_t + cself * f
 // ascending in the stage index with f = the tendency just computed (the last,
@@ -118,17 +118,31 @@ __device__ __forceinline__ KVec kvec32(unsigned idx, const GeomArgs& g) {
 #ifndef SRK_PC_CH
 #define SRK_PC_CH 256  // modes per chunk (and threads) of the fused K6 + stage-sum kernel; ncu: 128 -> 256 is 1-7% faster
 #endif
+// shared-memory components streamed per mode: G, state, and (fused stage sum)
+// ybase + the NTC earlier stages, each with the state's component count
+template <int DIMS, bool DENS, int NTC, bool DIAG>
+constexpr int proj_streams() {
+  return (DENS ? 2 * DIMS : DIMS) + (DENS ? DIMS + 1 : DIMS) +
+         (NTC < 0 ? 0 : ((DIAG ? 0 : 1) + NTC) * (DENS ? DIMS + 1 : DIMS));
+}
+// modes per chunk: 256, or 128 when a 256-mode two-stage ring would not fit
+// the 227 KB opt-in shared memory (3D Boussinesq with 5-6 earlier stages)
+template <int DIMS, bool DENS, int NTC, bool DIAG>
+constexpr int proj_chunk() {
+  return NTC < 0 ? SRK_PT_CH
+                 : (2 * proj_streams<DIMS, DENS, NTC, DIAG>() * SRK_PC_CH * 16 <= 227 * 1024 - 64 ? SRK_PC_CH : 128);
+}
 template <int DIMS, bool DENS, int NTC = -1, bool DIAG = false>
-__global__ void __launch_bounds__(NTC < 0 ? SRK_PT_CH : SRK_PC_CH) k_project_tma(const ProjArgs a) {
+__global__ void __launch_bounds__(proj_chunk<DIMS, DENS, NTC, DIAG>()) k_project_tma(const ProjArgs a) {
   extern __shared__ __align__(128) cplx psm[];
-  constexpr int CH = NTC < 0 ? SRK_PT_CH : SRK_PC_CH;
+  constexpr int CH = proj_chunk<DIMS, DENS, NTC, DIAG>();
   constexpr int d = DIMS;
   constexpr int NG = DENS ? 2 * d : d;  // G components
   constexpr int NY = DENS ? d + 1 : d;  // state components
-  // ybase + F_t components (DIAG: ybase is the state, already in the ring)
-  constexpr int NC = NTC < 0 ? 0 : (DIAG ? 0 : d) + d * NTC;
+  // ybase + F_t components, NY each (DIAG: ybase is the state, already in the ring)
+  constexpr int NC = NTC < 0 ? 0 : ((DIAG ? 0 : 1) + NTC) * NY;
   constexpr int NS = NG + NY + NC;
-  static_assert(NTC < 0 || (DIMS == 3 && !DENS), "fused stage combination: 3D NS only");
+  static_assert(NS == proj_streams<DIMS, DENS, NTC, DIAG>(), "stream count");
   static_assert(!DIAG || NTC == 0, "refresh: the state's own next-stage input only");
   double e_acc = 0.0, ep_acc = 0.0, z_acc = 0.0;  // DIAG: E, eps, Z partial sums of this thread
   __shared__ __align__(8) unsigned long long mb[2];
@@ -154,12 +168,12 @@ __global__ void __launch_bounds__(NTC < 0 ? SRK_PT_CH : SRK_PC_CH) k_project_tma
     for (int j = 0; j < NY; ++j) bulk_g2s(st + (NG + j) * CH, a.y + j * n + i0, cnt * 16u, &mb[b]);
     if constexpr (NTC >= 0 && !DIAG) {
 #pragma unroll
-      for (int j = 0; j < d; ++j) bulk_g2s(st + (NG + NY + j) * CH, a.yb + j * n + i0, cnt * 16u, &mb[b]);
+      for (int j = 0; j < NY; ++j) bulk_g2s(st + (NG + NY + j) * CH, a.yb + j * n + i0, cnt * 16u, &mb[b]);
 #pragma unroll
       for (int t = 0; t < (NTC < 0 ? 0 : NTC); ++t)
 #pragma unroll
-        for (int j = 0; j < d; ++j)
-          bulk_g2s(st + (NG + NY + d + t * d + j) * CH, a.F[t] + j * n + i0, cnt * 16u, &mb[b]);
+        for (int j = 0; j < NY; ++j)
+          bulk_g2s(st + (NG + 2 * NY + t * NY + j) * CH, a.F[t] + j * n + i0, cnt * 16u, &mb[b]);
     }
   };
   issue(blockIdx.x, 0);
@@ -210,7 +224,7 @@ __global__ void __launch_bounds__(NTC < 0 ? SRK_PT_CH : SRK_PC_CH) k_project_tma
           cplx acc = DIAG ? u : st[(NG + NY + j) * CH + tid];
 #pragma unroll
           for (int t = 0; t < (NTC < 0 ? 0 : NTC); ++t)
-            acc = radd(acc, rmul(a.c[t], st[(NG + NY + (DIAG ? 0 : d) + t * d + j) * CH + tid]));
+            acc = radd(acc, rmul(a.c[t], st[(NG + NY + (DIAG ? 0 : NY) + t * NY + j) * CH + tid]));
           a.ynext[j * n + i] = radd(acc, rmul(a.cself, o));
         }
       }
@@ -221,6 +235,13 @@ __global__ void __launch_bounds__(NTC < 0 ? SRK_PT_CH : SRK_PC_CH) k_project_tma
         cplx o = make_double2(div.y, -div.x);  // -1j * div
         o = rsub(o, rmul(__ddiv_rn(kv.k2, a.re_pr), rho));
         a.f[d * n + i] = o;
+        if constexpr (NTC >= 0) {  // the density component of the next stage input
+          cplx acc = DIAG ? rho : st[(NG + NY + d) * CH + tid];
+#pragma unroll
+          for (int t = 0; t < (NTC < 0 ? 0 : NTC); ++t)
+            acc = radd(acc, rmul(a.c[t], st[(NG + 2 * NY + t * NY + d) * CH + tid]));
+          a.ynext[d * n + i] = radd(acc, rmul(a.cself, o));
+        }
       }
     }
     __syncthreads();  // stage b consumed
@@ -609,9 +630,8 @@ __global__ void k_band_scale(cplx* __restrict__ u, const long long* __restrict__
 
 template <int DIMS, bool DENS, int NTC = -1, bool DIAG = false>
 static int launch_project_tma(const ProjArgs& a, cudaStream_t st) {
-  constexpr int CH = NTC < 0 ? SRK_PT_CH : SRK_PC_CH;
-  constexpr int NS = (DENS ? 2 * DIMS : DIMS) + (DENS ? DIMS + 1 : DIMS) +
-                     (NTC < 0 ? 0 : (DIAG ? 0 : DIMS) + DIMS * NTC);
+  constexpr int CH = proj_chunk<DIMS, DENS, NTC, DIAG>();
+  constexpr int NS = proj_streams<DIMS, DENS, NTC, DIAG>();
   const int smem = 2 * NS * CH * 16;
   static int blocks = 0;
   if (!blocks) {
@@ -630,23 +650,35 @@ static int launch_project_tma(const ProjArgs& a, cudaStream_t st) {
 }
 
 bool srk_launch_project_refresh(const ProjArgs& a, double* out, cudaStream_t st) {
-  if (a.g.dims != 3 || a.density || a.modes >= (1LL << 32) || !a.partial) return false;
-  const int grid = launch_project_tma<3, false, 0, true>(a, st);
+  if (a.modes >= (1LL << 32) || !a.partial) return false;
+  int grid;
+  if (a.g.dims == 3)
+    grid = a.density ? launch_project_tma<3, true, 0, true>(a, st) : launch_project_tma<3, false, 0, true>(a, st);
+  else
+    grid = a.density ? launch_project_tma<2, true, 0, true>(a, st) : launch_project_tma<2, false, 0, true>(a, st);
   k_finalize<<<1, 256, 0, st>>>(a.partial, grid, out);
   return true;
 }
 
-// K6 with the next stage input formed in the same pass (3D NS, modes < 2^32,
-// at most SRK_PC_MAXT earlier stages); returns false when the shape does not qualify
-bool srk_launch_project_comb(const ProjArgs& a, cudaStream_t st) {
-  if (a.g.dims != 3 || a.density || a.modes >= (1LL << 32) || a.nt < 0 || a.nt > SRK_PC_MAXT) return false;
+// K6 with the next stage input formed in the same pass (3D / 2D, NS or
+// Boussinesq, modes < 2^32, at most SRK_PC_MAXT earlier stages); returns false
+// when the shape does not qualify
+template <int DIMS, bool DENS>
+static void launch_project_comb(const ProjArgs& a, cudaStream_t st) {
   switch (a.nt) {
 #define CASE(N) \
-  case N: launch_project_tma<3, false, N>(a, st); break;
+  case N: launch_project_tma<DIMS, DENS, N>(a, st); break;
     CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6)
 #undef CASE
-    default: return false;
+    default: break;
   }
+}
+bool srk_launch_project_comb(const ProjArgs& a, cudaStream_t st) {
+  if (a.modes >= (1LL << 32) || a.nt < 0 || a.nt > SRK_PC_MAXT) return false;
+  if (a.g.dims == 3)
+    a.density ? launch_project_comb<3, true>(a, st) : launch_project_comb<3, false>(a, st);
+  else
+    a.density ? launch_project_comb<2, true>(a, st) : launch_project_comb<2, false>(a, st);
   return true;
 }
 

@@ -22,7 +22,7 @@ struct ProjArgs {
   long long modes;  // n0*n1*K
   int density;
   double nu, ri, re_pr;
-  // fused next-stage combination (k_project_tma<3, false, NT>):
+  // fused next-stage combination (k_project_tma<DIMS, DENS, NT>, every state component):
   //   ynext = yb + sum_{t < nt} c[t] F[t] + cself * f
   const cplx* yb;
   const cplx* F[SRK_MAX_TERMS];

@@ -723,8 +723,7 @@ int srk_rhs_combine(srk_plan* p, const void* y, void* f, double nu, double ri, d
 int srk_rhs_refresh(srk_plan* p, const void* y, void* f, double nu, double ri, double re_pr, double coef_self,
                     void* ynext, double* diag_out, void* stream) {
   if (!p) return fail(SRK_ERR_INVALID, "null plan");
-  if (p->dims != 3 || p->density || p->nranks != 1)
-    return fail(SRK_ERR_UNSUPPORTED, "srk_rhs_refresh: 3D NS on an unsplit plan only");
+  if (p->nranks != 1) return fail(SRK_ERR_UNSUPPORTED, "srk_rhs_refresh: unsplit plans only");
   if (!ynext || !diag_out || ynext == y || ynext == f) return fail(SRK_ERR_INVALID, "srk_rhs_refresh: bad outputs");
   if (!p->partial) {
     cudaError_t err = cudaMalloc(&p->partial, sizeof(double) * SRK_NQ * SRK_RED_BLOCKS);
@@ -864,7 +863,7 @@ int rhs_impl(srk_plan* p, const void* y_, void* f_, double nu, double ri, double
     pa.partial = p->partial;
     pa.cself = cs->cself;
     pa.ynext = cs->ynext;
-    if (!srk_launch_project_refresh(pa, cs->diag_out, st)) return fail(SRK_ERR_UNSUPPORTED, "srk_rhs_refresh: 3D NS only");
+    if (!srk_launch_project_refresh(pa, cs->diag_out, st)) return fail(SRK_ERR_UNSUPPORTED, "srk_rhs_refresh: mode count >= 2^32");
     p->last_launches += 2;
     if (p->timing && p->nev < 16) cudaEventRecord(p->ev[p->nev++], st);
     return check_launch("k_project_tma (refresh)");

@@ -82,7 +82,8 @@ class FlowRHS:
         (integrators.py:327-339): returns ``(f, ybase + sum c_j F_j + coef_self f)``,
         summed in ascending stage order with f last -- bitwise the unfused
         ``combine(ybase, terms + [(coef_self, f)])`` -- in one srk_rhs_combine call
-        (the 3D projection kernel forms the sum while f is in registers)."""
+        (the projection kernel forms the sum while f is in registers; 2D / 3D,
+        with or without density)."""
         y, _ = to_device(fields, torch.complex128)
         yb, _ = to_device(ybase, torch.complex128)
         f = torch.empty_like(y)
@@ -104,17 +105,9 @@ class FlowRHS:
         step's first stage sum: returns ``(f, y + coef_self f, sums)`` with ``f =
         self(t, y)`` and ``sums`` the 9 reduce_sums values of (y, f) for the
         diagnostics record (entries 4, 5, 8 = E, eps, Z sums; diag_from_sums).
-        One projection pass on the 3D NS path (srk_rhs_refresh); elsewhere the
-        separate calls."""
-        from .diagnostics import reduce_sums
-        from .integrators import combine
-
+        One projection pass (srk_rhs_refresh; E, eps, Z over the velocity
+        components, density included in the stage sum)."""
         y, _ = to_device(fields, torch.complex128)
-        g = self.grid
-        if g.dims != 3 or self.density:
-            f = self(t, y)
-            q = reduce_sums(g, y, fl=f, flags=2, ncomp=min(y.shape[0], g.dims), host=True).tolist()
-            return f, combine(y, [(coef_self, f)]), q
         f = torch.empty_like(y)
         ynext = torch.empty_like(y)
         p = self.params

@@ -20,7 +20,7 @@ def _state(g, ncomp, seed):
 
 
 CASES = [((32, 32, 32), False), ((16, 32, 48), False), ((64, 64, 64), False), ((256, 256, 256), False),
-         ((64, 256), False), ((16, 32, 24), True), ((64, 128), True)]
+         ((64, 256), False), ((16, 32, 24), True), ((64, 128), True), ((1024, 1024), True), ((128, 128, 128), True)]
 
 
 @pytest.mark.parametrize("shape,density", CASES)
@@ -107,21 +107,27 @@ def test_forcing_with_step_energy_sum_is_bitwise_the_full_pass():
     assert torch.equal(a, b)
 
 
-def test_refresh_matches_separate_calls():
+@pytest.mark.parametrize("shape,density", [((64, 64, 64), False), ((16, 32, 24), True), ((64, 128), True),
+                                           ((64, 128), False), ((1024, 1024), True)])
+def test_refresh_matches_separate_calls(shape, density):
     """srk_rhs_refresh: f and y + c f bitwise the separate calls, the diagnostics
-    sums equal to srk_step_reduce's (different fixed summation order)."""
+    sums equal to srk_step_reduce's (different fixed summation order); 3D / 2D,
+    NS / Boussinesq (sums over the velocity components)."""
     from paper_1810_10197_b200.diagnostics import reduce_sums
     from paper_1810_10197_b200.integrators import combine
 
-    g = srk.Grid((64, 64, 64))
-    rhs = srk.FlowRHS(g, srk.PhysParams(700.0))
-    y = srk.hit_init(g, srk.ProblemSpec("hit", a=4.0, energy=0.5, seed=9)).fields
+    g = srk.Grid(shape)
+    rhs = srk.FlowRHS(g, srk.PhysParams(700.0, 1.1, 0.9), density=density)
+    if len(shape) == 3 and not density:
+        y = srk.hit_init(g, srk.ProblemSpec("hit", a=4.0, energy=0.5, seed=9)).fields
+    else:
+        y = _state(g, g.dims + (1 if density else 0), 9)
     c = 1e-3 * 0.5
     f, y2, q = rhs.refresh(0.0, y, c)
     f_ref = rhs(0.0, y)
     assert torch.equal(f, f_ref)
     assert torch.equal(y2, combine(y, [(c, f_ref)]))
-    q_ref = reduce_sums(g, y, fl=f_ref, flags=2, ncomp=3, host=True).tolist()
+    q_ref = reduce_sums(g, y, fl=f_ref, flags=2, ncomp=g.dims, host=True).tolist()
     for k in (4, 5, 8):
         assert abs(q[k] - q_ref[k]) <= 1e-13 * abs(q_ref[k])
     assert all(q[k] == 0.0 for k in (0, 1, 2, 3, 6, 7))
