@@ -39,7 +39,25 @@ void srk_reg_1536(KEntry* t) {
 #elif SRK_NS3P1536 == 8
   SRK_NS3P(1536, (8, 8, 6), (12, 32))
 #endif
-#ifndef SRK_B2PAIR
+#if !defined(SRK_B2PAIR) && !defined(SRK_B2GEN)
+  // 2D Boussinesq z-pass with the fused middle stage (v15): one pencil per CTA,
+  // inverse prefix 8 8 6 on 2 columns (E = 24, 128 threads), last inverse
+  // radix-4 | u x w, rho u | first forward radix-4 in registers, forward suffix
+  // FR on the 2 packed product columns
+#if defined(SRK_B2FRSEL) && SRK_B2FRSEL == 2
+#define SRK_B2FR 12, 32
+#elif defined(SRK_B2FRSEL) && SRK_B2FRSEL == 3
+#define SRK_B2FR 16, 24
+#else
+#define SRK_B2FR 24, 16
+#endif
+  {
+    using Z2 = ColTile<1536, 2>;
+    using E2 = FastFFT<1536, 24, Z2, 8, 8, 6>;
+    t[KK_Z_B2] = KEntry{(const void*)(k_zpass_ns3p<1536, Z2, E2, ZOP_B2, SRK_B2FR>), E2::NT, 2,
+                        (int)(Z2::SIZE * 16) + E2::TWN * 16, 0, 1};
+  }
+#elif !defined(SRK_B2PAIR)
   // 2D Boussinesq z-pass, one pencil per CTA (2 columns, 128 threads, 3 CTAs/SM)
   {
     using Z2 = ColTile<1536, 2>;

@@ -1068,17 +1068,29 @@ struct LoopStageZ {
 #ifndef SRK_ZP1_MINB12
 #define SRK_ZP1_MINB12 5  // CTAs per SM for the E = 12 (M/4-thread) variant
 #endif
-template <int M, class L, class EngI, int... FR>
-__global__ void __launch_bounds__(EngI::NT, (EngI::NT == M / 8 ? (M <= 768 ? SRK_ZP1_MINB : 2) : SRK_ZP1_MINB12))
+#ifndef SRK_ZB2P_MINB
+#define SRK_ZB2P_MINB 3  // CTAs per SM of the 2D Boussinesq variant (M = 1536, 128 threads)
+#endif
+// OP = ZOP_B2 (2D Boussinesq, v15): 2 inverse columns [u0 + i u1][w + i rho],
+// the four products [w u1 + i(-w u0)][rho u0 + i rho u1] packed in the 2
+// forward columns, both extracted two-for-one; NT = M/12 (E = 24 on 2 columns,
+// three fused-middle rows per thread).
+template <int M, class L, class EngI, int OP, int... FR>
+__global__ void __launch_bounds__(EngI::NT, (OP == ZOP_B2 ? SRK_ZB2P_MINB
+                                                          : (EngI::NT == M / 8 ? (M <= 768 ? SRK_ZP1_MINB : 2)
+                                                                               : SRK_ZP1_MINB12)))
     k_zpass_ns3p(const ZArgs a, int, int) {
   extern __shared__ __align__(16) cplx smraw[];
   cplx* const sm = smraw + EngI::TWN;  // [twiddle table][tile]
   const cplx* const twp = smraw;
   tw_fill<M>(smraw, a.tw);
-  // NT = M/8 (E = 24: two fused-middle rows per thread) or M/4 (E = 12: one)
-  constexpr int S = 3, NT = EngI::NT, K = M / 3 + 1, Q = M / 4, RPT = Q / NT;
-  static_assert(NT == M / 8 || NT == M / 4, "inverse prefix must use M/8 or M/4 threads");
-  static_assert(L::C == 3, "three tile columns");
+  static_assert(OP == ZOP_NS3 || OP == ZOP_B2, "NS3 or 2D Boussinesq");
+  // NT = M/8 (E = 24: two fused-middle rows per thread) or M/4 (E = 12: one);
+  // B2: M/12 (three rows)
+  constexpr int S = OP == ZOP_B2 ? 2 : 3, NT = EngI::NT, K = M / 3 + 1, Q = M / 4, RPT = Q / NT;
+  static_assert(OP == ZOP_B2 ? NT == M / 12 : (NT == M / 8 || NT == M / 4), "inverse prefix thread count");
+  static_assert(L::C == S, "one tile column per inverse complex signal");
+  static_assert(Q % NT == 0, "whole fused-middle rows per thread");
   const int pen = blockIdx.x;
   const int tid = threadIdx.x;
   SRK_TS_INIT(a.dbg, 6)
@@ -1162,11 +1174,16 @@ __global__ void __launch_bounds__(EngI::NT, (EngI::NT == M / 8 ? (M <= 768 ? SRK
       cplx F0[4], F1[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const double r[6] = {v[h][0][q].x, v[h][0][q].y, v[h][1][q].x, v[h][1][q].y, v[h][2][q].x, v[h][2][q].y};
-        double o[3];
-        zphys<ZOP_NS3>(r, o);
+        double r[2 * S];
+#pragma unroll
+        for (int c = 0; c < S; ++c) {
+          r[2 * c] = v[h][c][q].x;
+          r[2 * c + 1] = v[h][c][q].y;
+        }
+        double o[4];
+        zphys<OP>(r, o);
         F0[q] = cmk(o[0], o[1]);
-        F1[q] = cmk(o[2], 0.0);
+        F1[q] = cmk(o[2], OP == ZOP_B2 ? o[3] : 0.0);
       }
       DFT<4, -1>::run(F0);
       DFT<4, -1>::run(F1);
@@ -1198,7 +1215,13 @@ __global__ void __launch_bounds__(EngI::NT, (EngI::NT == M / 8 ? (M <= 768 ? SRK
     cplx* o = a.out + (long long)pen * K + k;
     o[0] = cmk(0.5 * (Zk.x + Zm.x), 0.5 * (Zk.y - Zm.y));
     o[a.out_sig_stride] = cmk(0.5 * (Zk.y + Zm.y), -0.5 * (Zk.x - Zm.x));
-    o[2 * a.out_sig_stride] = (k == 0) ? cmk(P2.x, 0.0) : P2;
+    if constexpr (OP == ZOP_B2) {  // column 1 = [P2 + i P3]: two-for-one as well
+      const cplx Wm = live ? sm[L::idx(k == 0 ? 0 : M - k, 1)] : cmk(0.0, 0.0);
+      o[2 * a.out_sig_stride] = cmk(0.5 * (P2.x + Wm.x), 0.5 * (P2.y - Wm.y));
+      o[3 * a.out_sig_stride] = cmk(0.5 * (P2.y + Wm.y), -0.5 * (P2.x - Wm.x));
+    } else {
+      o[2 * a.out_sig_stride] = (k == 0) ? cmk(P2.x, 0.0) : P2;
+    }
   }
   if (a.dbg) {
     __syncthreads();

@@ -176,7 +176,7 @@ struct GenCols {
   {                                                                                                \
     using ZL = ColTile<M, 3>;                                                                      \
     using EI = FastFFT<M, 24, ZL, SRK_UNPAREN IR>;                                                 \
-    t[KK_Z_NS3] = KEntry{(const void*)(k_zpass_ns3p<M, ZL, EI, SRK_UNPAREN FR>), M / 8, 3,          \
+    t[KK_Z_NS3] = KEntry{(const void*)(k_zpass_ns3p<M, ZL, EI, ZOP_NS3, SRK_UNPAREN FR>), M / 8, 3,          \
                          (int)(ZL::SIZE * 16) + EI::TWN * 16, 0, 1};                               \
   }
 // same with E = 12 in the inverse prefix (M/4 threads, one fused-middle row each)
@@ -184,7 +184,7 @@ struct GenCols {
   {                                                                                                \
     using ZL = ColTile<M, 3>;                                                                      \
     using EI = FastFFT<M, 12, ZL, SRK_UNPAREN IR>;                                                 \
-    t[KK_Z_NS3] = KEntry{(const void*)(k_zpass_ns3p<M, ZL, EI, SRK_UNPAREN FR>), M / 4, 3,          \
+    t[KK_Z_NS3] = KEntry{(const void*)(k_zpass_ns3p<M, ZL, EI, ZOP_NS3, SRK_UNPAREN FR>), M / 4, 3,          \
                          (int)(ZL::SIZE * 16) + EI::TWN * 16, 0, 1};                               \
   }
 #define SRK_NS3F(M, IR, EF, FR)                                                                     \
