@@ -233,6 +233,15 @@ int srk_ipc_close(void* dev_ptr, int64_t offset);
  * tools/phase_timing.py).  Not a compute entry point. */
 int srk_debug_phase_buffer(srk_plan* plan, void* dev_buf, int launch_index);
 
+/* Throughput probe (not a compute entry point): one launch of blocks_per_sm
+ * x SMs CTAs of 256 threads, each thread running `iters` trips of 8 ops:
+ * mode 0 fp64 FMA, 1 fp64 add, 2 16-byte shared-memory loads, 3 warp
+ * shuffles, 4 two shared loads + eight shuffles interleaved.  scratch: a
+ * device buffer of >= blocks_per_sm * SMs doubles.  *ops_out = thread-level
+ * operations issued (time the launch with events on `stream`).  Used by
+ * bench.py for the measured fp64 ceiling of the z-pass. */
+int srk_probe(int mode, int iters, int blocks_per_sm, void* scratch, void* stream, double* ops_out);
+
 /* Number of kernel launches the last srk_rhs issued (launch accounting for
  * the bench's gpu_launches claim). */
 int srk_rhs_launch_count(const srk_plan* plan);

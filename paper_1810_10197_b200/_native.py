@@ -11,7 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("SRK_LIB") or os.path.join(_HERE, "_lib", "libsrk.so")  # SRK_LIB: experiment builds
+LIB_PATH = os.path.join(_HERE, "_lib", "libsrk.so")
 
 SRK_OK = 0
 SRK_ERR_INVALID = 1
@@ -30,7 +30,7 @@ EXPORTS = (
     "srk_slab_forward_kz", "srk_slab_inverse_y_kz", "srk_slab_zpass", "srk_slab_forward_y_kz",
     "srk_slab_forward_x_kz", "srk_slab_project", "srk_store_mapped", "srk_slab_set_peers",
     "srk_slab_forward_kz_peer", "srk_slab_forward_y_kz_peer", "srk_ipc_export", "srk_ipc_import", "srk_ipc_close",
-    "srk_rhs_refresh",
+    "srk_rhs_refresh", "srk_probe",
 )
 
 _lib = None
@@ -81,6 +81,7 @@ def load():
         "srk_band_energy": (c_int, [vp, vp, c_int, vp, vp, c_int, vp, vp]),
         "srk_band_scale": (c_int, [vp, vp, c_int, vp, c_int, c_dbl, vp]),
         "srk_store_mapped": (c_int, [vp, vp, c_int, vp]),
+        "srk_probe": (c_int, [c_int, c_int, c_int, vp, vp, P(c_dbl)]),
         "srk_rhs_refresh": (c_int, [vp, vp, vp, c_dbl, c_dbl, c_dbl, c_dbl, vp, vp, vp]),
         "srk_slab_set_peers": (c_int, [vp, P(vp), P(vp), c_int]),
         "srk_slab_forward_kz_peer": (c_int, [vp, vp, c_int, c_int, vp]),
@@ -133,7 +134,6 @@ def stream_ptr(stream=None):
 
 
 _HOST_RESULT = {}
-NO_HOST_RESULT = bool(os.environ.get("SRK_NO_HOST_RESULT"))  # A/B experiments: device result + cudaMemcpy
 
 
 def host_result(n):
@@ -160,8 +160,6 @@ def fetch_small(t, stream=None):
     import torch
 
     t = t.to(torch.float64).contiguous()
-    if NO_HOST_RESULT:
-        return t.cpu()
     buf = host_result(t.numel())
     check(load().srk_store_mapped(ptr(t), ctypes.c_void_p(buf.data_ptr()), t.numel(), stream_ptr(stream)),
           "srk_store_mapped")

@@ -122,7 +122,7 @@ __device__ __forceinline__ cplx tw_get(const cplx* tws, unsigned m) {
 // (and w^8, w^16) come from the table; w^(8a+b) = w^(8a) * w^b is formed on
 // the fly, so at most 10 powers are live (a few extra roundings, ~5e-16
 // relative).  Products instead of per-exponent table lookups measured 0.8 ms
-// faster per 512^3 RHS; SRK_TW_BINARY keeps all R-1 powers (binary products).
+// faster per 512^3 RHS.
 template <int M, int SIGN>
 __device__ __forceinline__ cplx tw_pow(const cplx* tw, unsigned e) {
   cplx w = tw_get<M>(tw, e);
@@ -131,7 +131,6 @@ __device__ __forceinline__ cplx tw_pow(const cplx* tw, unsigned e) {
 }
 template <int M, int R, int SIGN>
 __device__ __forceinline__ void stage_twiddle(cplx* v, const cplx* tw, unsigned kts) {
-#ifndef SRK_TW_BINARY
   constexpr int B = R < 8 ? R : 8;
   cplx wb[8];
 #pragma unroll
@@ -153,21 +152,6 @@ __device__ __forceinline__ void stage_twiddle(cplx* v, const cplx* tw, unsigned 
       for (int b = 1; b < 8 && 8 * a + b < R; ++b) v[8 * a + b] = cmul(v[8 * a + b], cmul(wa, wb[b]));
     }
   }
-#else
-  cplx pw[R];
-#pragma unroll
-  for (int t = 1; t < R; ++t) {
-    if ((t & (t - 1)) == 0) {
-      pw[t] = tw_pow<M, SIGN>(tw, (unsigned)t * kts);
-    } else {
-      int hb = 1;
-      while (2 * hb <= t) hb *= 2;
-      pw[t] = cmul(pw[hb], pw[t - hb]);
-    }
-  }
-#pragma unroll
-  for (int t = 1; t < R; ++t) v[t] = cmul(v[t], pw[t]);
-#endif
   static_assert(R <= 32, "stage_twiddle covers radices up to 32");
 }
 

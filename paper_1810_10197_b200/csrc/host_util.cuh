@@ -1,0 +1,82 @@
+// Host-side launch helpers shared by the translation units of libsrk: every
+// per-kernel launch setting that depends on the device (the opt-in shared
+// memory attribute, SM count, resident CTAs per SM) is cached per
+// (device, kernel), so one process may drive several GPUs (the single-process
+// multi-device layout of SURVEY §8e, or a caller that switches
+// torch.cuda.set_device between plans).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <map>
+#include <mutex>
+#include <tuple>
+
+inline int srk_current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+
+namespace srk_host {
+inline std::mutex& mu() {
+  static std::mutex m;
+  return m;
+}
+inline std::map<std::pair<int, const void*>, int>& smem_set() {
+  static std::map<std::pair<int, const void*>, int> m;
+  return m;
+}
+inline std::map<std::tuple<int, const void*, int, int>, int>& occ() {
+  static std::map<std::tuple<int, const void*, int, int>, int> m;
+  return m;
+}
+inline std::map<int, int>& sms() {
+  static std::map<int, int> m;
+  return m;
+}
+}  // namespace srk_host
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize >= bytes on the current device,
+// set once per (device, kernel) and only raised.
+inline cudaError_t srk_ensure_smem(const void* fn, int bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  const int dev = srk_current_device();
+  std::lock_guard<std::mutex> lk(srk_host::mu());
+  auto& m = srk_host::smem_set();
+  auto it = m.find({dev, fn});
+  if (it != m.end() && it->second >= bytes) return cudaSuccess;
+  cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (err == cudaSuccess) m[{dev, fn}] = bytes;
+  return err;
+}
+
+inline int srk_sm_count() {
+  const int dev = srk_current_device();
+  std::lock_guard<std::mutex> lk(srk_host::mu());
+  auto& m = srk_host::sms();
+  auto it = m.find(dev);
+  if (it != m.end()) return it->second;
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  if (n < 1) n = 1;
+  m[dev] = n;
+  return n;
+}
+
+// resident CTAs per SM of fn (nt threads, smem dynamic bytes) on the current device
+inline int srk_blocks_per_sm(const void* fn, int nt, int smem) {
+  const int dev = srk_current_device();
+  {
+    std::lock_guard<std::mutex> lk(srk_host::mu());
+    auto& m = srk_host::occ();
+    auto it = m.find({dev, fn, nt, smem});
+    if (it != m.end()) return it->second;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nt, smem);
+  if (per_sm < 1) per_sm = 1;
+  std::lock_guard<std::mutex> lk(srk_host::mu());
+  srk_host::occ()[{dev, fn, nt, smem}] = per_sm;
+  return per_sm;
+}

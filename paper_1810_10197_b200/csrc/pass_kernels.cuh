@@ -16,8 +16,6 @@
 //                            :163-184)   [rhs_kernels.cu]
 #pragma once
 
-#include <cooperative_groups.h>
-
 #include "fft_engine.cuh"
 
 #define SRK_MAX_PEERS 8
@@ -242,13 +240,9 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
   const bool use_tma = kTMA && a.tma;
   // TMA output: the last stage writes a dense [M][C] tile in smem (over the
   // FFT tile, after the stage's load barrier), then one thread stores it
-#ifdef SRK_NO_TMAO_BUILD
-  constexpr bool kTMAO = false;
-#else
   // (K2 only: measured 5.48 -> 5.30 ms at 512^3; the x-pass K1, whose output
   // rows are 2 MB apart, was slower with TMA stores, 2.98 -> 3.43 ms)
   constexpr bool kTMAO = Eng::kFast && !(FL & PF_BOUT) && KIND == PK_INV_CURLY;
-#endif
   const bool use_tmo = kTMAO && a.tma_out;
   auto flush_out = [&]() {
     if (use_tmo) {
@@ -866,132 +860,6 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
 
 
 // ---------------------------------------------------------------------------
-// K5 + K6 fused over a thread-block cluster (cluster = the So product signals
-// of one column tile; cluster rank = signal).  Each CTA runs the x-forward
-// transform of its signal, keeps the truncated, scaled tile G_o (n0 rows x C
-// columns) in shared memory, and after a cluster barrier projects its own
-// component reading the peers' G tiles through distributed shared memory:
-//   f_o = G_o - k_o (k.G)/|k|^2 - nu |k|^2 u_o            (physics.py:119-129)
-// Boussinesq: G_{d-1} -= Ri rho before the projection; rank d writes the density
-// tendency -i k.(rho u)^ - |k|^2 rho / (Re Pr) (physics.py:163-184).
-// ---------------------------------------------------------------------------
-template <class Eng, int FL>
-__global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 128 ? 3 : 1)) k_xfwd_proj(const PassArgs a) {
-  namespace cg = cooperative_groups;
-  extern __shared__ __align__(16) cplx smraw[];
-  cplx* const sm = smraw + Eng::TWN;
-  tw_fill<Eng::M>(smraw, a.tw);  // ordered by the staging barrier
-  constexpr int C = Eng::C;
-  constexpr bool CTN = (FL & PF_CTN) && Eng::kFast;
-  cg::cluster_group cluster = cg::this_cluster();
-  const int So = a.planes;
-  const int o = blockIdx.x % So;
-  const int wt = blockIdx.x / So;
-  const int w0 = wt * C;
-  const int ncols = min(C, a.Qp - w0);
-  const unsigned rs = (unsigned)a.row_stride;
-  const int M = CTN ? Eng::M : a.M;
-  const int n = CTN ? 2 * Eng::M / 3 : a.n;
-  const int in_rpb = (FL & PF_BIN) ? a.in_rpb : 0;
-  const cplx* __restrict__ inp = a.in + o * a.in_plane_stride + w0;
-  cplx* G = sm;  // [n][C] after the transform (aliases the FFT tile)
-  // ---- x forward transform + truncation + (1/1.5)^d into smem ----
-  stage_rows<C>(sm, inp, M, rs, ncols, in_rpb, a.in_bstride);
-  cp_async_wait_all();
-  __syncthreads();
-  {
-    const double sc = a.scale;
-    const bool zdc = (w0 == 0) && (a.y0 == 0);
-    auto ld = [&](int row, int col) -> cplx { return sm[row * C + col]; };
-    auto st = [&](int row, int col, cplx v) {
-      const int c = trunc_dst(row, n, M, true);
-      if (c == -1) return;
-      cplx ov = cmk(v.x * sc, v.y * sc);
-      if (c == -2) ov = cmk(0.0, 0.0);
-      if (zdc && c == 0 && col == 0) ov.y = 0.0;
-      G[(c == -2 ? (n >> 1) : c) * C + col] = ov;
-    };
-    Eng::template run<-1, true, true>(a.gp, sm, smraw, ncols, ld, st);
-  }
-  cluster.sync();
-  // ---- projection of component o on the tile (rows = coarse x, cols = (y, kz)) ----
-  const int d = a.dims;
-  const bool writer = (o < d) || (a.density && o == d);
-  if (writer) {
-    // peer tiles through DSMEM (scalar pointers: no local-memory arrays)
-    const cplx* g0 = cluster.map_shared_rank(G, 0);
-    const cplx* g1 = cluster.map_shared_rank(G, 1);
-    const cplx* g2 = cluster.map_shared_rank(G, So > 2 ? 2 : 0);
-    const cplx* g3 = cluster.map_shared_rank(G, So > 3 ? 3 : 0);
-    const cplx* g4 = cluster.map_shared_rank(G, So > 4 ? 4 : 0);
-    const cplx* g5 = cluster.map_shared_rank(G, So > 5 ? 5 : 0);
-    const long long cs = a.comp_stride;
-    for (int i = threadIdx.x; i < n * C; i += blockDim.x) {
-      const int row = i / C, col = i - (i / C) * C;
-      if (col >= ncols) continue;
-      const int q = w0 + col;
-      const double kx = mode_full(row, n) * a.ck0;
-      double k1v, k2v;
-      if (d == 3) {
-        const int yl = q / a.K, kzi = q - yl * a.K;
-        k1v = mode_full(a.y0 + yl, a.n1g) * a.ck1;
-        k2v = (double)kzi * a.ck2;
-      } else {
-        k1v = (double)q * a.ck2;
-        k2v = 0.0;
-      }
-      const double k2 = __dadd_rn(__dadd_rn(__dmul_rn(kx, kx), __dmul_rn(k1v, k1v)), __dmul_rn(k2v, k2v));
-      const double inv = (k2 == 0.0) ? 0.0 : __ddiv_rn(1.0, k2);
-      const long long off = (long long)row * rs + q;  // offset within a component
-      cplx rho = cmk(0.0, 0.0);
-      if (a.density) rho = a.y[d * cs + off];
-      if (o < d) {
-        cplx G0 = g0[i], G1 = g1[i], G2 = (d == 3) ? g2[i] : cmk(0.0, 0.0);
-        if (a.density) {
-          cplx& Gl = (d == 3) ? G2 : G1;
-          Gl.x = __dsub_rn(Gl.x, __dmul_rn(a.ri, rho.x));
-          Gl.y = __dsub_rn(Gl.y, __dmul_rn(a.ri, rho.y));
-        }
-        cplx kd = cmk(__dmul_rn(kx, G0.x), __dmul_rn(kx, G0.y));
-        kd.x = __dadd_rn(kd.x, __dmul_rn(k1v, G1.x));
-        kd.y = __dadd_rn(kd.y, __dmul_rn(k1v, G1.y));
-        if (d == 3) {
-          kd.x = __dadd_rn(kd.x, __dmul_rn(k2v, G2.x));
-          kd.y = __dadd_rn(kd.y, __dmul_rn(k2v, G2.y));
-        }
-        kd = cmk(__dmul_rn(inv, kd.x), __dmul_rn(inv, kd.y));
-        const double nuk2 = __dmul_rn(a.nu, k2);
-        const double ko = (o == 0) ? kx : (o == 1 ? k1v : k2v);
-        const cplx Go = (o == 0) ? G0 : (o == 1 ? G1 : G2);
-        const cplx u = a.y[o * cs + off];
-        cplx fo;
-        fo.x = __dsub_rn(__dsub_rn(Go.x, __dmul_rn(ko, kd.x)), __dmul_rn(nuk2, u.x));
-        fo.y = __dsub_rn(__dsub_rn(Go.y, __dmul_rn(ko, kd.y)), __dmul_rn(nuk2, u.y));
-        a.f[o * cs + off] = fo;
-      } else {  // density tendency (rank d): fluxes at ranks d .. 2d-1
-        const cplx F0 = (d == 3) ? g3[i] : g2[i];
-        const cplx F1 = (d == 3) ? g4[i] : g3[i];
-        cplx div = cmk(__dmul_rn(kx, F0.x), __dmul_rn(kx, F0.y));
-        div.x = __dadd_rn(div.x, __dmul_rn(k1v, F1.x));
-        div.y = __dadd_rn(div.y, __dmul_rn(k1v, F1.y));
-        if (d == 3) {
-          const cplx F2 = g5[i];
-          div.x = __dadd_rn(div.x, __dmul_rn(k2v, F2.x));
-          div.y = __dadd_rn(div.y, __dmul_rn(k2v, F2.y));
-        }
-        const double dr = __ddiv_rn(k2, a.re_pr);
-        cplx fo = cmk(div.y, -div.x);  // -1j * div
-        fo.x = __dsub_rn(fo.x, __dmul_rn(dr, rho.x));
-        fo.y = __dsub_rn(fo.y, __dmul_rn(dr, rho.y));
-        a.f[d * cs + off] = fo;
-      }
-    }
-  }
-  cluster.sync();  // peers may still be reading this CTA's tile
-}
-
-
-// ---------------------------------------------------------------------------
 // Stages after a caller-run prefix with the thread -> (column, butterfly) map
 // redone per stage and NCOL * M/R butterflies looped over the CTA (each
 // thread keeps ceil(NCOL*M/R / NT) butterflies live across the barrier).
@@ -1062,33 +930,23 @@ struct LoopStageZ {
 // SM with independent phases instead of 2 CTAs (12 warps) -- at the price of
 // one extra 768-point forward transform per two pencils (P2 rides alone).
 // ---------------------------------------------------------------------------
-#ifndef SRK_ZP1_MINB
-#define SRK_ZP1_MINB 5  // CTAs per SM the register budget targets (shared memory allows 5)
-#endif
-#ifndef SRK_ZP1_MINB12
-#define SRK_ZP1_MINB12 5  // CTAs per SM for the E = 12 (M/4-thread) variant
-#endif
-#ifndef SRK_ZB2P_MINB
+#define SRK_ZP1_MINB 5   // CTAs per SM the register budget targets (shared memory allows 5)
 #define SRK_ZB2P_MINB 3  // CTAs per SM of the 2D Boussinesq variant (M = 1536, 128 threads)
-#endif
 // OP = ZOP_B2 (2D Boussinesq, v15): 2 inverse columns [u0 + i u1][w + i rho],
 // the four products [w u1 + i(-w u0)][rho u0 + i rho u1] packed in the 2
 // forward columns, both extracted two-for-one; NT = M/12 (E = 24 on 2 columns,
 // three fused-middle rows per thread).
 template <int M, class L, class EngI, int OP, int... FR>
-__global__ void __launch_bounds__(EngI::NT, (OP == ZOP_B2 ? SRK_ZB2P_MINB
-                                                          : (EngI::NT == M / 8 ? (M <= 768 ? SRK_ZP1_MINB : 2)
-                                                                               : SRK_ZP1_MINB12)))
+__global__ void __launch_bounds__(EngI::NT, (OP == ZOP_B2 ? SRK_ZB2P_MINB : (M <= 768 ? SRK_ZP1_MINB : 2)))
     k_zpass_ns3p(const ZArgs a, int, int) {
   extern __shared__ __align__(16) cplx smraw[];
   cplx* const sm = smraw + EngI::TWN;  // [twiddle table][tile]
   const cplx* const twp = smraw;
   tw_fill<M>(smraw, a.tw);
   static_assert(OP == ZOP_NS3 || OP == ZOP_B2, "NS3 or 2D Boussinesq");
-  // NT = M/8 (E = 24: two fused-middle rows per thread) or M/4 (E = 12: one);
-  // B2: M/12 (three rows)
+  // NT = M/8 (E = 24: two fused-middle rows per thread); B2: M/12 (three rows)
   constexpr int S = OP == ZOP_B2 ? 2 : 3, NT = EngI::NT, K = M / 3 + 1, Q = M / 4, RPT = Q / NT;
-  static_assert(OP == ZOP_B2 ? NT == M / 12 : (NT == M / 8 || NT == M / 4), "inverse prefix thread count");
+  static_assert(OP == ZOP_B2 ? NT == M / 12 : NT == M / 8, "inverse prefix thread count");
   static_assert(L::C == S, "one tile column per inverse complex signal");
   static_assert(Q % NT == 0, "whole fused-middle rows per thread");
   const int pen = blockIdx.x;

@@ -115,9 +115,7 @@ __device__ __forceinline__ KVec kvec32(unsigned idx, const GeomArgs& g) {
 // F_t ride in the same ring (256-mode chunks: one CTA per SM from 4 earlier
 // stages on, still faster than 128-mode chunks at two CTAs per SM).
 #define SRK_PT_CH 256
-#ifndef SRK_PC_CH
 #define SRK_PC_CH 256  // modes per chunk (and threads) of the fused K6 + stage-sum kernel; ncu: 128 -> 256 is 1-7% faster
-#endif
 // shared-memory components streamed per mode: G, state, and (fused stage sum)
 // ybase + the NTC earlier stages, each with the state's component count
 template <int DIMS, bool DENS, int NTC, bool DIAG>
@@ -371,68 +369,6 @@ void srk_launch_combine(const CombArgs& a, cudaStream_t st) {
 //   q[7]           : count of sc <= 0 (control.py:74-75)
 //   q[8]           : sum_w |k|^2 |y1|^2 velocity    (enstrophy)
 // ---------------------------------------------------------------------------
-template <int NT>
-__global__ void __launch_bounds__(256) k_reduce(const RedArgs a) {
-  double acc[SRK_NQ];
-#pragma unroll
-  for (int q = 0; q < SRK_NQ; ++q) acc[q] = 0.0;
-  const long long n = a.modes;
-  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const long long nthr = (long long)gridDim.x * blockDim.x;
-  for (int c = 0; c < a.ncomp; ++c) {
-    double r2 = 0.0, e = 0.0, ep = 0.0, bad = 0.0, neg = 0.0, z = 0.0;
-    const bool vel = c < a.dvel;
-    for (long long i = tid; i < n; i += nthr) {
-      const long long ix = c * n + i;
-      const cplx y1 = a.y1[ix];
-      if (a.do_norm) {
-        cplx dl = make_double2(0.0, 0.0);
-#pragma unroll
-        for (int j = 0; j < NT; ++j) dl = radd(dl, rmul(a.c[j], a.F[j][ix]));
-        const cplx y0 = a.y0[ix];
-        const double sc = DADD(a.atol, DMUL(fmax(hypot(y0.x, y0.y), hypot(y1.x, y1.y)), a.rtol));
-        const double rt = __ddiv_rn(hypot(dl.x, dl.y), sc);
-        r2 = DADD(r2, DMUL(rt, rt));
-        if (!(isfinite(dl.x) && isfinite(dl.y))) bad += 1.0;
-        if (sc <= 0.0) neg += 1.0;
-      }
-      if (!(isfinite(y1.x) && isfinite(y1.y))) bad += 1.0;
-      if (a.do_diag && vel) {
-        const int kz = (int)(i % a.K);
-        const double w = (kz == 0 || kz == a.K - 1) ? 1.0 : 2.0;
-        e = DADD(e, DMUL(w, DADD(DMUL(y1.x, y1.x), DMUL(y1.y, y1.y))));
-        const cplx fl = a.fl[ix];
-        ep = DADD(ep, DMUL(w, DADD(DMUL(y1.x, fl.x), DMUL(y1.y, fl.y))));
-        const double k2 = kvec(i, a.g).k2;
-        z = DADD(z, DMUL(DMUL(w, k2), DADD(DMUL(y1.x, y1.x), DMUL(y1.y, y1.y))));
-      }
-    }
-#pragma unroll
-    for (int cc = 0; cc < 4; ++cc)
-      if (cc == c) acc[cc] = r2;  // static indices only (no local-memory array)
-    acc[4] += e;
-    acc[5] += ep;
-    acc[6] += bad;
-    acc[7] += neg;
-    acc[8] += z;
-  }
-  __shared__ double red[SRK_NQ][32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int q = 0; q < SRK_NQ; ++q) {
-    double v = acc[q];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
-    if (lane == 0) red[q][warp] = v;
-  }
-  __syncthreads();
-  if (threadIdx.x < SRK_NQ) {
-    double v = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += red[threadIdx.x][w];
-    a.partial[threadIdx.x * gridDim.x + blockIdx.x] = v;
-  }
-}
-
 // TMA-streamed K7 (default): the up to NT + 3 input streams of a chunk of
 // SRK_RT_CH modes are fetched by 1D bulk copies into a two-stage shared-memory
 // ring (one elected thread, mbarrier completion), so the memory parallelism no
@@ -566,27 +502,11 @@ __global__ void k_finalize(const double* __restrict__ partial, int nblk, double*
 }
 
 void srk_launch_reduce(const RedArgs& a, double* out, cudaStream_t st) {
-  static const bool legacy = getenv("SRK_REDUCE_LEGACY") != nullptr;  // A/B switch
-  if (legacy) {
-    switch (a.nt) {
-#define CASE(N) \
-  case N: k_reduce<N><<<SRK_RED_BLOCKS, 256, 0, st>>>(a); break;
-      CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
-#undef CASE
-      default: break;
-    }
-    k_finalize<<<1, 256, 0, st>>>(a.partial, SRK_RED_BLOCKS, out);
-    return;
-  }
   switch (a.nt) {
 #define CASE(N)                                                                                      \
   case N: {                                                                                          \
     const int smem = 2 * (3 + N) * SRK_RT_CH * 16;                                                   \
-    static bool attr = false;                                                                        \
-    if (!attr) {                                                                                     \
-      cudaFuncSetAttribute(k_reduce_tma<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);      \
-      attr = true;                                                                                   \
-    }                                                                                                \
+    srk_ensure_smem((const void*)k_reduce_tma<N>, smem);                                             \
     k_reduce_tma<N><<<SRK_RT_BLOCKS, SRK_RT_CH, smem, st>>>(a);                                      \
   } break;
     CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
@@ -633,16 +553,10 @@ static int launch_project_tma(const ProjArgs& a, cudaStream_t st) {
   constexpr int CH = proj_chunk<DIMS, DENS, NTC, DIAG>();
   constexpr int NS = proj_streams<DIMS, DENS, NTC, DIAG>();
   const int smem = 2 * NS * CH * 16;
-  static int blocks = 0;
-  if (!blocks) {
-    cudaFuncSetAttribute(k_project_tma<DIMS, DENS, NTC, DIAG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    int per_sm = 0, dev = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_project_tma<DIMS, DENS, NTC, DIAG>, CH, smem);
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    blocks = std::max(1, per_sm) * sms;
-    if (DIAG) blocks = std::min(blocks, SRK_RED_BLOCKS);  // partials buffer
-  }
+  const void* fn = (const void*)k_project_tma<DIMS, DENS, NTC, DIAG>;
+  srk_ensure_smem(fn, smem);  // per (device, kernel)
+  int blocks = srk_blocks_per_sm(fn, CH, smem) * srk_sm_count();
+  if (DIAG) blocks = std::min(blocks, SRK_RED_BLOCKS);  // partials buffer
   const long long nch = (a.modes + CH - 1) / CH;
   const int grid = (int)std::min<long long>(blocks, nch);
   k_project_tma<DIMS, DENS, NTC, DIAG><<<grid, CH, smem, st>>>(a);
@@ -683,8 +597,7 @@ bool srk_launch_project_comb(const ProjArgs& a, cudaStream_t st) {
 }
 
 void srk_launch_project(const ProjArgs& a, cudaStream_t st) {
-  static const bool legacy = getenv("SRK_PROJECT_LEGACY") != nullptr;  // A/B switch
-  if (!legacy && a.modes < (1LL << 32)) {
+  if (a.modes < (1LL << 32)) {  // TMA-streamed kernel (32-bit mode indices)
     if (a.g.dims == 3)
       a.density ? launch_project_tma<3, true>(a, st) : launch_project_tma<3, false>(a, st);
     else

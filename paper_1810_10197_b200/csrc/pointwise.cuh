@@ -1,6 +1,7 @@
 // Argument structs / launchers for pointwise.cu (internal to libsrk).
 #pragma once
 
+#include "host_util.cuh"
 #include "srk_common.cuh"
 
 #define SRK_NQ 9

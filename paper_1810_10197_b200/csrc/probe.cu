@@ -1,0 +1,90 @@
+// Throughput probes (srk_probe_*): the ceilings the FFT passes are judged
+// against on this GPU, measured in-process by bench.py / tools/probe_peaks.py.
+//   mode 0: fp64 DFMA  -- 8 independent FMA chains per thread (2 flop each)
+//   mode 1: fp64 DADD  -- 8 independent add chains per thread
+//   mode 2: LDS.128    -- shared-memory crossbar: 16 B loads, conflict free
+//   mode 3: SHFL.32    -- warp shuffles (xor pattern), 8 independent chains
+//   mode 4: LDS.128 + SHFL interleaved (do they share the MIO datapath?)
+// Each thread runs `iters` loop trips; the result is folded into out[] so the
+// compiler cannot drop the work.  Units of work per trip and thread: 8 ops.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/srk.h"
+#include "host_util.cuh"
+
+namespace {
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_probe(double* out, int iters, double b, double c) {
+  __shared__ __align__(16) uint4 buf[2048];  // 32 KB
+  const int tid = threadIdx.x;
+  double acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = (double)(tid + i) * 1e-3;
+  if constexpr (MODE == 0) {
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = fma(acc[i], b, c);
+    }
+  } else if constexpr (MODE == 1) {
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = acc[i] + c;
+    }
+  } else {
+    for (int i = tid; i < 2048; i += blockDim.x) buf[i] = make_uint4(i, i * 3u, i * 5u, i * 7u);
+    __syncthreads();
+    unsigned x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = tid * 2654435761u + i;
+    uint4 y = make_uint4(0, 0, 0, 0);
+    const int lane = tid & 31;
+    for (int it = 0; it < iters; ++it) {
+      if constexpr (MODE == 2 || MODE == 4) {
+#pragma unroll
+        for (int i = 0; i < (MODE == 4 ? 2 : 8); ++i) {
+          // consecutive 16 B per lane: 4 wavefronts per warp load, conflict free
+          const uint4 v = buf[((it * 8 + i) * 32 + lane + (tid >> 5) * 256) & 2047];
+          y.x ^= v.x;
+          y.y ^= v.y;
+          y.z ^= v.z;
+          y.w ^= v.w;
+        }
+      }
+      if constexpr (MODE == 3 || MODE == 4) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = __shfl_xor_sync(0xffffffffu, x[i], 1 + (i & 15)) + (unsigned)it;
+      }
+    }
+    unsigned s = y.x ^ y.y ^ y.z ^ y.w;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s ^= x[i];
+    acc[0] = (double)s;
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += acc[i];
+  if (s == 1.2345e-300) out[blockIdx.x] = s;  // never true; keeps the work alive
+}
+
+}  // namespace
+
+extern "C" int srk_probe(int mode, int iters, int blocks_per_sm, void* scratch, void* stream, double* ops_out) {
+  if (mode < 0 || mode > 4 || iters < 1 || blocks_per_sm < 1 || !scratch) return SRK_ERR_INVALID;
+  const int grid = blocks_per_sm * srk_sm_count();
+  cudaStream_t st = (cudaStream_t)stream;
+  double* out = (double*)scratch;
+  switch (mode) {
+    case 0: k_probe<0><<<grid, 256, 0, st>>>(out, iters, 0.999999, 1e-7); break;
+    case 1: k_probe<1><<<grid, 256, 0, st>>>(out, iters, 0.999999, 1e-7); break;
+    case 2: k_probe<2><<<grid, 256, 0, st>>>(out, iters, 0.0, 0.0); break;
+    case 3: k_probe<3><<<grid, 256, 0, st>>>(out, iters, 0.0, 0.0); break;
+    default: k_probe<4><<<grid, 256, 0, st>>>(out, iters, 0.0, 0.0); break;
+  }
+  // thread-level operations issued (mode 0: FMAs; mode 2: 16 B loads; mode 3: shuffles;
+  // mode 4: 2 loads + 8 shuffles per trip)
+  const double per_trip = mode == 4 ? 10.0 : 8.0;
+  if (ops_out) *ops_out = per_trip * (double)iters * 256.0 * (double)grid;
+  return cudaGetLastError() == cudaSuccess ? SRK_OK : SRK_ERR_CUDA;
+}

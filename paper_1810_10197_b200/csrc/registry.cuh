@@ -25,12 +25,10 @@ enum KernelKind {
   KK_INV_KX_SLAB = 16,   // 3D K1, all-to-all #1 send layout
   KK_INV_CURLY = 17,     // 3D K2 (curl completed on load)
   KK_INV_CURLY_SLAB = 18,  // 3D K2 from the all-to-all #1 receive layout
-  KK_FWD_PROJ = 19,        // K5 + K6 fused over a cluster of So CTAs (DSMEM)
-  KK_FWD_PROJ_SLAB = 20,   // same, reading the all-to-all #2 receive layout
-  KK_FWD_P2D = 21,         // 2D x-forward + truncation (K5) when a narrower tile is registered
-  KK_INV_KX_PEER = 22,     // 3D K1, rows stored straight into the peers' all-to-all #1 receive buffers
-  KK_FWD_P_PEER = 23,      // K4, rows stored straight into the peers' all-to-all #2 receive buffers
-  KK_COUNT = 24
+  KK_FWD_P2D = 19,         // 2D x-forward + truncation (K5) when a narrower tile is registered
+  KK_INV_KX_PEER = 20,     // 3D K1, rows stored straight into the peers' all-to-all #1 receive buffers
+  KK_FWD_P_PEER = 21,      // K4, rows stored straight into the peers' all-to-all #2 receive buffers
+  KK_COUNT = 22
 };
 
 struct KEntry {
@@ -38,7 +36,6 @@ struct KEntry {
   int nt;    // threads per block
   int cols;  // columns per block (strided) / complex columns capacity (z)
   int smem;  // dynamic shared memory bytes
-  int persistent = 0;  // z pass: grid-stride over pencil pairs (grid = resident CTAs)
   int ppc = 2;         // z pass: pencils per CTA (k_zpass_ns3p: 1)
 };
 
@@ -76,9 +73,7 @@ struct GenCols {
     t[KK_FWD_P_PEER] = SRK_ENTRY((k_colpass<SE, PK_FWD, -1, PF_CTN | PF_BOUT | PF_PEER>), SE, SL::SIZE * 16); \
     t[KK_INV_CURLY] = SRK_ENTRY((k_colpass<SE, PK_INV_CURLY, +1, PF_CTN>), SE, SRK_RHS_SMEM(M, CS)); \
     t[KK_INV_CURLY_SLAB] = SRK_ENTRY((k_colpass<SE, PK_INV_CURLY, +1, PF_CTN | PF_BIN>), SE,       \
-                                     SRK_RHS_SMEM(M, CS));                                         \
-    t[KK_FWD_PROJ] = SRK_ENTRY((k_xfwd_proj<SE, PF_CTN>), SE, SL::SIZE * 16);                      \
-    t[KK_FWD_PROJ_SLAB] = SRK_ENTRY((k_xfwd_proj<SE, PF_CTN | PF_BIN>), SE, SL::SIZE * 16);
+                                     SRK_RHS_SMEM(M, CS));
 
 // Instantiate every kernel kind for one fast FFT length.
 #define SRK_DEFINE_SIZE(NAME, M, E, CS, ...) SRK_DEFINE_SIZE_F(NAME, M, E, CS, E, (__VA_ARGS__), __VA_ARGS__)
@@ -177,20 +172,12 @@ struct GenCols {
     using ZL = ColTile<M, 3>;                                                                      \
     using EI = FastFFT<M, 24, ZL, SRK_UNPAREN IR>;                                                 \
     t[KK_Z_NS3] = KEntry{(const void*)(k_zpass_ns3p<M, ZL, EI, ZOP_NS3, SRK_UNPAREN FR>), M / 8, 3,          \
-                         (int)(ZL::SIZE * 16) + EI::TWN * 16, 0, 1};                               \
-  }
-// same with E = 12 in the inverse prefix (M/4 threads, one fused-middle row each)
-#define SRK_NS3P12(M, IR, FR)                                                                      \
-  {                                                                                                \
-    using ZL = ColTile<M, 3>;                                                                      \
-    using EI = FastFFT<M, 12, ZL, SRK_UNPAREN IR>;                                                 \
-    t[KK_Z_NS3] = KEntry{(const void*)(k_zpass_ns3p<M, ZL, EI, ZOP_NS3, SRK_UNPAREN FR>), M / 4, 3,          \
-                         (int)(ZL::SIZE * 16) + EI::TWN * 16, 0, 1};                               \
+                         (int)(ZL::SIZE * 16) + EI::TWN * 16, 1};                                  \
   }
 #define SRK_NS3F(M, IR, EF, FR)                                                                     \
   {                                                                                                \
     using ZL = ColTile<M, 6>;                                                                           \
     using EI = FastFFT<M, 24, ZL, SRK_UNPAREN IR>;                                                 \
     t[KK_Z_NS3] = KEntry{(const void*)(k_zpass_ns3f<M, ZL, EI, EF, SRK_UNPAREN FR>), M / 4, 6,      \
-                         (int)(ZL::SIZE * 16) + EI::TWN * 16, 0};                                  \
+                         (int)(ZL::SIZE * 16) + EI::TWN * 16, 2};                                  \
   }

@@ -47,7 +47,6 @@ struct Table {
 std::mutex g_mu;
 std::map<int, Table>* g_fast = nullptr;
 Table* g_generic = nullptr;
-std::map<const void*, int> g_smem_set;
 
 void init_registry() {
   std::lock_guard<std::mutex> lk(g_mu);
@@ -107,14 +106,8 @@ int get_entry(int kind, int M, KEntry& e, GenPlan& gp) {
 }
 
 int ensure_smem(const KEntry& e) {
-  if (e.smem <= 48 * 1024) return SRK_OK;
-  std::lock_guard<std::mutex> lk(g_mu);
-  auto it = g_smem_set.find(e.fn);
-  if (it != g_smem_set.end()) return SRK_OK;
-  cudaError_t err = cudaFuncSetAttribute(e.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, e.smem);
+  cudaError_t err = srk_ensure_smem(e.fn, e.smem);  // per (device, kernel)
   if (err != cudaSuccess) return fail(SRK_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(err));
-
-  g_smem_set[e.fn] = 1;
   return SRK_OK;
 }
 
@@ -192,13 +185,7 @@ int need_ws(srk_plan* p) {
 }
 
 // ---- strided pass launch -------------------------------------------------
-int curly_xblk(int X) {
-  int want = 2;
-  if (const char* e = getenv("SRK_XBLK")) want = atoi(e);
-  for (int b = want; b > 1; --b)
-    if (X % b == 0) return b;
-  return 1;
-}
+int curly_xblk(int X) { return X % 2 == 0 ? 2 : 1; }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
 typedef CUresult (*srk_encode_tiled_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -209,7 +196,6 @@ srk_encode_tiled_fn encode_tiled() {
   static srk_encode_tiled_fn fn = [] {
     void* f = nullptr;
     cudaDriverEntryPointQueryResult q;
-    if (getenv("SRK_NO_TMA")) return (srk_encode_tiled_fn) nullptr;  // A/B switch: cp.async staging
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
         q != cudaDriverEntryPointSuccess)
       return (srk_encode_tiled_fn) nullptr;
@@ -218,12 +204,7 @@ srk_encode_tiled_fn encode_tiled() {
   return fn;
 }
 
-CUtensorMapL2promotion promo() {
-  static const int v = getenv("SRK_TMA_PROMO") ? atoi(getenv("SRK_TMA_PROMO")) : 3;
-  return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
-                : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-                         : v == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-}
+CUtensorMapL2promotion promo() { return CU_TENSOR_MAP_L2_PROMOTION_L2_256B; }
 
 // Tensor map of a strided pass's input: 4D {2*kc doubles, ngrp column groups,
 // rows, planes} based at the chunk's first column, box {2*C, 1, rows/nb <= 256,
@@ -265,9 +246,6 @@ void setup_tma(int kind, int cols, PassArgs& a, CUtensorMap* tm) {
                    kind == KK_FWD_P2D;
   const bool slab_in = kind == KK_INV_CURLY_SLAB || kind == KK_INV_P_SLAB;  // blocked input rows
   if (!(inv || fwd || slab_in) || !g_fast->count(a.M)) return;
-  static const int skip_mask = getenv("SRK_TMA_SKIP") ? atoi(getenv("SRK_TMA_SKIP")) : 0;  // experiments
-  if (a.in_rpb > 0 && getenv("SRK_NO_TMA5")) return;
-  if (skip_mask & (1 << kind)) return;
   if ((kind == KK_INV_KX || kind == KK_INV_KX_SLAB || kind == KK_INV_KX_PEER) && a.comp_stride != a.in_plane_stride)
     return;
   const int rows = fwd ? a.M : a.n;
@@ -288,7 +266,7 @@ void setup_tma(int kind, int cols, PassArgs& a, CUtensorMap* tm) {
 void setup_tma_out(int kind, int cols, PassArgs& a, CUtensorMap* tm) {
   a.tma_out = 0;
   const bool inv = kind == KK_INV_CURLY || kind == KK_INV_CURLY_SLAB;  // see kTMAO in k_colpass
-  if (!inv || a.out_rpb != 0 || !g_fast->count(a.M) || getenv("SRK_NO_TMAO")) return;
+  if (!inv || a.out_rpb != 0 || !g_fast->count(a.M)) return;
   const int nb = (a.M + 255) / 256;
   if (a.M % nb) return;
   const int box = a.M / nb;
@@ -316,17 +294,9 @@ void normalise_cols(PassArgs& a, int cols) {
 }
 
 // NS3 z-pass L2 warm-up distance: one wave of resident CTAs (2 per SM); measured
-// 9.48 -> 9.24 ms at 512^3 (SRK_ZPF overrides, 0 disables).
-int zpass_prefetch_distance() {
-  static const int d = [] {
-    if (const char* e = getenv("SRK_ZPF")) return atoi(e);
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    return 2 * sms;
-  }();
-  return d;
-}
+// 9.48 -> 9.24 ms at 512^3.  One-pencil kernels recompute it from their own
+// occupancy in launch_z.
+int zpass_prefetch_distance() { return 2 * srk_sm_count(); }
 
 int launch_col(srk_plan* p, int kind, PassArgs a, cudaStream_t st) {
   const bool padded_kind = kind == KK_INV_P || kind == KK_FWD_P || kind == KK_INV_RHS || kind >= KK_INV_RHS_SLAB;
@@ -347,53 +317,11 @@ int launch_col(srk_plan* p, int kind, PassArgs a, cudaStream_t st) {
   memset(&tmo, 0, sizeof(tmo));
   setup_tma_out(kind, e.cols, a, &tmo);
   void* args[] = {&a, &tm, &tmo};
-  static const int smem_pad = getenv("SRK_SMEM_PAD") ? atoi(getenv("SRK_SMEM_PAD")) : 0;  // experiments: occupancy
-  if (smem_pad) {
-    e.smem += smem_pad;
-    cudaFuncSetAttribute(e.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, e.smem);
-  }
   cudaError_t err = cudaLaunchKernel(e.fn, dim3((unsigned)grid), dim3(e.nt), args, e.smem, st);
   if (err != cudaSuccess) return fail(SRK_ERR_CUDA, std::string("colpass launch: ") + cudaGetErrorString(err));
   p->last_launches++;
   if (p->timing && p->nev < 16) cudaEventRecord(p->ev[p->nev++], st);
   return SRK_OK;
-}
-
-// ---- fused x-forward + projection over clusters of So CTAs --------------------
-int launch_fwd_proj(srk_plan* p, int kind, PassArgs a, cudaStream_t st) {
-  KEntry e;
-  int rc = get_entry(kind, a.M, e, a.gp);
-  if (rc) return rc;
-  if (!e.fn || !g_fast->count(a.M)) return fail(SRK_ERR_UNSUPPORTED, "no fused projection kernel");
-  if ((rc = get_tw(p, a.M, &a.tw))) return rc;
-  if ((rc = ensure_smem(e))) return rc;
-  a.tpp = (a.Qp + e.cols - 1) / e.cols;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(a.planes * a.tpp));
-  cfg.blockDim = dim3(e.nt);
-  cfg.dynamicSmemBytes = e.smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = a.planes;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  void* args[] = {&a};
-  cudaError_t err = cudaLaunchKernelExC(&cfg, e.fn, args);
-  if (err != cudaSuccess) return fail(SRK_ERR_CUDA, std::string("fused projection launch: ") + cudaGetErrorString(err));
-  p->last_launches++;
-  if (p->timing && p->nev < 16) cudaEventRecord(p->ev[p->nev++], st);
-  return SRK_OK;
-}
-
-// Opt-in (SRK_FUSEPROJ=1): measured slower than K5 + K6 on B200 at 512^3
-// (6.2 ms vs 2.3 + 2.0 ms; DSMEM reads of the peer tiles and cluster
-// co-scheduling cost more than the 6.5 GB of G traffic they save).
-bool use_fused_proj(const srk_plan* p) {
-  init_registry();
-  return getenv("SRK_FUSEPROJ") && g_fast->count(p->m0) && g_fast->at(p->m0).e[KK_FWD_PROJ].fn;
 }
 
 // ---- z pass launch (pairs of pencils) ---------------------------------------
@@ -404,25 +332,8 @@ int launch_z(srk_plan* p, int kind, ZArgs a, int S_rt, int So_rt, cudaStream_t s
   if ((rc = get_tw(p, a.M, &a.tw))) return rc;
   if ((rc = ensure_smem(e))) return rc;
   int grid = e.ppc == 1 ? a.P : (a.P + 1) / 2;
-  if (e.ppc == 1 && a.pf_dist) {  // L2 warm-up one wave of resident CTAs ahead (in pencils)
-    static const int d1 = [&] {
-      if (const char* s = getenv("SRK_ZPF1")) return atoi(s);
-      int per_sm = 0, dev = 0, nsm = 148;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, e.fn, e.nt, e.smem);
-      return std::max(1, per_sm) * nsm;
-    }();
-    a.pf_dist = d1;
-  }
-  if (e.persistent && !getenv("SRK_NOPERSIST")) {
-    int per_sm = 0, dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, e.fn, e.nt, e.smem);
-    if (getenv("SRK_DEBUG")) fprintf(stderr, "srk: persistent z-pass %d CTAs/SM x %d SMs\n", per_sm, nsm);
-    grid = std::min(grid, std::max(1, per_sm) * nsm);
-  }
+  if (e.ppc == 1 && a.pf_dist)  // L2 warm-up one wave of resident CTAs ahead (in pencils)
+    a.pf_dist = srk_blocks_per_sm(e.fn, e.nt, e.smem) * srk_sm_count();
   void* args[] = {&a, &S_rt, &So_rt};
   cudaError_t err = cudaLaunchKernel(e.fn, dim3(grid), dim3(e.nt), args, e.smem, st);
   if (err != cudaSuccess) return fail(SRK_ERR_CUDA, std::string("zpass launch: ") + cudaGetErrorString(err));
@@ -822,24 +733,6 @@ int rhs_impl(srk_plan* p, const void* y_, void* f_, double nu, double ri, double
   c5.scale = std::pow(1.0 / 1.5, d);
   c5.zero_nyq = 1;
   c5.zero_dc_imag = 1;
-  if (use_fused_proj(p)) {  // K5 + K6 fused over a thread-block cluster (DSMEM)
-    c5.y = y;
-    c5.f = f;
-    c5.density = p->density;
-    c5.nu = nu;
-    c5.ri = ri;
-    c5.re_pr = re_pr;
-    c5.dims = d;
-    c5.K = p->K;
-    c5.n1g = p->n1g;
-    c5.y0 = p->y0;
-    c5.ck0 = p->ck0;
-    c5.ck1 = p->ck1;
-    c5.ck2 = p->ck2;
-    c5.comp_stride = p->modes;
-    if ((rc = launch_fwd_proj(p, KK_FWD_PROJ, c5, st))) return rc;
-    return cs ? comb_after(p, cs, f, st) : SRK_OK;
-  }
   int k5 = KK_FWD_P;
   if (d == 2) {  // 2D: a narrower x-forward tile where one is registered (more CTAs per SM)
     init_registry();
@@ -868,7 +761,7 @@ int rhs_impl(srk_plan* p, const void* y_, void* f_, double nu, double ri, double
     if (p->timing && p->nev < 16) cudaEventRecord(p->ev[p->nev++], st);
     return check_launch("k_project_tma (refresh)");
   }
-  if (cs && !getenv("SRK_NO_PCOMB")) {
+  if (cs) {
     pa.yb = cs->yb;
     pa.nt = cs->nt;
     for (int j = 0; j < cs->nt; ++j) {
@@ -1167,22 +1060,6 @@ int srk_slab_finish(srk_plan* p, const void* recv2, const void* y, void* f, doub
   c5.zero_nyq = 1;
   c5.zero_dc_imag = 1;
   c5.y0 = p->y0;
-  if (use_fused_proj(p)) {
-    c5.y = (const cplx*)y;
-    c5.f = (cplx*)f;
-    c5.density = p->density;
-    c5.nu = nu;
-    c5.ri = ri;
-    c5.re_pr = re_pr;
-    c5.dims = p->dims;
-    c5.K = p->K;
-    c5.n1g = p->n1g;
-    c5.ck0 = p->ck0;
-    c5.ck1 = p->ck1;
-    c5.ck2 = p->ck2;
-    c5.comp_stride = p->modes;
-    return launch_fwd_proj(p, KK_FWD_PROJ_SLAB, c5, st);
-  }
   if ((rc = launch_col(p, KK_FWD_P_SLABI, c5, st))) return rc;
   ProjArgs pa{};
   pa.g = geom(p);

@@ -44,7 +44,6 @@ def reduce_sums(grid: Grid, y1, fl=None, y0=None, terms=(), tol_abs=0.0, tol_rel
     lib = _native.load()
     h = get_plan(grid).h if plan is None else plan
     ncomp = y1.shape[0] if ncomp is None else ncomp
-    host = host and not _native.NO_HOST_RESULT
     out = _native.host_result(9) if host else torch.empty(9, dtype=torch.float64, device=y1.device)
     Fs = [t for _, t in terms]
     cs = [c for c, _ in terms]

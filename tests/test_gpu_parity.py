@@ -472,17 +472,6 @@ def test_work_precision_sweep_small():
     assert {p.rhs_evals for p in pts if p.integrator == "rk4"} == {10 * 4 + 1}
 
 
-def test_fused_cluster_projection_matches(monkeypatch):
-    """Opt-in K5+K6 fusion over a thread-block cluster (DSMEM) gives the same RHS."""
-    og = O.OGrid((64, 64, 64))
-    y = dev(O.hit(og, a=4.0, energy=0.5, seed=2))
-    g = srk.Grid((64, 64, 64))
-    f0 = srk.FlowRHS(g, srk.PhysParams(500.0))(0.0, y)
-    monkeypatch.setenv("SRK_FUSEPROJ", "1")
-    f1 = srk.FlowRHS(g, srk.PhysParams(500.0))(0.0, y)
-    assert rel(f1, f0) <= 1e-15
-
-
 @pytest.mark.parametrize("P,shape", [(2, (32, 32, 32)), (3, (32, 48, 16)), (4, (64, 64, 64)),
                                      (8, (64, 64, 64)), (2, (256, 256, 256))])
 def test_slab_peer_stores_emulated_ranks_match_single_gpu(P, shape):
