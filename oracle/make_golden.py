@@ -1,6 +1,6 @@
 """Generate golden vectors by running the REFERENCE itself (build container only).
 
-    PYTHONDONTWRITEBYTECODE=1 python oracle/make_golden.py
+    PYTHONDONTWRITEBYTECODE=1 python oracle/make_golden.py [--round2]
 
 Imports ``spectralrk`` read-only from /root/reference/pkg/src and writes small
 fixtures to tests/golden/.  /root/reference does not exist on the GPU box; the
@@ -131,6 +131,45 @@ def trajectories(srk):
     return out
 
 
+def round2_cases(srk):
+    """Round-2 pins: AB2 trajectories (simulation.py:274-310, integrators.py:361-363)
+    incl. the uneven-tail RK4 restart, and 3D Boussinesq at fast-plan sizes --
+    a Rayleigh-Taylor RHS (problems.py:65-82, z-Nyquist content) and RK4 / BS5
+    windows through the reference driver."""
+    out = {}
+
+    def run(shape, kind, re, integ, mode, t_end, h=None, tol=None, lengths=None, **kw):
+        spec = srk.ProblemSpec(kind=kind, params=srk.PhysParams(reynolds=re), **kw)
+        c = srk.RunConfig(grid_shape=shape, problem=spec, integrator=integ, mode=mode, t_end=t_end, h=h,
+                          lengths=lengths)
+        if tol is not None:
+            c.tol_abs = c.tol_rel = tol
+        return srk.run_simulation(c)
+
+    # AB2: TG 32^3, 10 full steps + a 0.005 tail (RK4 restart)
+    r = run((32, 32, 32), "taylor_green", 1600.0, "ab2", "fixed", 0.105, h=0.01)
+    out["ab2_tg32"] = dict(y=r.state.fields, rec=_records(r))
+    # AB2: 2D RT Boussinesq 16x64 (density in the multistep update)
+    L = srk.default_lengths("rayleigh_taylor", (16, 64))
+    r = run((16, 64), "rayleigh_taylor", 1600.0, "ab2", "fixed", 0.2, h=0.01, lengths=L)
+    out["ab2_rt2d"] = dict(y=r.state.fields, rec=_records(r))
+    # 3D RT Boussinesq 32x32x64 (padded lengths 48, 48, 96: fast plans)
+    shape = (32, 32, 64)
+    L = srk.default_lengths("rayleigh_taylor", shape)
+    g = srk.Grid(shape, L)
+    y = srk.rayleigh_taylor_init(g, srk.ProblemSpec(kind="rayleigh_taylor", amplitude=0.05)).fields + 0.0
+    rng = np.random.default_rng(33)
+    y[:3] = 0.01 * (rng.standard_normal((3,) + g.kshape) + 1j * rng.standard_normal((3,) + g.kshape))
+    p = srk.PhysParams(reynolds=800.0, richardson=1.0, prandtl=0.7)
+    out["rt3d_rhs"] = dict(y=y, f=srk.FlowRHS(g, p, density=True)(0.0, y), shape=np.array(shape),
+                           lengths=np.array(L))
+    r = run(shape, "rayleigh_taylor", 1600.0, "rk4", "fixed", 0.05, h=0.01, lengths=L)
+    out["rt3d_rk4"] = dict(y=r.state.fields, rec=_records(r))
+    r = run(shape, "rayleigh_taylor", 1600.0, "bs5", "adaptive", 0.3, tol=1e-6, lengths=L)
+    out["rt3d_bs5"] = dict(y=r.state.fields, rec=_records(r))
+    return out
+
+
 def ics(srk):
     out = {}
     g = srk.Grid((16, 16, 16))
@@ -178,11 +217,16 @@ def main():
 
     srk = _ref()
     os.makedirs(OUT, exist_ok=True)
+    if "--round2" in sys.argv:  # only the round-2 file (the earlier fixtures stay as committed)
+        _save("r2_cases.npz", round2_cases(srk))
+        print("wrote r2_cases.npz")
+        return
     _save("rhs_cases.npz", rhs_cases(srk))
     _save("dealias_cases.npz", dealias_cases(srk))
     _save("ics.npz", ics(srk))
     _save("trajectories.npz", trajectories(srk))
     _save("io_cases.npz", io_cases(srk))
+    _save("r2_cases.npz", round2_cases(srk))
     man = dict(reference="spectralrk " + srk.__version__, numpy=np.__version__,
                scipy=scipy.__version__, generator="oracle/make_golden.py")
     with open(os.path.join(OUT, "MANIFEST.json"), "w") as fh:

@@ -23,7 +23,7 @@ __all__ = [
     "error_norm_delta", "propose_step", "Ctrl", "CtrlState", "adaptive_advance",
     "NonFinite", "Underflow", "ForcingErr", "taylor_green", "rayleigh_taylor",
     "hit", "rt_tanh_ic", "Record", "run_fixed", "run_adaptive", "replay_steps",
-    "set_fft_workers",
+    "set_fft_workers", "ab2_combine", "run_ab2",
 ]
 
 _WORKERS = 1
@@ -732,6 +732,57 @@ def run_fixed(f, y, g, tab, h, t_end, max_steps=None):
         else:
             fnow = f(t, y)
             ev += 1
+        recs.append(_rec(t, hi, y, fnow, g, ev, 0))
+    return y, recs
+
+
+def ab2_combine(y, h, f_curr, f_prev):
+    """integrators.py:361-363 (numpy's association and rounding)."""
+    return y + h * (1.5 * f_curr - 0.5 * f_prev)
+
+
+def run_ab2(f, y, g, h, t_end, max_steps=None):
+    """_run_ab2 (simulation.py:274-310), t0 = 0: one RK4 bootstrap step, then
+    AB2 from the cached slopes; an uneven tail step restarts with RK4."""
+    rk4 = tableau("rk4")
+    fnow = f(0.0, y)
+    ev = 1
+    t = 0.0
+    recs = [_rec(t, h, y, fnow, g, ev, 0)]
+    n_full = int(np.floor(t_end / h + 1e-9))
+    h_last = t_end - n_full * h
+    if h_last < 1e-12 * h:
+        h_last = 0.0
+    total = n_full + (1 if h_last > 0.0 else 0)
+    if max_steps is not None:
+        total = min(total, max_steps)
+    if total == 0:
+        return y, recs
+
+    def time_at(i):
+        return t_end if i >= n_full else (i + 1) * h
+
+    h0 = h if n_full > 0 else h_last
+    o = rk_step(f, y, t, h0, rk4, fnow)
+    ev += o.evals
+    f_prev = fnow
+    y = o.y_new
+    t = time_at(0)
+    fnow = f(t, y)
+    ev += 1
+    recs.append(_rec(t, h0, y, fnow, g, ev, 0))
+    for i in range(1, total):
+        hi = h if i < n_full else h_last
+        if hi != h:
+            o = rk_step(f, y, t, hi, rk4, fnow)
+            ev += o.evals
+            y = o.y_new
+        else:
+            y = ab2_combine(y, h, fnow, f_prev)  # no finiteness check here (as the reference)
+        f_prev = fnow
+        t = time_at(i)
+        fnow = f(t, y)
+        ev += 1
         recs.append(_rec(t, hi, y, fnow, g, ev, 0))
     return y, recs
 

@@ -13,7 +13,7 @@ from .spectral import (DealiasWorkspace, curl, dealiased_product, forward_transf
                        zero_nyquist, zero_self_conjugate_imag)
 from .physics import (FlowRHS, FlowState, ForcingError, PhysParams, apply_forcing, boussinesq_rhs,
                       leray_project, ns_rhs)
-from .integrators import (ButcherPair, NonFiniteStateError, StepOutcome, ab2_combine, make_bs5, make_dp5,
+from .integrators import (ButcherPair, NonFiniteStateError, StepOutcome, ab2_combine, ab2_step, make_bs5, make_dp5,
                           make_kcl5, make_pair, make_rk4, rk_step)
 from .control import (AdvanceOutcome, ControllerConfig, ControllerState, StepSizeUnderflowError,
                       adaptive_advance, error_norm, error_norm_delta, propose_step, scale_vector)

@@ -38,9 +38,11 @@ inline std::map<int, int>& sms() {
 }  // namespace srk_host
 
 // cudaFuncAttributeMaxDynamicSharedMemorySize >= bytes on the current device,
-// set once per (device, kernel) and only raised.
+// set once per (device, kernel) and only raised.  Set even below 48 KB: the
+// default limit counts static shared memory too (a 48 KB dynamic ring plus an
+// mbarrier needs the opt-in).
 inline cudaError_t srk_ensure_smem(const void* fn, int bytes) {
-  if (bytes <= 48 * 1024) return cudaSuccess;
+  if (bytes <= 0) return cudaSuccess;
   const int dev = srk_current_device();
   std::lock_guard<std::mutex> lk(srk_host::mu());
   auto& m = srk_host::smem_set();

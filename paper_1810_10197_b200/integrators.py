@@ -19,7 +19,7 @@ from . import _native
 from .spectral import from_device, to_device
 
 __all__ = ["NonFiniteStateError", "ButcherPair", "StepOutcome", "make_rk4", "make_dp5", "make_bs5",
-           "make_kcl5", "make_pair", "rk_step", "combine", "ab2_combine"]
+           "make_kcl5", "make_pair", "rk_step", "combine", "ab2_combine", "ab2_step"]
 
 
 class NonFiniteStateError(RuntimeError):
@@ -265,7 +265,33 @@ def rk_step(f, y, t, h, pair, first_stage=None):
 
 
 def ab2_combine(y, h, f_curr, f_prev):
-    """y + h (1.5 f_curr - 0.5 f_prev) (integrators.py:361-363)."""
-    if isinstance(y, torch.Tensor):
-        return y + h * (1.5 * f_curr - 0.5 * f_prev)
-    return y + h * (1.5 * f_curr - 0.5 * f_prev)
+    """y + h (1.5 f_curr - 0.5 f_prev) on the device (integrators.py:361-363).
+
+    Two srk_combine passes in the reference's association: g = 1.5 f_curr +
+    (-0.5) f_prev (0 + 1.5 f is exact, x + (-y) == x - y), then y + h g --
+    bitwise numpy's rounding of ``y + h * (1.5 * f_curr - 0.5 * f_prev)``.
+    numpy inputs are moved to the device and the result comes back as numpy."""
+    yd, was_np = to_device(y, torch.complex128)
+    fc = to_device(f_curr, torch.complex128)[0]
+    fp = to_device(f_prev, torch.complex128)[0]
+    g = combine(None, [(1.5, fc), (-0.5, fp)])
+    return from_device(combine(yd, [(float(h), g)], out=g), was_np)
+
+
+def ab2_step(f, y, t, h, f_prev):
+    """One AB2 step (integrators.py:366-381): returns (y_new, f_curr)."""
+    from .diagnostics import reduce_sums
+    from .grid import Grid
+
+    if f_prev is None:
+        raise ValueError("ab2_step requires the previous slope; bootstrap first")
+    yd, was_np = to_device(y, torch.complex128)
+    fd = _as_dev_fn(f)
+    f_curr = fd(t, yd)
+    y_new = ab2_combine(yd, h, f_curr, to_device(f_prev, torch.complex128)[0])
+    kshape = tuple(yd.shape[1:])
+    grid = Grid(kshape[:-1] + (2 * (kshape[-1] - 1),))
+    q = reduce_sums(grid, y_new, flags=0, ncomp=yd.shape[0], host=True).tolist()
+    if q[6] > 0:
+        raise NonFiniteStateError(f"non-finite state at t={t}")
+    return from_device(y_new, was_np), from_device(f_curr, was_np)

@@ -301,7 +301,7 @@ def _run_fixed(drv, max_steps=None):
 
 
 def _run_ab2(drv, h, t_end, max_steps=None):
-    from .integrators import ab2_combine, combine
+    from .integrators import ab2_combine
 
     total, n_full, h_last, time_at = _fixed_step_times(drv, h, t_end)
     if max_steps is not None:
@@ -325,7 +325,7 @@ def _run_ab2(drv, h, t_end, max_steps=None):
             drv.evals += ev
             drv.y = y_new
         else:
-            drv.y = combine(drv.y, [(h * 1.5, drv.f_now), (-h * 0.5, f_prev)])
+            drv.y = ab2_combine(drv.y, h, drv.f_now, f_prev)  # reference association (integrators.py:361-363)
         f_prev = drv.f_now
         drv.t = time_at(i)
         drv.after_accept(None, fsal_ok=False)

@@ -103,3 +103,42 @@ def test_enstrophy_consistent_with_eps():
     f = O.OracleRHS(g, re)(0.0, y)
     eps = O.dissipation_rate(y, f, g)
     assert abs(eps - 2.0 / re * O.enstrophy(y, g)) <= 1e-8 * abs(eps)
+
+
+R2 = load_golden("r2_cases")
+
+
+def test_oracle_ab2_tg_with_uneven_tail():
+    """AB2 (simulation.py:274-310): RK4 bootstrap, AB2 steps, RK4 restart on the tail."""
+    g = O.OGrid((32, 32, 32))
+    y, recs = O.run_ab2(O.OracleRHS(g, 1600.0), O.taylor_green(g), g, 0.01, 0.105)
+    _check_traj(y, recs, R2["ab2_tg32"])
+
+
+def test_oracle_ab2_rt2d():
+    shape = (16, 64)
+    g = O.OGrid(shape, (2 * np.pi, 2 * np.pi * 64 / 16))
+    y, recs = O.run_ab2(O.OracleRHS(g, 1600.0, density=True), O.rayleigh_taylor(g), g, 0.01, 0.2)
+    _check_traj(y, recs, R2["ab2_rt2d"])
+
+
+def test_oracle_ab2_update_is_the_reference_expression(rng):
+    y, fc, fp = (rng.standard_normal((3, 8, 5)) + 1j * rng.standard_normal((3, 8, 5)) for _ in range(3))
+    assert np.array_equal(O.ab2_combine(y, 0.013, fc, fp), y + 0.013 * (1.5 * fc - 0.5 * fp))
+
+
+def test_oracle_rt3d_rhs():
+    c = R2["rt3d_rhs"]
+    g = O.OGrid(tuple(c["shape"]), tuple(c["lengths"]))
+    f = O.OracleRHS(g, 800.0, ri=1.0, pr=0.7, density=True)(0.0, c["y"])
+    assert rel(f, c["f"]) <= 1e-14
+
+
+def test_oracle_rt3d_rk4_and_bs5_windows():
+    shape = (32, 32, 64)
+    g = O.OGrid(shape, (2 * np.pi, 2 * np.pi, 4 * np.pi))
+    f = O.OracleRHS(g, 1600.0, density=True)
+    y, recs = O.run_fixed(f, O.rayleigh_taylor(g), g, O.tableau("rk4"), 0.01, 0.05)
+    _check_traj(y, recs, R2["rt3d_rk4"])
+    y, recs, _ = O.run_adaptive(f, O.rayleigh_taylor(g), g, O.tableau("bs5"), O.Ctrl(), 1e-3, 0.3)
+    _check_traj(y, recs, R2["rt3d_bs5"])
