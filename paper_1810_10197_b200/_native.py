@@ -11,7 +11,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libsrk.so")
+# SRK_LIB_PATH: load another build of the same sources (A/B timing of a change, tools/ab_lib.sh)
+LIB_PATH = os.environ.get("SRK_LIB_PATH") or os.path.join(_HERE, "_lib", "libsrk.so")
 
 SRK_OK = 0
 SRK_ERR_INVALID = 1

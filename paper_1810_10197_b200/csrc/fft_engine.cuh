@@ -18,6 +18,8 @@
 // reference's own tests; one thread per column, local-memory ping-pong.
 #pragma once
 
+#include <type_traits>
+
 #include "srk_common.cuh"
 
 // ---------------------------------------------------------------------------
@@ -155,6 +157,46 @@ __device__ __forceinline__ void stage_twiddle(cplx* v, const cplx* tw, unsigned 
   static_assert(R <= 32, "stage_twiddle covers radices up to 32");
 }
 
+// Shared-memory-lean twiddles for the z passes, which are bound by the SM's
+// shared-memory datapath (128 B/clk, shuffles included -- tools/probe_peaks.py),
+// not by the fp64 pipe: one table read (w^1) per butterfly, every other power
+// formed in registers (w^2 = (w^1)^2, w^4 = (w^2)^2, w^8, w^16 likewise;
+// w^(a+b) = w^a w^b).  A few roundings more than stage_twiddle (~1e-16
+// relative per product); the table reads they replace were ~9% of the z-pass's
+// shared-memory wavefronts (ncu, v15).
+SRK_DEV cplx csq(cplx a) { return make_double2(fma(a.x, a.x, -a.y * a.y), fma(a.x, a.y, a.x * a.y)); }
+template <int M, int R, int SIGN>
+__device__ __forceinline__ void stage_twiddle_sq(cplx* v, const cplx* tw, unsigned kts) {
+  static_assert(R <= 32, "stage_twiddle_sq covers radices up to 32");
+  constexpr int B = R < 8 ? R : 8;
+  cplx wb[8];
+  wb[1] = tw_pow<M, SIGN>(tw, kts);
+#pragma unroll
+  for (int b = 2; b < B; ++b) wb[b] = ((b & (b - 1)) == 0) ? csq(wb[b / 2]) : cmul(wb[b & (b - 1)], wb[b & -b]);
+#pragma unroll
+  for (int b = 1; b < B; ++b) v[b] = cmul(v[b], wb[b]);
+  if constexpr (R > 8) {
+    const cplx w8 = csq(wb[4]);
+    const cplx w16 = (R > 16) ? csq(w8) : w8;
+#pragma unroll
+    for (int a = 1; 8 * a < R; ++a) {
+      const cplx wa = a == 1 ? w8 : (a == 2 ? w16 : cmul(w8, w16));
+      v[8 * a] = cmul(v[8 * a], wa);
+#pragma unroll
+      for (int b = 1; b < 8 && 8 * a + b < R; ++b) v[8 * a + b] = cmul(v[8 * a + b], cmul(wa, wb[b]));
+    }
+  }
+}
+
+// First-stage loaders may take the compile-time row range of the 32-lane group
+// (rlo, rhi: the rows j + t*STRIDE can reach for any lane): a loader that knows
+// which rows are structurally zero (the 3/2-rule zero band of a padded inverse)
+// then skips their shared-memory reads at compile time.
+template <class T, class = void>
+struct ld_has_range : std::false_type {};
+template <class T>
+struct ld_has_range<T, decltype(void(T::kRange))> : std::true_type {};
+
 template <bool WS, int TPC>
 __device__ __forceinline__ void stage_sync() {
   if constexpr (WS && TPC <= 32)
@@ -257,7 +299,10 @@ struct FastStageW {
 #pragma unroll
       for (int b = 0; b < NB; ++b) {
         const int j = tj + b * TPC;
-        if constexpr (FIRST) {
+        if constexpr (FIRST && ld_has_range<LD>::value) {
+#pragma unroll
+          for (int t = 0; t < R; ++t) v[b][t] = ld(j + t * STRIDE, col, t * STRIDE + b * TPC, t * STRIDE + b * TPC + TPC - 1);
+        } else if constexpr (FIRST) {
 #pragma unroll
           for (int t = 0; t < R; ++t) v[b][t] = ld(j + t * STRIDE, col);
         } else if constexpr (STRIDE % 8 == 0) {
@@ -280,7 +325,7 @@ struct FastStageW {
         if constexpr (Ls > 1) {
           constexpr int TS = M / (Ls * R);
           const unsigned kts = k * (unsigned)TS;
-          stage_twiddle<M, R, SIGN>(v[b], tw, kts);
+          stage_twiddle_sq<M, R, SIGN>(v[b], tw, kts);
         }
         DFT<R, SIGN>::run(v[b]);
       }
@@ -444,7 +489,7 @@ struct OneStageZ {
     }
     const unsigned k = (unsigned)j % (unsigned)Ls;
     if (act) {
-      stage_twiddle<M, R, SIGN>(v, tw, k * (unsigned)(M / (Ls * R)));
+      stage_twiddle_sq<M, R, SIGN>(v, tw, k * (unsigned)(M / (Ls * R)));
       DFT<R, SIGN>::run(v);
     }
     __syncthreads();

@@ -686,6 +686,49 @@ __global__ void __launch_bounds__(Eng::NT, (PPC == 1 && Eng::NT <= 128 ? 3 : (En
 
 
 // ---------------------------------------------------------------------------
+// First-stage loader of the fused z-passes: Hermitian extension of the staged
+// rows (K stored modes each) onto the padded axis and two-for-one packing of
+// real signals 2c, 2c+1 into complex column c.  With the row range of the lane
+// group known at compile time (ld_has_range), rows in the 3/2-rule zero band
+// [K, M-K+1) are never read and pure head / tail groups drop the selects (the
+// inverse's staged-row reads were ~19% of the z-pass's shared-memory traffic).
+// irfft ignores Im of the DC mode (2k == M cannot occur inside the padded band).
+// ---------------------------------------------------------------------------
+template <int M>
+struct ZHermLoad {
+  static constexpr int kRange = 1;
+  static constexpr int K = M / 3 + 1;
+  const cplx* stg;
+  __device__ __forceinline__ static cplx pack(cplx A, cplx B) { return cmk(A.x - B.y, A.y + B.x); }
+  __device__ __forceinline__ cplx head(int k, int c) const {
+    cplx A = stg[(2 * c) * K + k], B = stg[(2 * c + 1) * K + k];
+    if (k == 0) A.y = B.y = 0.0;
+    return pack(A, B);
+  }
+  __device__ __forceinline__ cplx tail(int k, int c) const {
+    const cplx A = stg[(2 * c) * K + (M - k)], B = stg[(2 * c + 1) * K + (M - k)];
+    return pack(cmk(A.x, -A.y), cmk(B.x, -B.y));
+  }
+  __device__ __forceinline__ cplx operator()(int k, int c) const {
+    const bool hd = k < K, tl = k >= M - (K - 1);
+    const int kk = hd ? k : (tl ? M - k : 0);
+    cplx A = stg[(2 * c) * K + kk], B = stg[(2 * c + 1) * K + kk];
+    if (tl) {
+      A.y = -A.y;
+      B.y = -B.y;
+    }
+    if (k == 0) A.y = B.y = 0.0;
+    return (hd || tl) ? pack(A, B) : cmk(0.0, 0.0);
+  }
+  __device__ __forceinline__ cplx operator()(int k, int c, int rlo, int rhi) const {
+    if (rlo >= K && rhi < M - (K - 1)) return cmk(0.0, 0.0);  // zero band: no read
+    if (rhi < K) return head(k, c);
+    if (rlo >= M - (K - 1)) return tail(k, c);
+    return (*this)(k, c);
+  }
+};
+
+// ---------------------------------------------------------------------------
 // NS3 z-pass with a fused middle stage (fast plans only).  Inverse plan
 // (IR..., 4), forward plan (4, FR...), E = 24, M/4 threads (= 6 columns x
 // M/24).  Thread j runs the last inverse radix-4 butterfly of all 6 complex
@@ -739,21 +782,9 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
   cp_async_wait_all();
   __syncthreads();
   SRK_TS(1)
-  auto hs = [&](int g, int k) -> cplx {
-    const bool head = k < K;
-    const bool tail = k >= M - (K - 1);
-    const int kk = head ? k : (tail ? M - k : 0);
-    cplx X = stg[g * K + kk];
-    X.y = tail ? -X.y : X.y;
-    if (k == 0) X.y = 0.0;  // irfft ignores Im of DC (2k == M cannot occur in the padded band)
-    return (head || tail) ? X : cmk(0.0, 0.0);
-  };
   // ---- inverse prefix stages (Stockham, in place) ----
   {
-    auto ld = [&](int k, int c) -> cplx {
-      cplx A = hs(2 * c, k), B = hs(2 * c + 1, k);
-      return cmk(A.x - B.y, A.y + B.x);
-    };
+    ZHermLoad<M> ld{stg};
     auto st = [&](int n, int c, cplx v) { sm[L::idx(n, c)] = v; };
     EngI::template run_ws<+1, true, true>(a.gp, sm, twp, S, ld, st);
   }
@@ -775,11 +806,10 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
       }
     }
     cplx w[4];
-#pragma unroll
-    for (int t = 1; t < 4; ++t) {
-      w[t] = tw_get<M>(twp, (unsigned)(t * j));
-      w[t].y = -w[t].y;  // inverse sign
-    }
+    w[1] = tw_get<M>(twp, (unsigned)j);
+    w[1].y = -w[1].y;  // inverse sign
+    w[2] = csq(w[1]);
+    w[3] = cmul(w[2], w[1]);
     __syncthreads();
     double o[4][6];
 #pragma unroll
@@ -888,7 +918,7 @@ struct LoopStageZ {
           for (int t = 0; t < R; ++t) v[b][t] = sm[L::idx(j + t * STRIDE, col)];
         }
         const unsigned k = (unsigned)j % (unsigned)Ls;
-        stage_twiddle<M, R, SIGN>(v[b], tw, k * (unsigned)(M / (Ls * R)));
+        stage_twiddle_sq<M, R, SIGN>(v[b], tw, k * (unsigned)(M / (Ls * R)));
         DFT<R, SIGN>::run(v[b]);
       }
     }
@@ -976,20 +1006,8 @@ __global__ void __launch_bounds__(EngI::NT, (OP == ZOP_B2 ? SRK_ZB2P_MINB : (M <
   cp_async_wait_all();
   __syncthreads();
   SRK_TS(1)
-  auto hs = [&](int g, int k) -> cplx {
-    const bool head = k < K;
-    const bool tail = k >= M - (K - 1);
-    const int kk = head ? k : (tail ? M - k : 0);
-    cplx X = stg[g * K + kk];
-    X.y = tail ? -X.y : X.y;
-    if (k == 0) X.y = 0.0;  // irfft ignores Im of DC
-    return (head || tail) ? X : cmk(0.0, 0.0);
-  };
   {
-    auto ld = [&](int k, int c) -> cplx {
-      cplx A = hs(2 * c, k), B = hs(2 * c + 1, k);
-      return cmk(A.x - B.y, A.y + B.x);
-    };
+    ZHermLoad<M> ld{stg};
     auto st = [&](int n, int c, cplx v) { sm[L::idx(n, c)] = v; };
     EngI::template run_ws<+1, true, true>(a.gp, sm, twp, S, ld, st);
   }
@@ -1018,11 +1036,10 @@ __global__ void __launch_bounds__(EngI::NT, (OP == ZOP_B2 ? SRK_ZB2P_MINB : (M <
     for (int h = 0; h < RPT; ++h) {
       const int j = tid + h * NT;
       cplx w[4];
-#pragma unroll
-      for (int t = 1; t < 4; ++t) {
-        w[t] = tw_get<M>(twp, (unsigned)(t * j));
-        w[t].y = -w[t].y;  // inverse sign
-      }
+      w[1] = tw_get<M>(twp, (unsigned)j);
+      w[1].y = -w[1].y;  // inverse sign
+      w[2] = csq(w[1]);  // one table read per row (stage_twiddle_sq)
+      w[3] = cmul(w[2], w[1]);
 #pragma unroll
       for (int c = 0; c < S; ++c) {
 #pragma unroll
