@@ -9,9 +9,12 @@ invalidated by the forcing, simulation.py:165-182).  The metric is RK stages
 
     python bench.py                       # N=1, 512^3, K=10, W=3
     python bench.py --impl reference      # CPU oracle port (the reference's algorithm)
-    torchrun --nproc-per-node N bench.py --gpus N   # y-slab decomposed N^3 over N GPUs (strong scaling)
+    python bench.py --gpus N              # re-launches itself under torchrun: N ranks, y-slab
+                                          # decomposed N^3 (strong scaling); at N >= 4 also a
+                                          # 1024^3 leg with SURVEY M4's E_P
+    torchrun --nproc-per-node N bench.py --gpus N   # the same, launched by the caller
+    python bench.py --gpus 2 --dry-run    # launcher check on CPU (gloo ranks, no GPU work)
     python bench.py --mode slab --grid 256  # the slab path on one GPU (NCCL world of 1)
-    torchrun ... bench.py --mode replicas # N independent replicas (weak scaling)
 """
 
 from __future__ import annotations
@@ -50,18 +53,24 @@ def parse():
                          "into K1 / K4 (row blocks stored into the peers' receive buffers over CUDA IPC)")
     ap.add_argument("--mode", default="auto", choices=["auto", "single", "slab", "replicas"],
                     help="auto: single GPU at N=1, slab decomposition (strong scaling) for N>1")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher / rank plumbing only: gloo ranks on the CPU, no GPU work (tests)")
+    ap.add_argument("--no-1024", action="store_true", help="N >= 4: skip the 1024^3 E_P leg")
     return ap.parse_args()
 
 
 def model_bytes(n):
-    """SURVEY §8(d) M3 byte model (3/2-rule padded algorithm, complex128)."""
+    """SURVEY §8(d) M3 byte model (3/2-rule padded algorithm, complex128) for the
+    stage fraction; per kernel, the bytes each launch of this implementation must
+    move: K1 writes 5 x-padded signals [u0, u1, u2, kx u1, kx u2] (the curl is
+    finished in K2), K2 reads those 5 and writes 6."""
     m, k = 3 * n // 2, n // 2 + 1
     sc, sx, sxy = n * n * k, m * n * k, m * m * k
     b_rhs = 16 * (9 * sc + 18 * sx + 18 * sxy)
     f = 3 * sc * 16
     per_kernel = {  # algorithmic bytes each kernel of srk_rhs must move
-        "K1_xinv_curl": 16 * (3 * sc + 6 * sx),
-        "K2_yinv": 16 * (6 * sx + 6 * sxy),
+        "K1_xinv_curl": 16 * (3 * sc + 5 * sx),
+        "K2_yinv": 16 * (5 * sx + 6 * sxy),
         "K3_z_c2r_cross_r2c": 16 * (6 * sxy + 3 * sxy),
         "K4_yfwd": 16 * (3 * sxy + 3 * sx),
         "K5_xfwd": 16 * (3 * sx + 3 * sc),
@@ -77,6 +86,64 @@ def peaks():
         return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def lib_sha256():
+    import hashlib
+
+    from paper_1810_10197_b200 import _native
+
+    h = hashlib.sha256()
+    with open(_native.LIB_PATH, "rb") as fh:
+        for blk in iter(lambda: fh.read(1 << 22), b""):
+            h.update(blk)
+    return h.hexdigest()
+
+
+def ncu_counters(n, kernel):
+    """Per-launch ncu counters of `kernel` at N = n from profiles/ncu_kernels.json,
+    only if that capture was taken of the libsrk.so loaded now (sha256 match);
+    otherwise None -- stale counters are never reported."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_kernels.json")) as fh:
+            d = json.load(fh)
+    except Exception:
+        return None, "no profiles/ncu_kernels.json"
+    if d.get("lib_sha256") != lib_sha256():
+        return None, "profiles/ncu_kernels.json was captured from another libsrk.so build"
+    e = d.get(str(n), {}).get(kernel)
+    return e, d.get("report")
+
+
+def probe_peaks():
+    """Live on-chip ceilings (srk_probe, burst): fp64 FMA rate and the shared-memory
+    datapath (16 B loads), for the z-pass's non-HBM roofline."""
+    import ctypes
+
+    import torch
+
+    from paper_1810_10197_b200 import _native
+
+    lib = _native.load()
+    nsm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    scratch = torch.zeros(64 * nsm, dtype=torch.float64, device="cuda")
+    out = {}
+    for mode, iters, key in ((0, 20000, "fp64"), (2, 4000, "smem")):
+        ops = ctypes.c_double(0)
+        best = None
+        for _ in range(4):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            _native.check(lib.srk_probe(mode, iters, 4, _native.ptr(scratch), _native.stream_ptr(),
+                                        ctypes.byref(ops)), "srk_probe")
+            e1.record()
+            e1.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        out[key] = 2 * ops.value / (best * 1e-3) / 1e12 if mode == 0 else 16 * ops.value / (best * 1e-3) / 1e9
+    return {"fp64_tflops": out["fp64"], "smem_GBps": out["smem"],
+            "source": "srk_probe in this process: 8 independent DFMA chains / conflict-free 16 B shared loads, "
+                      "4 CTAs x 256 threads per SM, best of 4 launches"}
 
 
 class ClockSampler:
@@ -184,13 +251,19 @@ def cpu_sample(n_target, steps=1, n_sample=128, workers=None):
                 gpts_stage_per_s=evals / dt * pts / 1e9)
 
 
+CPU_SAMPLE_N = 128  # both CPU legs: one forced BS5 step on 128^3, scaled by points to N^3
+
+
 def run_reference(args, rank, world):
+    """The reference's own algorithm on the host cores (oracle port: the reference is
+    Python, nothing to compile into oracle/_ref), all cores, each step one forced
+    BS5 step at 128^3 (~6 s at 16 workers) scaled by points to the bench's N^3."""
     if rank != 0:
         return
     steps_per = 1
     vals = []
     for i in range(args.warmup + args.steps):
-        r = cpu_sample(args.n, steps=steps_per, n_sample=64 if args.n >= 64 else args.n)
+        r = cpu_sample(args.n, steps=steps_per, n_sample=min(args.n, CPU_SAMPLE_N))
         if i >= args.warmup:
             vals.append(r)
     v = statistics.median([r["value"] for r in vals])
@@ -200,7 +273,8 @@ def run_reference(args, rank, world):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded HIT spectrum, a=4, E=0.5)",
         "config": {"workload": f"forced_hit_bs5_{args.n}^3", "n": args.n, "nu": 5e-4, "tol": 1e-6, "k_f": 2.0},
         "cpu_baseline": {"value": v, "unit": "stages/s", "cores": vals[-1]["cores"], "kind": "port",
-                         "sample": vals[-1]["sample"]},
+                         "sample": vals[-1]["sample"], "scaled_from": f"{min(args.n, CPU_SAMPLE_N)}^3",
+                         "gpts_stage_per_s": statistics.median([r["gpts_stage_per_s"] for r in vals])},
         "e2e": {"value": v, "unit": "stages/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -311,21 +385,28 @@ def run_native(args, rank, world, local_rank):
     dom = int(np.argmax(kms))
     peak, peak_src = peaks()
     achieved = mb["per_kernel"][kn[dom]] / (kms[dom] * 1e-3) / 1e9
-    traffic = None
+    # ncu counters of the dominant kernel, only from a capture of this very binary
+    cnt, cnt_src = ncu_counters(n, kn[dom])
+    traffic = cnt.get("dram_bytes") if cnt else None
+    # The z-pass is not bound by HBM: the SM's shared-memory datapath (128 B/clk,
+    # shuffles included) and the fp64 pipe are its ceilings.  Live
+    # probe peaks; the kernel's wavefront / fp64-instruction counts per launch come
+    # from the sha-matched ncu capture.
+    ceil = None
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_dram_bytes.json")) as fh:
-            traffic = json.load(fh).get(str(n), {}).get(kn[dom])
-    except Exception:
-        pass
-    # The FFT passes are bound by fp64 issue latency, not HBM (DESIGN.md §6,
-    # tools/l2_probe.py): the ncu fp64-pipe activity of the dominant kernel from
-    # the committed profile, when one exists for this size.
-    fp64 = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_fp64_pipe.json")) as fh:
-            fp64 = json.load(fh).get(str(n), {}).get(kn[dom])
-    except Exception:
-        pass
+        pk = probe_peaks()
+        ceil = {"probe": pk}
+        if cnt and cnt.get("smem_wavefronts") is not None:
+            sm_gbps = cnt["smem_wavefronts"] * 128 / (kms[dom] * 1e-3) / 1e9
+            ceil["smem"] = {"achieved_GBps": sm_gbps, "peak_GBps": pk["smem_GBps"],
+                            "frac": sm_gbps / pk["smem_GBps"], "wavefronts_per_launch": cnt["smem_wavefronts"]}
+        if cnt and cnt.get("fp64_flops") is not None:
+            tf = cnt["fp64_flops"] / (kms[dom] * 1e-3) / 1e12
+            ceil["fp64"] = {"achieved_tflops": tf, "peak_tflops": pk["fp64_tflops"], "frac": tf / pk["fp64_tflops"],
+                            "flops_per_launch": cnt["fp64_flops"],
+                            "counted_as": "2 per DFMA + 1 per DADD/DMUL thread instruction (ncu sass counters)"}
+    except Exception as exc:  # the probe is evidence, never a reason to lose the line
+        ceil = {"error": str(exc)}
 
     # ---- e2e: through the public API with the state resident on the host ----
     # The state crosses PCIe every step (hostio.HostMirror, pinned): y is copied
@@ -401,8 +482,13 @@ def run_native(args, rank, world, local_rank):
         return
     cpu = None
     if world == 1 and not args.no_cpu:
-        cpu = cpu_sample(n, steps=1, n_sample=min(n, 128))
-        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        ns = min(n, CPU_SAMPLE_N)
+        c_all = cpu_sample(n, steps=1, n_sample=ns)
+        c_one = cpu_sample(n, steps=1, n_sample=ns, workers=1)
+        cpu = {k: c_all[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        cpu["scaled_from"] = f"{ns}^3"
+        cpu["one_core"] = {"value": c_one["value"], "unit": "stages/s", "cores": 1, "sample": c_one["sample"],
+                           "note": "BASELINE.md primary: the reference is single-threaded by default"}
     stage_frac = mb["b_stage_bs5"] * (value / world) / (peak * 1e9)
     line = {
         "metric": METRIC, "value": value, "unit": "stages/s", "n_gpus": world, "steps": args.steps,
@@ -421,7 +507,9 @@ def run_native(args, rank, world, local_rank):
                      "kernel_ms": {k: round(float(v), 4) for k, v in zip(kn, kms)},
                      "kernel_share": {k: round(float(v), 4) for k, v in zip(kn, shares)},
                      "algorithmic_bytes_per_launch": mb["per_kernel"][kn[dom]],
-                     "fp64_pipe_active": fp64},
+                     "traffic_source": cnt_src,
+                     "fp64_pipe_active": cnt.get("fp64_pipe") if cnt else None,
+                     "on_chip_ceilings": ceil},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
@@ -600,6 +688,17 @@ def run_slab(args, rank, world, local_rank):
                        "adaptive_advance (BS5, rank-order sums) + forcing, y_new slab device->host overlapped "
                        "with the FSAL stage; bytes are per rank"}
 
+    big = None
+    rhs_peer, rhs_chunks = rhs.peer, len(rhs.chunks)
+    if world >= 4 and n == 512 and not args.no_1024:
+        rhs.close()
+        del s, rhs, b, yk, fk
+        if not args.no_e2e:
+            del s2, mirror, yd
+        try:
+            big = leg_1024(args, rank, world)
+        except Exception as exc:  # evidence leg: never lose the main line
+            big = {"workload": "forced_hit_bs5_1024^3", "error": repr(exc)[:300]}
     if rank != 0:
         return
     names = ["K1 (forward)", "K2-K4 (middle)", "K5-K6 (finish)"]
@@ -610,8 +709,8 @@ def run_slab(args, rank, world, local_rank):
         "data": "synthetic (device-side seeded HIT-spectrum slabs, E=0.5)",
         "config": {"workload": f"forced_hit_bs5_{n}^3", "n": n, "nu": 5e-4, "tol": 1e-6, "k_f": 2.0,
                    "parallelism": (f"y-slab x{world}, exchange fused into K1/K4 (peer stores over CUDA IPC)"
-                                   if rhs.peer else
-                                   f"y-slab x{world}, NCCL all-to-all, {len(rhs.chunks)} kz chunks pipelined"),
+                                   if rhs_peer else
+                                   f"y-slab x{world}, NCCL all-to-all, {rhs_chunks} kz chunks pipelined"),
                    "l2": "inputs larger than L2"},
         "gpts_stage_per_s": value * n ** 3 / 1e9,
         "rhs_evals": evals,
@@ -620,19 +719,184 @@ def run_slab(args, rank, world, local_rank):
                      "traffic": None, "kernel": names[dom], "peak_source": peak_src,
                      "phase_ms": {"forward": ph[0], "a2a1": ph[1], "middle": ph[2], "a2a2": ph[3],
                                   "finish": ph[4], "serial_rhs": float(sum(ph[:5])),
-                                  "pipelined_rhs": ph[5], "kz_chunks": len(rhs.chunks)}},
+                                  "pipelined_rhs": ph[5], "kz_chunks": rhs_chunks}},
         "nvlink": {"bytes_per_rhs_per_gpu": a2a_bytes, "achieved_GBps": a2a_bytes / (a2a_ms * 1e-3) / 1e9
                    if world > 1 else None, "peak_GBps": 770.0, "peak_source": "B200_PROFILING.md peer copy"},
         "cpu_baseline": None, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
     }
+    if big is not None:
+        line["strong_1024"] = big
+    assert line["n_gpus"] == args.gpus
     print(json.dumps(line), flush=True)
+
+
+def single_gpu_ms_per_stage(n, steps, warmup):
+    """ms per RHS evaluation of the single-GPU forced-HIT BS5 loop (run_native's step)."""
+    import torch
+
+    import paper_1810_10197_b200 as srk
+
+    g = srk.Grid((n, n, n))
+    params = srk.PhysParams(reynolds=2000.0)
+    rhs = srk.FlowRHS(g, params)
+    pair, cfg = srk.make_bs5(), srk.ControllerConfig(tol_abs=1e-6, tol_rel=1e-6)
+    y = srk.hit_init(g, srk.ProblemSpec("hit", a=4.0, energy=0.5, seed=42)).fields
+    s = dict(y=y, t=0.0, f=rhs(0.0, y), ctrl=srk.ControllerState(h=1e-3))
+    a21 = float(pair.A[1, 0])
+
+    def step():
+        out = srk.adaptive_advance(s["y"], s["t"], pair, s["ctrl"], cfg, rhs, first_stage=s["f"], grid=g,
+                                   second_input=s.get("y2"))
+        srk.apply_forcing(out.y_new, g, 0.5, 2.0, energy_sum=out.diag_sums[4])
+        h = s["ctrl"].h
+        f, y2, _ = rhs.refresh(out.t_new, out.y_new, h * a21)
+        s.update(y=out.y_new, t=out.t_new, f=f, y2=(h, y2))
+        return out.rhs_evals + 1
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    ev = sum(step() for _ in range(steps))
+    e1.record()
+    e1.synchronize()
+    return e0.elapsed_time(e1) / ev
+
+
+def slab_ms_per_stage(args, n, steps, warmup, rank, world):
+    """ms per RHS evaluation (max over ranks) of the y-slab BS5 loop at N = n."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1810_10197_b200 as srk
+    from paper_1810_10197_b200.diagnostics import reduce_sums
+    from paper_1810_10197_b200.slab import SlabFlowRHS, dist_sum_in_rank_order, hit_slab
+
+    g = srk.Grid((n, n, n))
+    red = dist_sum_in_rank_order()
+    rhs = SlabFlowRHS(g, srk.PhysParams(reynolds=2000.0), rank, world, chunks=4, peer=args.exchange == "peer")
+    plan = rhs.backend.h
+    pair, cfg = srk.make_bs5(), srk.ControllerConfig(tol_abs=1e-6, tol_rel=1e-6)
+    y = hit_slab(g, rank, world, a=4.0, energy=0.5, seed=42, allreduce=red)
+    s = dict(y=y, t=0.0, f=rhs(0.0, y), ctrl=srk.ControllerState(h=1e-3))
+
+    def step():
+        out = srk.adaptive_advance(s["y"], s["t"], pair, s["ctrl"], cfg, rhs, first_stage=s["f"], grid=g,
+                                   allreduce=red, plan=plan)
+        srk.apply_forcing(out.y_new, g, 0.5, 2.0, plan=plan, allreduce=red, slab=(rank, world),
+                          energy_sum=out.diag_sums[4])
+        f = rhs(out.t_new, out.y_new)
+        red(reduce_sums(g, out.y_new, fl=f, flags=2, ncomp=3, plan=plan))
+        s.update(y=out.y_new, t=out.t_new, f=f)
+        return out.rhs_evals + 1
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    ev = sum(step() for _ in range(steps))
+    e1.record()
+    e1.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / ev], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    rhs.close()
+    return t.item()
+
+
+def leg_1024(args, rank, world):
+    """SURVEY M4 at 1024^3 (does not fit one GPU): E_P = (B_stage(1024) / (P T_P)) /
+    (B_stage(512) / T_1(512)), T = time per RHS evaluation, T_1 measured here on
+    rank 0 with the single-GPU path, T_P with the y-slab path on all P ranks."""
+    import gc
+
+    import torch
+    import torch.distributed as dist
+
+    gc.collect()
+    torch.cuda.empty_cache()
+    t1 = torch.zeros(1, dtype=torch.float64, device="cuda")
+    if rank == 0:
+        t1[0] = single_gpu_ms_per_stage(512, steps=3, warmup=2)
+        gc.collect()
+        torch.cuda.empty_cache()
+    dist.broadcast(t1, 0)
+    need = 725e9 / world  # measured footprint of a 1024^3 y-slab BS5 run (DESIGN.md §7)
+    free = float(torch.cuda.mem_get_info()[0])
+    fits = torch.tensor([1.0 if free > 1.05 * need else 0.0], device="cuda")
+    dist.all_reduce(fits, op=dist.ReduceOp.MIN)
+    out = {"workload": "forced_hit_bs5_1024^3", "T1_512_ms_per_stage": t1.item(),
+           "need_GB_per_gpu": need / 1e9, "free_GB_per_gpu": free / 1e9}
+    if fits.item() < 1.0:
+        out["skipped"] = "1024^3 y-slab state does not fit this GPU count"
+        return out
+    tp = slab_ms_per_stage(args, 1024, steps=2, warmup=1, rank=rank, world=world)
+    b1024, b512 = model_bytes(1024)["b_stage_bs5"], model_bytes(512)["b_stage_bs5"]
+    out.update({"TP_ms_per_stage": tp, "stages_per_s": 1e3 / tp, "gpts_stage_per_s": 1024 ** 3 / (tp * 1e-3) / 1e9,
+                "E_P": (b1024 / (world * tp)) / (b512 / t1.item()), "P": world,
+                "E_P_definition": "SURVEY M4: per-GPU achieved model bandwidth at P GPUs (1024^3) / 1-GPU (512^3)"})
+    return out
+
+
+def free_port():
+    import socket
+
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def self_launch(args):
+    """`bench.py --gpus N` without a torchrun environment: re-run this command under
+    torch.distributed.run with N ranks (one per GPU) on 127.0.0.1; rank 0's JSON
+    line reaches our stdout."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "4")
+    return subprocess.call(cmd, env=env)
+
+
+def run_dry(args, rank, world):
+    """Launcher / rank plumbing check on the CPU (gloo): barrier, max-over-ranks
+    timing of a token host step, rank 0 prints the line shape the GPU run prints."""
+    import torch
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo")
+    x = torch.ones(1 << 16, dtype=torch.float64)
+    for _ in range(args.warmup):
+        x = x * 1.0000001
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        x = x * 1.0000001
+    dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64)
+    dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+    ranks = torch.tensor([1.0])
+    dist.all_reduce(ranks)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": "stages/s", "n_gpus": world,
+                          "ranks_seen": int(ranks.item()), "steps": args.steps, "warmup": args.warmup,
+                          "dry_run": True, "backend": "gloo", "max_rank_s": dt.item(),
+                          "config": {"workload": f"forced_hit_bs5_{args.n}^3"}}), flush=True)
+    dist.destroy_process_group()
 
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl != "reference" and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} ranks")
+    if args.dry_run:
+        run_dry(args, rank, world)
+        return
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -646,7 +910,7 @@ def main():
         torch.cuda.set_device(local_rank)
         if world == 1:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            os.environ.setdefault("MASTER_PORT", "29531")
+            os.environ.setdefault("MASTER_PORT", str(free_port()))
             os.environ.setdefault("RANK", "0")
             os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl")

@@ -124,6 +124,20 @@ int srk_leray_project(srk_plan* plan, const void* u, void* out, void* stream);
 int srk_combine(int64_t n, const void* y, int nterms, const void* const* F, const double* coef, void* out,
                 void* stream);
 
+/* Step-size-scaled variants for CUDA-graph replay of an RK attempt
+ * (integrators.py:322-347 with h read on the device): every coefficient is
+ * passed as the tableau value a (host array, baked into the graph) and used as
+ * (*h_dev) * a -- one rounding, bitwise the host product h * a of the unscaled
+ * calls.  h_dev: one double in device memory, updated before each replay. */
+int srk_combine_scaled(int64_t n, const void* y, int nterms, const void* const* F, const double* a,
+                       const double* h_dev, void* out, void* stream);
+int srk_rhs_combine_scaled(srk_plan* plan, const void* y, void* f, double nu, double ri, double re_pr,
+                           const void* ybase, int nterms, const void* const* F, const double* a, double a_self,
+                           const double* h_dev, void* ynext, void* stream);
+int srk_step_reduce_scaled(srk_plan* plan, const void* y0, const void* y1, int nterms, const void* const* F,
+                           const double* d, const double* h_dev, const void* fl, int ncomp, double tol_abs,
+                           double tol_rel, int flags, double* out_dev, void* stream);
+
 /* Fused embedded-error norm + diagnostics reduction (deterministic):
  *   flags & 1: error vector Delta = sum_j coef[j] F[j] (integrators.py:341-347),
  *              sc = tol_abs + max(|y0|,|y1|) tol_rel (control.py:51-57),

@@ -31,7 +31,7 @@ EXPORTS = (
     "srk_slab_forward_kz", "srk_slab_inverse_y_kz", "srk_slab_zpass", "srk_slab_forward_y_kz",
     "srk_slab_forward_x_kz", "srk_slab_project", "srk_store_mapped", "srk_slab_set_peers",
     "srk_slab_forward_kz_peer", "srk_slab_forward_y_kz_peer", "srk_ipc_export", "srk_ipc_import", "srk_ipc_close",
-    "srk_rhs_refresh", "srk_probe",
+    "srk_rhs_refresh", "srk_probe", "srk_combine_scaled", "srk_rhs_combine_scaled", "srk_step_reduce_scaled",
 )
 
 _lib = None
@@ -83,6 +83,11 @@ def load():
         "srk_band_scale": (c_int, [vp, vp, c_int, vp, c_int, c_dbl, vp]),
         "srk_store_mapped": (c_int, [vp, vp, c_int, vp]),
         "srk_probe": (c_int, [c_int, c_int, c_int, vp, vp, P(c_dbl)]),
+        "srk_combine_scaled": (c_int, [i64, vp, c_int, P(vp), P(c_dbl), vp, vp, vp]),
+        "srk_rhs_combine_scaled": (c_int, [vp, vp, vp, c_dbl, c_dbl, c_dbl, vp, c_int, P(vp), P(c_dbl), c_dbl, vp,
+                                           vp, vp]),
+        "srk_step_reduce_scaled": (c_int, [vp, vp, vp, c_int, P(vp), P(c_dbl), vp, vp, c_int, c_dbl, c_dbl, c_int,
+                                           vp, vp]),
         "srk_rhs_refresh": (c_int, [vp, vp, vp, c_dbl, c_dbl, c_dbl, c_dbl, vp, vp, vp]),
         "srk_slab_set_peers": (c_int, [vp, P(vp), P(vp), c_int]),
         "srk_slab_forward_kz_peer": (c_int, [vp, vp, c_int, c_int, vp]),

@@ -18,6 +18,12 @@ __device__ __forceinline__ cplx rmul(double s, cplx a) { return make_double2(DMU
 __device__ __forceinline__ cplx radd(cplx a, cplx b) { return make_double2(DADD(a.x, b.x), DADD(a.y, b.y)); }
 __device__ __forceinline__ cplx rsub(cplx a, cplx b) { return make_double2(DSUB(a.x, b.x), DSUB(a.y, b.y)); }
 
+// coefficient j of a combination: c[j], or (*hs) * c[j] when the step size lives
+// in device memory (graph replays); one rounding either way
+__device__ __forceinline__ double coef(const double* c, const double* hs, int j) {
+  return hs ? DMUL(__ldg(hs), c[j]) : c[j];
+}
+
 struct KVec {
   double k[3];
   double k2, inv_k2;
@@ -143,6 +149,10 @@ __global__ void __launch_bounds__(proj_chunk<DIMS, DENS, NTC, DIAG>()) k_project
   static_assert(NS == proj_streams<DIMS, DENS, NTC, DIAG>(), "stream count");
   static_assert(!DIAG || NTC == 0, "refresh: the state's own next-stage input only");
   double e_acc = 0.0, ep_acc = 0.0, z_acc = 0.0;  // DIAG: E, eps, Z partial sums of this thread
+  double cf[NTC > 0 ? NTC : 1];
+#pragma unroll
+  for (int t = 0; t < (NTC > 0 ? NTC : 0); ++t) cf[t] = coef(a.c, a.hs, t);
+  const double cself = a.hs ? DMUL(__ldg(a.hs), a.cself) : a.cself;
   __shared__ __align__(8) unsigned long long mb[2];
   const int tid = threadIdx.x;
   const long long n = a.modes;
@@ -222,8 +232,8 @@ __global__ void __launch_bounds__(proj_chunk<DIMS, DENS, NTC, DIAG>()) k_project
           cplx acc = DIAG ? u : st[(NG + NY + j) * CH + tid];
 #pragma unroll
           for (int t = 0; t < (NTC < 0 ? 0 : NTC); ++t)
-            acc = radd(acc, rmul(a.c[t], st[(NG + NY + (DIAG ? 0 : NY) + t * NY + j) * CH + tid]));
-          a.ynext[j * n + i] = radd(acc, rmul(a.cself, o));
+            acc = radd(acc, rmul(cf[t], st[(NG + NY + (DIAG ? 0 : NY) + t * NY + j) * CH + tid]));
+          a.ynext[j * n + i] = radd(acc, rmul(cself, o));
         }
       }
       if constexpr (DENS) {
@@ -237,8 +247,8 @@ __global__ void __launch_bounds__(proj_chunk<DIMS, DENS, NTC, DIAG>()) k_project
           cplx acc = DIAG ? rho : st[(NG + NY + d) * CH + tid];
 #pragma unroll
           for (int t = 0; t < (NTC < 0 ? 0 : NTC); ++t)
-            acc = radd(acc, rmul(a.c[t], st[(NG + 2 * NY + t * NY + d) * CH + tid]));
-          a.ynext[d * n + i] = radd(acc, rmul(a.cself, o));
+            acc = radd(acc, rmul(cf[t], st[(NG + 2 * NY + t * NY + d) * CH + tid]));
+          a.ynext[d * n + i] = radd(acc, rmul(cself, o));
         }
       }
     }
@@ -336,11 +346,14 @@ __global__ void k_leray(const GeomArgs g, const cplx* __restrict__ u, cplx* __re
 // per multiply and per add (y == nullptr starts from zeros, :343-347).
 template <int NT>
 __global__ void k_combine(const CombArgs a) {
+  double cf[NT > 0 ? NT : 1];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) cf[j] = coef(a.c, a.hs, j);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.n;
        i += (long long)gridDim.x * blockDim.x) {
     cplx acc = a.y ? a.y[i] : make_double2(0.0, 0.0);
 #pragma unroll
-    for (int j = 0; j < NT; ++j) acc = radd(acc, rmul(a.c[j], a.F[j][i]));
+    for (int j = 0; j < NT; ++j) acc = radd(acc, rmul(cf[j], a.F[j][i]));
     a.out[i] = acc;
   }
 }
@@ -393,6 +406,9 @@ __global__ void __launch_bounds__(SRK_RT_CH) k_reduce_tma(const RedArgs a) {
   double acc[SRK_NQ];
 #pragma unroll
   for (int q = 0; q < SRK_NQ; ++q) acc[q] = 0.0;
+  double cf[NT > 0 ? NT : 1];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) cf[j] = coef(a.c, a.hs, j);
   if (tid == 0) {
     mbar_init(&mb[0], 1);
     mbar_init(&mb[1], 1);
@@ -440,7 +456,7 @@ __global__ void __launch_bounds__(SRK_RT_CH) k_reduce_tma(const RedArgs a) {
       if (a.do_norm) {
         cplx dl = make_double2(0.0, 0.0);
 #pragma unroll
-        for (int j = 0; j < NT; ++j) dl = radd(dl, rmul(a.c[j], st[(2 + j) * CH + tid]));
+        for (int j = 0; j < NT; ++j) dl = radd(dl, rmul(cf[j], st[(2 + j) * CH + tid]));
         const cplx y0 = st[CH + tid];
         const double sc = DADD(a.atol, DMUL(fmax(hypot(y0.x, y0.y), hypot(y1.x, y1.y)), a.rtol));
         const double rt = __ddiv_rn(hypot(dl.x, dl.y), sc);

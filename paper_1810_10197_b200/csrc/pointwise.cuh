@@ -31,6 +31,10 @@ struct ProjArgs {
   int nt;
   double cself;
   cplx* ynext;
+  // non-null: the coefficients are multiples of a step size held in device memory:
+  // every c[t] and cself is used as (*hs) * c (one rounding: exactly the host
+  // product h * a the reference forms) -- a CUDA graph replays with a new h
+  const double* hs;
   // k_project_tma<3, false, 0, true> (srk_rhs_refresh): ybase is the state itself
   // (not streamed) and the block partials of E, eps, Z over the velocity
   // components go to partial[q * gridDim.x + block] (q = 4, 5, 8; others 0)
@@ -41,6 +45,7 @@ struct CombArgs {
   const cplx* y;  // may be null (start from zero)
   const cplx* F[SRK_MAX_TERMS];
   double c[SRK_MAX_TERMS];
+  const double* hs;  // non-null: c[j] scaled by *hs in the kernel (ProjArgs::hs)
   int nt;
   cplx* out;
   long long n;
@@ -52,6 +57,7 @@ struct RedArgs {
   const cplx* y1;  // new state
   const cplx* F[SRK_MAX_TERMS];
   double c[SRK_MAX_TERMS];  // h*(b - b_hat) for the error vector
+  const double* hs;         // non-null: c[j] = (b - b_hat)_j scaled by *hs in the kernel
   int nt;
   const cplx* fl;  // tendency at y1 (diag)
   int fl_term;     // >= 0: fl is F[fl_term] (the FSAL stage): streamed once, read from that slot

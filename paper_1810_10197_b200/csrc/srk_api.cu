@@ -603,6 +603,7 @@ struct CombSpec {
   double cself;
   cplx* ynext;
   double* diag_out;  // srk_rhs_refresh: (E, eps, Z) sums of (y, f) -> out[4], [5], [8]
+  const double* hs;  // non-null: coefficients are multiples of the device step size *hs
 };
 int rhs_impl(srk_plan* p, const void* y_, void* f_, double nu, double ri, double re_pr, void* stream,
              const CombSpec* cs);
@@ -612,9 +613,29 @@ int srk_rhs(srk_plan* p, const void* y_, void* f_, double nu, double ri, double 
   return rhs_impl(p, y_, f_, nu, ri, re_pr, stream, nullptr);
 }
 
+namespace {
+int rhs_combine_impl(srk_plan* p, const void* y, void* f, double nu, double ri, double re_pr, const void* ybase,
+                     int nterms, const void* const* F, const double* coef, double coef_self, const double* hs,
+                     void* ynext, void* stream);
+}
+
 int srk_rhs_combine(srk_plan* p, const void* y, void* f, double nu, double ri, double re_pr, const void* ybase,
                     int nterms, const void* const* F, const double* coef, double coef_self, void* ynext,
                     void* stream) {
+  return rhs_combine_impl(p, y, f, nu, ri, re_pr, ybase, nterms, F, coef, coef_self, nullptr, ynext, stream);
+}
+
+int srk_rhs_combine_scaled(srk_plan* p, const void* y, void* f, double nu, double ri, double re_pr,
+                           const void* ybase, int nterms, const void* const* F, const double* a, double a_self,
+                           const double* h_dev, void* ynext, void* stream) {
+  if (!h_dev) return fail(SRK_ERR_INVALID, "srk_rhs_combine_scaled: null step-size pointer");
+  return rhs_combine_impl(p, y, f, nu, ri, re_pr, ybase, nterms, F, a, a_self, h_dev, ynext, stream);
+}
+
+namespace {
+int rhs_combine_impl(srk_plan* p, const void* y, void* f, double nu, double ri, double re_pr, const void* ybase,
+                     int nterms, const void* const* F, const double* coef, double coef_self, const double* hs,
+                     void* ynext, void* stream) {
   if (nterms < 0 || nterms + 1 > SRK_MAX_TERMS) return fail(SRK_ERR_INVALID, "srk_rhs_combine: at most 7 terms");
   if (!ynext || ynext == y || ynext == f) return fail(SRK_ERR_INVALID, "srk_rhs_combine: ynext must not alias y or f");
   CombSpec cs;
@@ -628,8 +649,10 @@ int srk_rhs_combine(srk_plan* p, const void* y, void* f, double nu, double ri, d
   }
   cs.cself = coef_self;
   cs.ynext = (cplx*)ynext;
+  cs.hs = hs;
   return rhs_impl(p, y, f, nu, ri, re_pr, stream, &cs);
 }
+}  // namespace
 
 int srk_rhs_refresh(srk_plan* p, const void* y, void* f, double nu, double ri, double re_pr, double coef_self,
                     void* ynext, double* diag_out, void* stream) {
@@ -661,6 +684,7 @@ int comb_after(srk_plan* p, const CombSpec* cs, const cplx* f, cudaStream_t st) 
   }
   a.F[cs->nt] = f;
   a.c[cs->nt] = cs->cself;
+  a.hs = cs->hs;
   a.nt = cs->nt + 1;
   a.out = cs->ynext;
   a.n = (long long)(p->dims + (p->density ? 1 : 0)) * p->modes;
@@ -770,6 +794,7 @@ int rhs_impl(srk_plan* p, const void* y_, void* f_, double nu, double ri, double
     }
     pa.cself = cs->cself;
     pa.ynext = cs->ynext;
+    pa.hs = cs->hs;
     fused = srk_launch_project_comb(pa, st);
   }
   if (!fused) srk_launch_project(pa, st);
@@ -856,11 +881,20 @@ int srk_leray_project(srk_plan* p, const void* u, void* out, void* stream) {
   return check_launch("k_leray");
 }
 
+int srk_combine_scaled(int64_t n, const void* y, int nterms, const void* const* F, const double* a_coef,
+                       const double* h_dev, void* out, void* stream);
+
 int srk_combine(int64_t n, const void* y, int nterms, const void* const* F, const double* coef, void* out,
                 void* stream) {
+  return srk_combine_scaled(n, y, nterms, F, coef, nullptr, out, stream);
+}
+
+int srk_combine_scaled(int64_t n, const void* y, int nterms, const void* const* F, const double* coef,
+                       const double* h_dev, void* out, void* stream) {
   if (nterms < 0 || nterms > SRK_MAX_TERMS) return fail(SRK_ERR_INVALID, "srk_combine: at most 8 terms");
   CombArgs a;
   memset(&a, 0, sizeof(a));
+  a.hs = h_dev;
   a.y = (const cplx*)y;
   for (int j = 0; j < nterms; ++j) {
     a.F[j] = (const cplx*)F[j];
@@ -873,9 +907,20 @@ int srk_combine(int64_t n, const void* y, int nterms, const void* const* F, cons
   return check_launch("k_combine");
 }
 
+int srk_step_reduce_scaled(srk_plan* p, const void* y0, const void* y1, int nterms, const void* const* F,
+                           const double* coef, const double* h_dev, const void* fl, int ncomp, double tol_abs,
+                           double tol_rel, int flags, double* out_dev, void* stream);
+
 int srk_step_reduce(srk_plan* p, const void* y0, const void* y1, int nterms, const void* const* F,
                     const double* coef, const void* fl, int ncomp, double tol_abs, double tol_rel, int flags,
                     double* out_dev, void* stream) {
+  return srk_step_reduce_scaled(p, y0, y1, nterms, F, coef, nullptr, fl, ncomp, tol_abs, tol_rel, flags, out_dev,
+                                stream);
+}
+
+int srk_step_reduce_scaled(srk_plan* p, const void* y0, const void* y1, int nterms, const void* const* F,
+                           const double* coef, const double* h_dev, const void* fl, int ncomp, double tol_abs,
+                           double tol_rel, int flags, double* out_dev, void* stream) {
   if (!p) return fail(SRK_ERR_INVALID, "null plan");
   if (nterms < 0 || nterms > SRK_MAX_TERMS) return fail(SRK_ERR_INVALID, "srk_step_reduce: at most 8 terms");
   if (ncomp < 1 || ncomp > 4) return fail(SRK_ERR_INVALID, "srk_step_reduce: 1..4 components");
@@ -891,6 +936,7 @@ int srk_step_reduce(srk_plan* p, const void* y0, const void* y1, int nterms, con
     a.F[j] = (const cplx*)F[j];
     a.c[j] = coef[j];
   }
+  a.hs = h_dev;
   a.fl = (const cplx*)fl;
   a.fl_term = -1;
   for (int j = 0; j < a.nt; ++j)

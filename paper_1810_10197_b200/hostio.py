@@ -79,8 +79,13 @@ class HostMirror:
             raise ValueError(f"HostMirror holds {self.shape} {self.dtype}, got {tuple(dev.shape)} {dev.dtype}")
 
     def load_host(self, src):
-        """Fill the host copy synchronously (numpy or CPU tensor); no push pending afterwards."""
+        """Fill the host copy synchronously (numpy or CPU tensor); no push pending afterwards.
+        The CPU write must not race queued copies on the mirror's own streams (a
+        push still writing the host copy, a pull still reading it), so the host
+        blocks on both before touching the pinned buffer."""
         self.wait()
+        self._d2h.synchronize()
+        self._h2d.synchronize()
         self.host.copy_(torch.as_tensor(src).reshape(self.shape))
         self._seg = [[(lo, hi, None, 0)] for (_, lo, hi) in self.chunks]
 

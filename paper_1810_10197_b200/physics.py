@@ -186,7 +186,18 @@ def apply_forcing(u_hat, grid: Grid, target_energy, k_f, plan=None, allreduce=No
 
     u = u_hat
     if not (isinstance(u, torch.Tensor) and u.is_cuda and u.is_contiguous()):
-        raise TypeError("apply_forcing works in place on a contiguous CUDA tensor")
+        # host arrays (the reference rescales numpy arrays in place): force a device
+        # copy and write the rescaled band back into the caller's array
+        if slab is not None:
+            raise TypeError("slab forcing works in place on the rank's CUDA slab")
+        ud, _ = to_device(u_hat, torch.complex128)
+        gamma = apply_forcing(ud, grid, target_energy, k_f, energy_sum=energy_sum)
+        host = ud.cpu()
+        if isinstance(u_hat, torch.Tensor):
+            u_hat.copy_(host.to(u_hat.dtype))
+        else:
+            np.copyto(u_hat, host.numpy())
+        return gamma
     if slab is None:
         idx, w, nb = forcing_band(grid, k_f, u.device)
         ph = get_plan(grid).h

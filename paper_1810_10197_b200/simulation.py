@@ -186,6 +186,7 @@ class _Driver:
             self.evals += 1
         self.records = []
         self.errs = []
+        self.graphs = False  # run_simulation decides (CUDA-graph replay of attempts)
         self.second_input = self.refresh_sums = None
         out_dir = getattr(config, "output_dir", None)
         self.out_dir = Path(out_dir) if out_dir else None
@@ -216,7 +217,9 @@ class _Driver:
     def record(self, h, sums=None):
         d = self.grid.dims
         if sums is None:
-            sums = reduce_sums(self.grid, self.y, fl=self.f_now, flags=2, ncomp=min(d, self.y.shape[0]), host=True).tolist()
+            # every component (density too) in the non-finite count; E / eps / Z stay
+            # over the velocity components (the kernel's dvel = min(dims, ncomp))
+            sums = reduce_sums(self.grid, self.y, fl=self.f_now, flags=2, ncomp=self.y.shape[0], host=True).tolist()
             if sums[6] > 0:
                 raise NonFiniteStateError(f"non-finite state at t={self.t}")
         e, eps, z = diag_from_sums(sums, self.grid)
@@ -341,6 +344,13 @@ def _run_adaptive(drv, max_steps=None):
     ctrl = ControllerState(h=drv.h_ctrl, prev_rejected=drv.prev_rejected, rejections=drv.rejections)
     a21 = float(pair.A[1, 0])
     drv.record(drv.h_ctrl)
+    # launch-bound sizes: replay each first attempt from a CUDA graph (graphs.py);
+    # unforced FSAL runs only (forcing refreshes f_now every step)
+    graph = None
+    if drv.graphs and pair.fsal and not cfg.forcing:
+        from .graphs import attempt_graph
+
+        graph = attempt_graph(drv.rhs, pair, cfg.controller, drv.grid)
     n = 0
     while drv.t < t_end and (max_steps is None or n < max_steps):
         remaining = t_end - drv.t
@@ -348,8 +358,11 @@ def _run_adaptive(drv, max_steps=None):
         h_saved = ctrl.h
         if clamped:
             ctrl.h = remaining
-        out = adaptive_advance(drv.y, drv.t, pair, ctrl, cfg.controller, drv.rhs, first_stage=drv.f_now,
-                               grid=drv.grid, second_input=drv.second_input)
+        if graph is not None and drv.second_input is None:
+            out = graph.advance(drv.y, drv.t, ctrl, drv.f_now)
+        else:
+            out = adaptive_advance(drv.y, drv.t, pair, ctrl, cfg.controller, drv.rhs, first_stage=drv.f_now,
+                                   grid=drv.grid, second_input=drv.second_input)
         drv.evals += out.rhs_evals
         drv.rejections += out.rejections
         drv.y = out.y_new
@@ -369,19 +382,28 @@ def _run_adaptive(drv, max_steps=None):
         drv.record(out.h_used, sums=out.diag_sums if fsal_used else drv.refresh_sums)
         drv.maybe_checkpoint()
         n += 1
+    if graph is not None:  # hand back buffers the graph will not overwrite
+        drv.y = drv.y.clone()
+        drv.f_now = drv.f_now.clone()
 
 
-def run_simulation(config, resume=None, initial_state=None, max_steps=None):
+USE_GRAPHS = True  # default for run_simulation(graphs=None)
+
+
+def run_simulation(config, resume=None, initial_state=None, max_steps=None, graphs=None):
     """simulation.py:350-368 on the device.
 
     ``resume``: CheckpointData (read_checkpoint) continuing a run bit-exactly.
     ``initial_state``: optional FlowState / array / callable(config) replacing
     make_initial_state (IC hook).  ``max_steps``: accepted-step cap
     (SURVEY D6).  With ``config.output_dir`` the diagnostics CSV, periodic and
-    final SRKL checkpoints are written like the reference.
+    final SRKL checkpoints are written like the reference.  ``graphs``: replay
+    each adaptive step's first attempt from a CUDA graph (default USE_GRAPHS;
+    bit-identical to the eager path, graphs.py).
     """
     config.validate()
     drv = _Driver(config, initial_state, resume)
+    drv.graphs = USE_GRAPHS if graphs is None else bool(graphs)
     if config.mode == "fixed":
         _run_fixed(drv, max_steps)
     else:

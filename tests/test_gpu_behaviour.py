@@ -187,6 +187,19 @@ def test_forcing_matches_oracle():
     assert np.abs(host(u) - un).max() <= 1e-15 * np.abs(un).max()
 
 
+def test_forcing_numpy_in_place_like_reference():
+    """physics.py:209-239 rescales a numpy array in place: same gamma and band as
+    the device path, the caller's array updated."""
+    g = srk.Grid((16, 16, 16))
+    og = O.OGrid((16, 16, 16))
+    un = host(_hit(g) * 0.8).copy()
+    ref = un.copy()
+    go = O.apply_forcing(ref, og, 1.0, 2.0)
+    gd = srk.apply_forcing(un, g, 1.0, 2.0)
+    assert abs(gd - go) <= 1e-14 * go
+    assert np.abs(un - ref).max() <= 1e-15 * np.abs(ref).max()
+
+
 # ---------------------------------------------------------------- rk_step known answers
 def _ode_state(val):
     return torch.full((1, 4, 4, 3), val, dtype=torch.complex128, device="cuda")
