@@ -11,6 +11,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <utility>
 
 inline int srk_current_device() {
   int d = 0;
@@ -81,4 +82,33 @@ inline int srk_blocks_per_sm(const void* fn, int nt, int smem) {
   std::lock_guard<std::mutex> lk(srk_host::mu());
   srk_host::occ()[{dev, fn, nt, smem}] = per_sm;
   return per_sm;
+}
+
+// Kernel launch with programmatic stream serialization (PDL, srk_common.cuh):
+// the kernel may begin while the previous kernel of the stream finishes; it
+// waits (pdl_wait) before touching data.
+inline cudaLaunchConfig_t srk_pdl_config(dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                         cudaLaunchAttribute* attr) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cfg;
+}
+inline cudaError_t srk_launch(const void* fn, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t st) {
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = srk_pdl_config(grid, block, smem, st, attr);
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t srk_launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                Args&&... args) {
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = srk_pdl_config(grid, block, smem, st, attr);
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }

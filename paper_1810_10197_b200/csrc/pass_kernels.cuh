@@ -185,9 +185,10 @@ __device__ __forceinline__ void tma_stage(cplx* sm, const CUtensorMap* tm, int w
 }
 
 template <class Eng, int KIND, int SIGN, int FL = 0>
-__global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 ? 3 : (Eng::NT <= 192 ? 2 : 1)))) k_colpass(const PassArgs a, const __grid_constant__ CUtensorMap tm,
+__global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 ? 3 : (Eng::NT <= 384 ? 2 : 1)))) k_colpass(const PassArgs a, const __grid_constant__ CUtensorMap tm,
                                                                   const __grid_constant__ CUtensorMap tmo) {
   extern __shared__ __align__(128) cplx smraw[];
+  pdl_launch_dependents();
   cplx* const sm = smraw + Eng::TWN;
   const cplx* const twp = Eng::kFast ? smraw : a.tw;
   if constexpr (Eng::kFast) tw_fill<Eng::M>(smraw, a.tw);  // ordered by the staging barrier
@@ -262,6 +263,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
     }
     __syncthreads();
   }
+  pdl_wait();  // the previous kernel's output is complete and visible from here on
 
   if constexpr (KIND == PK_INV) {
     const double sc = a.scale;
@@ -533,12 +535,14 @@ SRK_DEV void zphys(const double* r, double* o) {
 template <class Eng, class L, int OP, class EngF = Eng, int PPC = 2>
 __global__ void __launch_bounds__(Eng::NT, (PPC == 1 && Eng::NT <= 128 ? 3 : (Eng::NT <= 192 ? 2 : 1))) k_zpass(const ZArgs a, int S_rt, int So_rt) {
   extern __shared__ __align__(16) cplx smraw[];
+  pdl_launch_dependents();
   cplx* const sm = smraw + Eng::TWN;  // [twiddle table][tile]
   const cplx* const twp = Eng::kFast ? smraw : a.tw;
   if constexpr (Eng::kFast) {
     tw_fill<Eng::M>(smraw, a.tw);  // first use is after a CTA barrier
     cp_async_wait_all();
   }
+  pdl_wait();
   const int p0 = PPC * blockIdx.x;
   const int S = (OP >= ZOP_NS3) ? ZSig<OP>::S : S_rt;
   const int So = (OP >= ZOP_NS3) ? ZSig<OP>::So : So_rt;
@@ -744,6 +748,7 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
   extern __shared__ __align__(16) cplx smraw[];
   cplx* const sm = smraw + EngI::TWN;  // [twiddle table][tile]
   const cplx* const twp = smraw;
+  pdl_launch_dependents();
   tw_fill<M>(smraw, a.tw);  // cp.async; waited for before the staging barrier
   constexpr int S = 6, So = 3, NT = M / 4, K = M / 3 + 1, Q = M / 4;
   static_assert(EngI::NT == NT, "inverse prefix must use M/4 threads");
@@ -759,6 +764,7 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
     fence_mbar_init();
   }
   __syncthreads();
+  pdl_wait();
   if (tid == 0) {
     unsigned bytes = 0;
     for (int g = 0; g < 2 * S; ++g) bytes += (p0 + g / S < a.P) ? (unsigned)(K * 16) : 0u;
@@ -972,6 +978,7 @@ __global__ void __launch_bounds__(EngI::NT, (OP == ZOP_B2 ? SRK_ZB2P_MINB : (M <
   extern __shared__ __align__(16) cplx smraw[];
   cplx* const sm = smraw + EngI::TWN;  // [twiddle table][tile]
   const cplx* const twp = smraw;
+  pdl_launch_dependents();
   tw_fill<M>(smraw, a.tw);
   static_assert(OP == ZOP_NS3 || OP == ZOP_B2, "NS3 or 2D Boussinesq");
   // NT = M/8 (E = 24: two fused-middle rows per thread); B2: M/12 (three rows)
@@ -991,6 +998,7 @@ __global__ void __launch_bounds__(EngI::NT, (OP == ZOP_B2 ? SRK_ZB2P_MINB : (M <
     fence_mbar_init();
   }
   __syncthreads();
+  pdl_wait();
   if (tid == 0) {
     mbar_expect_tx(&mbar, (unsigned)(2 * S * K * 16));
     for (int s = 0; s < 2 * S; ++s)

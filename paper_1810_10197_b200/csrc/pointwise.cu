@@ -163,6 +163,8 @@ __global__ void __launch_bounds__(proj_chunk<DIMS, DENS, NTC, DIAG>()) k_project
     mbar_init(&mb[1], 1);
     fence_mbar_init();
   }
+  pdl_launch_dependents();
+  pdl_wait();
   __syncthreads();
   auto issue = [&](long long k, int b) {
     if (tid != 0 || k >= nch) return;
@@ -279,6 +281,8 @@ __global__ void __launch_bounds__(proj_chunk<DIMS, DENS, NTC, DIAG>()) k_project
 // K6: f = P[G] - nu k^2 u (physics.py:119-129); Boussinesq adds the buoyancy
 // before the projection and the density tendency (physics.py:163-184).
 __global__ void k_project(const ProjArgs a) {
+  pdl_launch_dependents();
+  pdl_wait();
   const GeomArgs& g = a.g;
   const long long n = a.modes;
   const int d = g.dims;
@@ -313,6 +317,8 @@ __global__ void k_project(const ProjArgs a) {
 
 // spectral.py:47-65
 __global__ void k_curl(const GeomArgs g, const cplx* __restrict__ u, cplx* __restrict__ w, long long n) {
+  pdl_launch_dependents();
+  pdl_wait();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     const KVec kv = kvec(i, g);
@@ -331,6 +337,8 @@ __global__ void k_curl(const GeomArgs g, const cplx* __restrict__ u, cplx* __res
 
 // physics.py:89-102
 __global__ void k_leray(const GeomArgs g, const cplx* __restrict__ u, cplx* __restrict__ out, long long n) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int d = g.dims;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
@@ -346,6 +354,8 @@ __global__ void k_leray(const GeomArgs g, const cplx* __restrict__ u, cplx* __re
 // per multiply and per add (y == nullptr starts from zeros, :343-347).
 template <int NT>
 __global__ void k_combine(const CombArgs a) {
+  pdl_launch_dependents();
+  pdl_wait();
   double cf[NT > 0 ? NT : 1];
 #pragma unroll
   for (int j = 0; j < NT; ++j) cf[j] = coef(a.c, a.hs, j);
@@ -365,7 +375,7 @@ void srk_launch_combine(const CombArgs& a, cudaStream_t st) {
   if (blocks < 1) blocks = 1;
   switch (a.nt) {
 #define CASE(N) \
-  case N: k_combine<N><<<(int)blocks, threads, 0, st>>>(a); break;
+  case N: srk_launch_k(k_combine<N>, dim3((int)blocks), dim3(threads), 0, st, a); break;
     CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
     default: break;
@@ -414,6 +424,8 @@ __global__ void __launch_bounds__(SRK_RT_CH) k_reduce_tma(const RedArgs a) {
     mbar_init(&mb[1], 1);
     fence_mbar_init();
   }
+  pdl_launch_dependents();
+  pdl_wait();
   __syncthreads();
   auto issue = [&](long long k, int b) {
     if (tid != 0 || k >= nch) return;
@@ -502,6 +514,8 @@ __global__ void __launch_bounds__(SRK_RT_CH) k_reduce_tma(const RedArgs a) {
 }
 
 __global__ void k_finalize(const double* __restrict__ partial, int nblk, double* __restrict__ out) {
+  pdl_launch_dependents();
+  pdl_wait();
   __shared__ double sh[256];
   for (int q = 0; q < SRK_NQ; ++q) {
     double v = 0.0;
@@ -523,13 +537,13 @@ void srk_launch_reduce(const RedArgs& a, double* out, cudaStream_t st) {
   case N: {                                                                                          \
     const int smem = 2 * (3 + N) * SRK_RT_CH * 16;                                                   \
     srk_ensure_smem((const void*)k_reduce_tma<N>, smem);                                             \
-    k_reduce_tma<N><<<SRK_RT_BLOCKS, SRK_RT_CH, smem, st>>>(a);                                      \
+    srk_launch_k(k_reduce_tma<N>, dim3(SRK_RT_BLOCKS), dim3(SRK_RT_CH), smem, st, a);                 \
   } break;
     CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
     default: break;
   }
-  k_finalize<<<1, 256, 0, st>>>(a.partial, SRK_RT_BLOCKS, out);
+  srk_launch_k(k_finalize, dim3(1), dim3(256), 0, st, (const double*)a.partial, (int)SRK_RT_BLOCKS, out);
 }
 
 // ---------------------------------------------------------------------------
@@ -539,6 +553,8 @@ void srk_launch_reduce(const RedArgs& a, double* out, cudaStream_t st) {
 __global__ void k_band_energy(const cplx* __restrict__ u, const long long* __restrict__ idx,
                               const double* __restrict__ w, int nb, int ncomp, long long modes,
                               double* __restrict__ out) {
+  pdl_launch_dependents();
+  pdl_wait();
   __shared__ double sh[256];
   double v = 0.0;
   for (int c = 0; c < ncomp; ++c)
@@ -557,6 +573,8 @@ __global__ void k_band_energy(const cplx* __restrict__ u, const long long* __res
 
 __global__ void k_band_scale(cplx* __restrict__ u, const long long* __restrict__ idx, int nb, int ncomp,
                              long long modes, double gamma) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nb * ncomp) return;
   const int c = t / nb, b = t - (t / nb) * nb;
@@ -575,7 +593,7 @@ static int launch_project_tma(const ProjArgs& a, cudaStream_t st) {
   if (DIAG) blocks = std::min(blocks, SRK_RED_BLOCKS);  // partials buffer
   const long long nch = (a.modes + CH - 1) / CH;
   const int grid = (int)std::min<long long>(blocks, nch);
-  k_project_tma<DIMS, DENS, NTC, DIAG><<<grid, CH, smem, st>>>(a);
+  srk_launch_k(k_project_tma<DIMS, DENS, NTC, DIAG>, dim3(grid), dim3(CH), smem, st, a);
   return grid;
 }
 
@@ -586,7 +604,7 @@ bool srk_launch_project_refresh(const ProjArgs& a, double* out, cudaStream_t st)
     grid = a.density ? launch_project_tma<3, true, 0, true>(a, st) : launch_project_tma<3, false, 0, true>(a, st);
   else
     grid = a.density ? launch_project_tma<2, true, 0, true>(a, st) : launch_project_tma<2, false, 0, true>(a, st);
-  k_finalize<<<1, 256, 0, st>>>(a.partial, grid, out);
+  srk_launch_k(k_finalize, dim3(1), dim3(256), 0, st, (const double*)a.partial, grid, out);
   return true;
 }
 
@@ -622,31 +640,33 @@ void srk_launch_project(const ProjArgs& a, cudaStream_t st) {
   }
   long long blocks = (a.modes + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  k_project<<<(int)blocks, 256, 0, st>>>(a);
+  srk_launch_k(k_project, dim3((int)blocks), dim3(256), 0, st, a);
 }
 void srk_launch_curl(const GeomArgs& g, const cplx* u, cplx* w, long long n, cudaStream_t st) {
   long long blocks = (n + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  k_curl<<<(int)blocks, 256, 0, st>>>(g, u, w, n);
+  srk_launch_k(k_curl, dim3((int)blocks), dim3(256), 0, st, g, u, w, n);
 }
 void srk_launch_leray(const GeomArgs& g, const cplx* u, cplx* o, long long n, cudaStream_t st) {
   long long blocks = (n + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  k_leray<<<(int)blocks, 256, 0, st>>>(g, u, o, n);
+  srk_launch_k(k_leray, dim3((int)blocks), dim3(256), 0, st, g, u, o, n);
 }
 void srk_launch_band_energy(const cplx* u, const long long* idx, const double* w, int nb, int ncomp,
                             long long modes, double* out, cudaStream_t st) {
-  k_band_energy<<<1, 256, 0, st>>>(u, idx, w, nb, ncomp, modes, out);
+  srk_launch_k(k_band_energy, dim3(1), dim3(256), 0, st, u, idx, w, nb, ncomp, modes, out);
 }
 __global__ void k_store_mapped(const double* __restrict__ src, double* dst, int n) {
+  pdl_launch_dependents();
+  pdl_wait();
   for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
 }
 void srk_launch_store_mapped(const double* src, double* dst, int n, cudaStream_t st) {
-  if (n > 0) k_store_mapped<<<1, 32, 0, st>>>(src, dst, n);
+  if (n > 0) srk_launch_k(k_store_mapped, dim3(1), dim3(32), 0, st, src, dst, n);
 }
 void srk_launch_band_scale(cplx* u, const long long* idx, int nb, int ncomp, long long modes, double gamma,
                            cudaStream_t st) {
   const int tot = nb * ncomp;
   if (tot <= 0) return;
-  k_band_scale<<<(tot + 127) / 128, 128, 0, st>>>(u, idx, nb, ncomp, modes, gamma);
+  srk_launch_k(k_band_scale, dim3((tot + 127) / 128), dim3(128), 0, st, u, idx, nb, ncomp, modes, gamma);
 }

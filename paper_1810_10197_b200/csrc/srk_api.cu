@@ -317,7 +317,7 @@ int launch_col(srk_plan* p, int kind, PassArgs a, cudaStream_t st) {
   memset(&tmo, 0, sizeof(tmo));
   setup_tma_out(kind, e.cols, a, &tmo);
   void* args[] = {&a, &tm, &tmo};
-  cudaError_t err = cudaLaunchKernel(e.fn, dim3((unsigned)grid), dim3(e.nt), args, e.smem, st);
+  cudaError_t err = srk_launch(e.fn, dim3((unsigned)grid), dim3(e.nt), args, e.smem, st);
   if (err != cudaSuccess) return fail(SRK_ERR_CUDA, std::string("colpass launch: ") + cudaGetErrorString(err));
   p->last_launches++;
   if (p->timing && p->nev < 16) cudaEventRecord(p->ev[p->nev++], st);
@@ -335,7 +335,7 @@ int launch_z(srk_plan* p, int kind, ZArgs a, int S_rt, int So_rt, cudaStream_t s
   if (e.ppc == 1 && a.pf_dist)  // L2 warm-up one wave of resident CTAs ahead (in pencils)
     a.pf_dist = srk_blocks_per_sm(e.fn, e.nt, e.smem) * srk_sm_count();
   void* args[] = {&a, &S_rt, &So_rt};
-  cudaError_t err = cudaLaunchKernel(e.fn, dim3(grid), dim3(e.nt), args, e.smem, st);
+  cudaError_t err = srk_launch(e.fn, dim3(grid), dim3(e.nt), args, e.smem, st);
   if (err != cudaSuccess) return fail(SRK_ERR_CUDA, std::string("zpass launch: ") + cudaGetErrorString(err));
   p->last_launches++;
   if (p->timing && p->nev < 16) cudaEventRecord(p->ev[p->nev++], st);

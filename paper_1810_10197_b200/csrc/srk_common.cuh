@@ -214,6 +214,21 @@ SRK_DEV int trunc_dst(int r, int n, int m, bool zero_nyq) {
 SRK_DEV double mode_full(int i, int n) { return (double)(i <= (n >> 1) ? i : i - n); }
 
 // ---------------------------------------------------------------------------
+// Programmatic dependent launch (PDL).  Every libsrk kernel is launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization (host_util.cuh
+// srk_launch), so the next kernel of a stream is scheduled while this one's
+// last wave drains and runs its prologue (shared twiddle table, mbarriers)
+// early.  Rules that keep it exact: each kernel signals launch_dependents at its
+// start (all its CTAs are then resident or done, so a waiting dependent can
+// never block it), and calls pdl_wait() -- which returns once the previous grid
+// of the stream has completed and its memory is visible -- before it touches
+// any global data another kernel produces or consumes.  Without the attribute
+// (or after a non-kernel stream operation) both are no-ops.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+// ---------------------------------------------------------------------------
 // mbarrier + 1D TMA bulk copy (sm_90+ PTX; used on sm_100a)
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ unsigned smem_u32(const void* p) {

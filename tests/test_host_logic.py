@@ -1,5 +1,6 @@
 """Host-side logic of the drop-in API vs the oracle restatement (CPU-only)."""
 
+import os
 import numpy as np
 import pytest
 
@@ -130,3 +131,21 @@ def test_plane_runs_and_forcing_planes():
     want = sorted(set(np.nonzero(band)[0].tolist()))
     got = [i for a, b in forcing_planes(g2, 2.5) for i in range(a, b)]
     assert got == want
+
+
+def test_bench_self_launches_n_ranks_dry_run():
+    """`bench.py --gpus 2` without a torchrun environment re-launches itself with 2
+    ranks (gloo, --dry-run: no GPU work) and rank 0's line reports n_gpus == 2."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    p = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run", "--steps", "2",
+                        "--warmup", "1"], cwd=root, env=env, capture_output=True, text=True, timeout=240)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["ranks_seen"] == 2 and d["dry_run"]
