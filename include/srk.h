@@ -256,6 +256,10 @@ int srk_debug_phase_buffer(srk_plan* plan, void* dev_buf, int launch_index);
  * bench.py for the measured fp64 ceiling of the z-pass. */
 int srk_probe(int mode, int iters, int blocks_per_sm, void* scratch, void* stream, double* ops_out);
 
+/* Build flags: bit 0 = hazard-probe build (make checks: schedule fuzzing at every
+ * barrier, NaN-poisoned shared memory, tile bounds asserts; tools/check_build.sh). */
+int srk_build_info(void);
+
 /* Number of kernel launches the last srk_rhs issued (launch accounting for
  * the bench's gpu_launches claim). */
 int srk_rhs_launch_count(const srk_plan* plan);

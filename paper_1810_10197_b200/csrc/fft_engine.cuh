@@ -50,6 +50,7 @@ struct RowTile {
   static constexpr int STEP8 = (C_ >= 8) ? 8 * C_ : 9 * C_;
   static constexpr int ROWSTEP = C_;
   __device__ __forceinline__ static int idx(int row, int col) {
+    SRK_ASSERT(row >= 0 && row < M_ && col >= 0 && col < C_);
     if constexpr (C_ >= 8) {
       return row * C_ + col;
     } else {
@@ -71,7 +72,10 @@ struct ColTile {
   static constexpr int SIZE = PITCH * C_;
   static constexpr int STEP8 = 9;
   static constexpr int ROWSTEP = 1;
-  __device__ __forceinline__ static int idx(int row, int col) { return col * PITCH + row + (row >> 3); }
+  __device__ __forceinline__ static int idx(int row, int col) {
+    SRK_ASSERT(row >= 0 && row < M_ && col >= 0 && col < C_);
+    return col * PITCH + row + (row >> 3);
+  }
   SRK_DEV static int col_of(int tid, int tpc) { return tid / tpc; }
   SRK_DEV static int tj_of(int tid, int tpc) { return tid % tpc; }
   static constexpr int roff(int q) { return q + (q >> 3); }
@@ -200,9 +204,9 @@ struct ld_has_range<T, decltype(void(T::kRange))> : std::true_type {};
 template <bool WS, int TPC>
 __device__ __forceinline__ void stage_sync() {
   if constexpr (WS && TPC <= 32)
-    __syncwarp();
+    SRK_WBAR();
   else
-    __syncthreads();
+    SRK_BAR();
 }
 
 template <int M, int E, class L, int SIGN, bool LD_SMEM, bool ST_SMEM, int Ls, int R, int... Rest>
@@ -252,7 +256,7 @@ struct FastStage {
         DFT<R, SIGN>::run(v[b]);
       }
     }
-    if constexpr ((!FIRST || LD_SMEM) && (!LAST || ST_SMEM)) __syncthreads();
+    if constexpr ((!FIRST || LD_SMEM) && (!LAST || ST_SMEM)) SRK_BAR();
     if (act) {
 #pragma unroll
       for (int b = 0; b < NB; ++b) {
@@ -277,7 +281,7 @@ struct FastStage {
       }
     }
     if constexpr (!LAST) {
-      __syncthreads();
+      SRK_BAR();
       FastStage<M, E, L, SIGN, LD_SMEM, ST_SMEM, Ls * R, Rest...>::go(sm, tw, col, tj, act, ld, st);
     }
   }
@@ -332,7 +336,7 @@ struct FastStageW {
     }
     if constexpr ((!FIRST || LD_SMEM) && (!LAST || ST_SMEM)) {
       if constexpr (FIRST)
-        __syncthreads();  // staging may alias other columns
+        SRK_BAR();  // staging may alias other columns
       else
         stage_sync<true, TPC>();
     }
@@ -437,7 +441,7 @@ struct OneStage {
       if constexpr (Ls > 1) stage_twiddle<M, R, SIGN>(v, tw, k * (unsigned)(M / (Ls * R)));
       DFT<R, SIGN>::run(v);
     }
-    if constexpr ((!FIRST || LD_SMEM) && (!LAST || ST_SMEM)) __syncthreads();
+    if constexpr ((!FIRST || LD_SMEM) && (!LAST || ST_SMEM)) SRK_BAR();
     if (act) {
       const int base = (int)(((unsigned)j - k) * (unsigned)R + k);
       if constexpr (LAST) {
@@ -457,7 +461,7 @@ struct OneStage {
       }
     }
     if constexpr (!LAST) {
-      __syncthreads();
+      SRK_BAR();
       OneStage<M, L, SIGN, LD_SMEM, ST_SMEM, Ls * R, Rest...>::go(sm, tw, col, tj, act_col, ld, st);
     }
   }
@@ -492,7 +496,7 @@ struct OneStageZ {
       stage_twiddle_sq<M, R, SIGN>(v, tw, k * (unsigned)(M / (Ls * R)));
       DFT<R, SIGN>::run(v);
     }
-    __syncthreads();
+    SRK_BAR();
     if (act) {
       const int base = (int)(((unsigned)j - k) * (unsigned)R + k);
       if constexpr (LAST) {
@@ -508,7 +512,7 @@ struct OneStageZ {
       }
     }
     if constexpr (!LAST) {
-      __syncthreads();
+      SRK_BAR();
       OneStageZ<M, L, SIGN, Ls * R, Rest...>::go(sm, tw, ncols, st);
     }
   }

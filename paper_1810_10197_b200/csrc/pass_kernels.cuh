@@ -181,7 +181,7 @@ __device__ __forceinline__ void tma_stage(cplx* sm, const CUtensorMap* tm, int w
   }
   cp_async_wait_all();  // this thread's twiddle-table copies
   mbar_wait(bar, 0);
-  __syncthreads();
+  SRK_BAR();
 }
 
 template <class Eng, int KIND, int SIGN, int FL = 0>
@@ -189,6 +189,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
                                                                   const __grid_constant__ CUtensorMap tmo) {
   extern __shared__ __align__(128) cplx smraw[];
   pdl_launch_dependents();
+  srk_poison_smem(smraw);
   cplx* const sm = smraw + Eng::TWN;
   const cplx* const twp = Eng::kFast ? smraw : a.tw;
   if constexpr (Eng::kFast) tw_fill<Eng::M>(smraw, a.tw);  // ordered by the staging barrier
@@ -218,7 +219,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
         if ((int)threadIdx.x == i) q = a.peer[i];
       s_peer[threadIdx.x] = q ? q + plane * a.out_plane_stride + w_out : nullptr;
     }
-    __syncthreads();
+    SRK_BAR();
   }
   const unsigned rso_ = (unsigned)a.out_rs;
   const int orpb_ = (FL & PF_BOUT) ? a.out_rpb : 0;
@@ -248,7 +249,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
   auto flush_out = [&]() {
     if (use_tmo) {
       fence_proxy_async_smem();
-      __syncthreads();
+      SRK_BAR();
       if (threadIdx.x == 0) {
         for (int b = 0; b < M / a.tmo_rows; ++b)
           tma_store_4d(&tmo, sm + b * a.tmo_rows * C, 2 * wl, g, b * a.tmo_rows, plane);
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
       mbar_init(&tbar, 1);
       fence_mbar_init();
     }
-    __syncthreads();
+    SRK_BAR();
   }
   pdl_wait();  // the previous kernel's output is complete and visible from here on
 
@@ -273,7 +274,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
     } else if constexpr (Eng::kFast) {
       stage_rows<C>(sm, inp, n, rs, ncols, in_rpb, a.in_bstride);
       cp_async_wait_all();
-      __syncthreads();
+      SRK_BAR();
       SRK_TS(1)
     }
     auto ld = [&](int row, int col) -> cplx {
@@ -333,7 +334,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
       stage_rows<C>(sm, pa, n, rs, ncols, in_rpb, a.in_bstride);
       if (is_curl) stage_rows<C>(sm + n * C, pb, n, rs, ncols, in_rpb, a.in_bstride);
       cp_async_wait_all();
-      __syncthreads();
+      SRK_BAR();
       SRK_TS(1)
     }
     auto ld = [&](int row, int col) -> cplx {
@@ -369,7 +370,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
     } else if constexpr (Eng::kFast) {
       stage_rows<C>(sm, pa, n, rs, ncols, in_rpb, a.in_bstride);
       cp_async_wait_all();
-      __syncthreads();
+      SRK_BAR();
       SRK_TS(1)
     }
     auto ld = [&](int row, int col) -> cplx {
@@ -415,7 +416,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
       stage_rows<C>(sm, pa, n, rs, ncols, in_rpb, a.in_bstride);
       if (is_curl) stage_rows<C>(sm + n * C, pb, n, rs, ncols, in_rpb, a.in_bstride);
       cp_async_wait_all();
-      __syncthreads();
+      SRK_BAR();
       SRK_TS(1)
     }
     auto ld = [&](int row, int col) -> cplx {
@@ -450,7 +451,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
     } else if constexpr (Eng::kFast) {
       stage_rows<C>(sm, inp, M, rs, ncols, in_rpb, a.in_bstride);
       cp_async_wait_all();
-      __syncthreads();
+      SRK_BAR();
       SRK_TS(1)
     }
     auto ld = [&](int row, int col) -> cplx {
@@ -467,7 +468,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
     Eng::template run<SIGN, Eng::kFast, false>(a.gp, sm, twp, ncols, ld, st);
   }
   if (a.dbg) {
-    __syncthreads();
+    SRK_BAR();
     SRK_TS(2)
   }
 }
@@ -536,6 +537,7 @@ template <class Eng, class L, int OP, class EngF = Eng, int PPC = 2>
 __global__ void __launch_bounds__(Eng::NT, (PPC == 1 && Eng::NT <= 128 ? 3 : (Eng::NT <= 192 ? 2 : 1))) k_zpass(const ZArgs a, int S_rt, int So_rt) {
   extern __shared__ __align__(16) cplx smraw[];
   pdl_launch_dependents();
+  srk_poison_smem(smraw);
   cplx* const sm = smraw + Eng::TWN;  // [twiddle table][tile]
   const cplx* const twp = Eng::kFast ? smraw : a.tw;
   if constexpr (Eng::kFast) {
@@ -565,7 +567,7 @@ __global__ void __launch_bounds__(Eng::NT, (PPC == 1 && Eng::NT <= 128 ? 3 : (En
         mbar_init(&mbar, 1);
         fence_mbar_init();
       }
-      __syncthreads();
+      SRK_BAR();
       if (threadIdx.x == 0) {
         unsigned bytes = 0;
         for (int g = 0; g < PPC * S; ++g) bytes += (p0 + g / S < a.P) ? (unsigned)(K * 16) : 0u;
@@ -580,14 +582,14 @@ __global__ void __launch_bounds__(Eng::NT, (PPC == 1 && Eng::NT <= 128 ? 3 : (En
       if (PPC == 2 && p0 + 1 >= a.P)
         for (int i = threadIdx.x; i < S * K; i += blockDim.x) stg[S * K + i] = cmk(0.0, 0.0);
       mbar_wait(&mbar, 0);
-      __syncthreads();
+      SRK_BAR();
     } else {
       for (int g = 0; g < PPC * S; ++g) {
         const int pp = g / S, s = g - pp * S, pen = p0 + pp;
         const cplx* __restrict__ src = a.in + s * a.in_sig_stride + (long long)pen * K;
         for (int k = threadIdx.x; k < K; k += blockDim.x) stg[g * K + k] = (pen < a.P) ? src[k] : cmk(0.0, 0.0);
       }
-      __syncthreads();
+      SRK_BAR();
     }
     // Hermitian extension of stored modes onto the padded z axis (branch free)
     auto hs = [&](int g, int k) -> cplx {
@@ -622,7 +624,7 @@ __global__ void __launch_bounds__(Eng::NT, (PPC == 1 && Eng::NT <= 128 ? 3 : (En
     } else {
       auto st = [&](int n, int c, cplx v) { sm[L::idx(n, c)] = v; };
       Eng::template run<+1, true, true>(a.gp, sm, twp, NCI, ld, st);
-      __syncthreads();
+      SRK_BAR();
       // ---- physical space: per row n, both pencils ----
       for (int n = threadIdx.x; n < M; n += blockDim.x) {
         double r[2 * 7];
@@ -638,7 +640,7 @@ __global__ void __launch_bounds__(Eng::NT, (PPC == 1 && Eng::NT <= 128 ? 3 : (En
 #pragma unroll
         for (int c = 0; c < PPC * ZSig<OP>::So / 2; ++c) sm[L::idx(n, c)] = cmk(o[2 * c], o[2 * c + 1]);
       }
-      __syncthreads();
+      SRK_BAR();
     }
   }
   // ---- forward: PPC*So/2 complex columns ----
@@ -664,7 +666,7 @@ __global__ void __launch_bounds__(Eng::NT, (PPC == 1 && Eng::NT <= 128 ? 3 : (En
     };
     EngF::template run<-1, true, true>(a.gp, sm, twp, NCO, ld, st);
   }
-  __syncthreads();
+  SRK_BAR();
   // ---- extraction: two real spectra from each complex column, keep K modes ----
   const bool zn = a.zero_nyq != 0;
   for (int i = threadIdx.x; i < NCO * K; i += blockDim.x) {
@@ -749,6 +751,7 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
   cplx* const sm = smraw + EngI::TWN;  // [twiddle table][tile]
   const cplx* const twp = smraw;
   pdl_launch_dependents();
+  srk_poison_smem(smraw);
   tw_fill<M>(smraw, a.tw);  // cp.async; waited for before the staging barrier
   constexpr int S = 6, So = 3, NT = M / 4, K = M / 3 + 1, Q = M / 4;
   static_assert(EngI::NT == NT, "inverse prefix must use M/4 threads");
@@ -763,7 +766,7 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
     mbar_init(&mbar, 1);
     fence_mbar_init();
   }
-  __syncthreads();
+  SRK_BAR();
   pdl_wait();
   if (tid == 0) {
     unsigned bytes = 0;
@@ -786,7 +789,7 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
     for (int i = tid; i < S * K; i += NT) stg[S * K + i] = cmk(0.0, 0.0);
   mbar_wait(&mbar, 0);
   cp_async_wait_all();
-  __syncthreads();
+  SRK_BAR();
   SRK_TS(1)
   // ---- inverse prefix stages (Stockham, in place) ----
   {
@@ -794,7 +797,7 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
     auto st = [&](int n, int c, cplx v) { sm[L::idx(n, c)] = v; };
     EngI::template run_ws<+1, true, true>(a.gp, sm, twp, S, ld, st);
   }
-  __syncthreads();
+  SRK_BAR();
   SRK_TS(2)
   // ---- fused: last inverse radix-4 (Ls = M/4) | u x w | first forward radix-4 ----
   {
@@ -816,7 +819,7 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
     w[1].y = -w[1].y;  // inverse sign
     w[2] = csq(w[1]);
     w[3] = cmul(w[2], w[1]);
-    __syncthreads();
+    SRK_BAR();
     double o[4][6];
 #pragma unroll
     for (int c = 0; c < S; ++c) {
@@ -844,7 +847,7 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
       for (int q = 0; q < 4; ++q) sm[a0 + q * L::ROWSTEP] = F[q];
     }
   }
-  __syncthreads();
+  SRK_BAR();
   SRK_TS(3)
   // ---- forward suffix stages (Ls = 4 ...) on the 3 packed columns ----
   {
@@ -862,7 +865,7 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
     else
       FastStageW<M, (EF > 0 ? EF : 24), L, -1, true, true, 4, FR...>::go(sm, twp, col, tj, act, ld, st);
   }
-  __syncthreads();
+  SRK_BAR();
   SRK_TS(4)
   // ---- extraction: two real spectra per complex column, K modes, kz = n/2 zeroed.
   // The 6 output rows are assembled in the idle tile columns So..S-1 and
@@ -879,7 +882,7 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
     ost[(2 * c + 1) * K + k] = cmk(0.5 * (Zk.y + Zm.y), -0.5 * (Zk.x - Zm.x));
   }
   fence_proxy_async_smem();
-  __syncthreads();
+  SRK_BAR();
   if (tid == 0) {
     for (int g = 0; g < 2 * So; ++g) {
       const int pp = g / So, s = g - pp * So, pen = p0 + pp;
@@ -888,7 +891,7 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
     bulk_commit_and_wait_read();
   }
   if (a.dbg) {
-    __syncthreads();
+    SRK_BAR();
     SRK_TS(5)
   }
 }
@@ -928,7 +931,7 @@ struct LoopStageZ {
         DFT<R, SIGN>::run(v[b]);
       }
     }
-    __syncthreads();
+    SRK_BAR();
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       const int u = tid + b * NT;
@@ -950,7 +953,7 @@ struct LoopStageZ {
       }
     }
     if constexpr (!LAST) {
-      __syncthreads();
+      SRK_BAR();
       LoopStageZ<M, L, SIGN, NCOL, NT, Ls * R, Rest...>::go(sm, tw, st);
     }
   }
@@ -979,6 +982,7 @@ __global__ void __launch_bounds__(EngI::NT, (OP == ZOP_B2 ? SRK_ZB2P_MINB : (M <
   cplx* const sm = smraw + EngI::TWN;  // [twiddle table][tile]
   const cplx* const twp = smraw;
   pdl_launch_dependents();
+  srk_poison_smem(smraw);
   tw_fill<M>(smraw, a.tw);
   static_assert(OP == ZOP_NS3 || OP == ZOP_B2, "NS3 or 2D Boussinesq");
   // NT = M/8 (E = 24: two fused-middle rows per thread); B2: M/12 (three rows)
@@ -997,7 +1001,7 @@ __global__ void __launch_bounds__(EngI::NT, (OP == ZOP_B2 ? SRK_ZB2P_MINB : (M <
     mbar_init(&mbar, 1);
     fence_mbar_init();
   }
-  __syncthreads();
+  SRK_BAR();
   pdl_wait();
   if (tid == 0) {
     mbar_expect_tx(&mbar, (unsigned)(2 * S * K * 16));
@@ -1012,14 +1016,14 @@ __global__ void __launch_bounds__(EngI::NT, (OP == ZOP_B2 ? SRK_ZB2P_MINB : (M <
   }
   mbar_wait(&mbar, 0);
   cp_async_wait_all();
-  __syncthreads();
+  SRK_BAR();
   SRK_TS(1)
   {
     ZHermLoad<M> ld{stg};
     auto st = [&](int n, int c, cplx v) { sm[L::idx(n, c)] = v; };
     EngI::template run_ws<+1, true, true>(a.gp, sm, twp, S, ld, st);
   }
-  __syncthreads();
+  SRK_BAR();
   SRK_TS(2)
   // ---- fused: last inverse radix-4 | u x w | first forward radix-4; rows j, j + NT ----
   {
@@ -1039,7 +1043,7 @@ __global__ void __launch_bounds__(EngI::NT, (OP == ZOP_B2 ? SRK_ZB2P_MINB : (M <
         }
       }
     }
-    __syncthreads();
+    SRK_BAR();
 #pragma unroll
     for (int h = 0; h < RPT; ++h) {
       const int j = tid + h * NT;
@@ -1078,16 +1082,19 @@ __global__ void __launch_bounds__(EngI::NT, (OP == ZOP_B2 ? SRK_ZB2P_MINB : (M <
       }
     }
   }
-  __syncthreads();
+  SRK_BAR();
   SRK_TS(3)
   // ---- forward suffix (Ls = 4 ...) on the 2 packed columns ----
   {
+    // only rows the extraction reads: column 0 (two-for-one) needs k < K-1 and its
+    // mirror M-k; NS3's column 1 is the real P2 alone and needs k < K-1 only
     auto st = [&](int n, int c, cplx v) {
-      if (n < K - 1 || n > M - K + 1) sm[L::idx(n, c)] = v;
+      const bool keep = (OP == ZOP_NS3 && c == 1) ? (n < K - 1) : (n < K - 1 || n > M - K + 1);
+      if (keep) sm[L::idx(n, c)] = v;
     };
     LoopStageZ<M, L, -1, 2, NT, 4, FR...>::go(sm, twp, st);
   }
-  __syncthreads();
+  SRK_BAR();
   SRK_TS(4)
   // ---- extraction: P0, P1 from column 0 (two-for-one), P2 = column 1; kz = n/2 zeroed ----
   for (int k = tid; k < K; k += NT) {
@@ -1107,7 +1114,7 @@ __global__ void __launch_bounds__(EngI::NT, (OP == ZOP_B2 ? SRK_ZB2P_MINB : (M <
     }
   }
   if (a.dbg) {
-    __syncthreads();
+    SRK_BAR();
     SRK_TS(5)
   }
 }

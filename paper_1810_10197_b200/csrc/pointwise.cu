@@ -139,6 +139,7 @@ constexpr int proj_chunk() {
 template <int DIMS, bool DENS, int NTC = -1, bool DIAG = false>
 __global__ void __launch_bounds__(proj_chunk<DIMS, DENS, NTC, DIAG>()) k_project_tma(const ProjArgs a) {
   extern __shared__ __align__(128) cplx psm[];
+  srk_poison_smem(psm);
   constexpr int CH = proj_chunk<DIMS, DENS, NTC, DIAG>();
   constexpr int d = DIMS;
   constexpr int NG = DENS ? 2 * d : d;  // G components
@@ -165,7 +166,7 @@ __global__ void __launch_bounds__(proj_chunk<DIMS, DENS, NTC, DIAG>()) k_project
   }
   pdl_launch_dependents();
   pdl_wait();
-  __syncthreads();
+  SRK_BAR();
   auto issue = [&](long long k, int b) {
     if (tid != 0 || k >= nch) return;
     const long long i0 = k * CH;
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__(proj_chunk<DIMS, DENS, NTC, DIAG>()) k_project
         }
       }
     }
-    __syncthreads();  // stage b consumed
+    SRK_BAR();  // stage b consumed
     issue(k + 2LL * G, b);
   }
   if constexpr (DIAG) {  // fixed-order block reduction -> partials (deterministic)
@@ -267,7 +268,7 @@ __global__ void __launch_bounds__(proj_chunk<DIMS, DENS, NTC, DIAG>()) k_project
       for (int off = 16; off > 0; off >>= 1) v[q] += __shfl_down_sync(0xffffffffu, v[q], off);
       if (lane == 0) red[q][warp] = v[q];
     }
-    __syncthreads();
+    SRK_BAR();
     if (tid < SRK_NQ) {
       double s = 0.0;
       const int q = tid == 4 ? 0 : (tid == 5 ? 1 : (tid == 8 ? 2 : -1));
@@ -405,6 +406,7 @@ static_assert(SRK_RT_BLOCKS <= SRK_RED_BLOCKS, "partials buffer sized by SRK_RED
 template <int NT>
 __global__ void __launch_bounds__(SRK_RT_CH) k_reduce_tma(const RedArgs a) {
   extern __shared__ __align__(128) cplx rsm[];
+  srk_poison_smem(rsm);
   constexpr int CH = SRK_RT_CH;
   constexpr int NS = 3 + NT;  // y1, y0, F[0..NT), fl
   __shared__ __align__(8) unsigned long long mb[2];
@@ -426,7 +428,7 @@ __global__ void __launch_bounds__(SRK_RT_CH) k_reduce_tma(const RedArgs a) {
   }
   pdl_launch_dependents();
   pdl_wait();
-  __syncthreads();
+  SRK_BAR();
   auto issue = [&](long long k, int b) {
     if (tid != 0 || k >= nch) return;
     const int c = (int)(k / cpc);
@@ -493,7 +495,7 @@ __global__ void __launch_bounds__(SRK_RT_CH) k_reduce_tma(const RedArgs a) {
         acc[8] = DADD(acc[8], DMUL(DMUL(w, k2), m2));
       }
     }
-    __syncthreads();  // stage b consumed (bulk copies only write it: no proxy fence needed)
+    SRK_BAR();  // stage b consumed (bulk copies only write it: no proxy fence needed)
     issue(k + 2LL * G, b);
   }
   __shared__ double red[SRK_NQ][CH / 32];
@@ -505,7 +507,7 @@ __global__ void __launch_bounds__(SRK_RT_CH) k_reduce_tma(const RedArgs a) {
     for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
     if (lane == 0) red[q][warp] = v;
   }
-  __syncthreads();
+  SRK_BAR();
   if (tid < SRK_NQ) {
     double v = 0.0;
     for (int w = 0; w < CH / 32; ++w) v += red[tid][w];
@@ -521,13 +523,13 @@ __global__ void k_finalize(const double* __restrict__ partial, int nblk, double*
     double v = 0.0;
     for (int i = threadIdx.x; i < nblk; i += blockDim.x) v += partial[q * nblk + i];
     sh[threadIdx.x] = v;
-    __syncthreads();
+    SRK_BAR();
     for (int s = blockDim.x / 2; s > 0; s >>= 1) {
       if ((int)threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
-      __syncthreads();
+      SRK_BAR();
     }
     if (threadIdx.x == 0) out[q] = sh[0];
-    __syncthreads();
+    SRK_BAR();
   }
 }
 
@@ -563,10 +565,10 @@ __global__ void k_band_energy(const cplx* __restrict__ u, const long long* __res
       v = DADD(v, DMUL(w[b], DADD(DMUL(z.x, z.x), DMUL(z.y, z.y))));
     }
   sh[threadIdx.x] = v;
-  __syncthreads();
+  SRK_BAR();
   for (int s = blockDim.x / 2; s > 0; s >>= 1) {
     if ((int)threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
-    __syncthreads();
+    SRK_BAR();
   }
   if (threadIdx.x == 0) out[0] = sh[0];
 }

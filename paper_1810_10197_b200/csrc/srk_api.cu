@@ -473,6 +473,14 @@ extern "C" {
 
 int srk_abi_version(void) { return 1; }
 
+int srk_build_info(void) {
+#ifdef SRK_DEBUG_CHECKS
+  return 1;  // hazard-probe build (schedule fuzzing, NaN-poisoned shared memory, asserts)
+#else
+  return 0;
+#endif
+}
+
 const char* srk_last_error(void) { return g_err.c_str(); }
 
 int srk_plan_create(srk_plan** out, int dims, const int64_t* shape, const double* lengths, int density,

@@ -213,6 +213,73 @@ SRK_DEV int trunc_dst(int r, int n, int m, bool zero_nyq) {
 // full-axis mode label (grid.py:75-82): Nyquist relabelled +n/2
 SRK_DEV double mode_full(int i, int n) { return (double)(i <= (n >> 1) ? i : i - n); }
 
+
+// ---------------------------------------------------------------------------
+// Debug-check builds (make CHECKS=1 -> _lib_chk/libsrk.so, tools/check_build.sh):
+// compute-sanitizer is closed on this GPU pool, so the library carries its own
+// hazard probes, compiled out of the production build:
+//  * SRK_BAR / SRK_WBAR: every CTA / warp barrier is followed by a pseudo-random
+//    per-warp delay (up to ~2k cycles, keyed by block, warp, site, launch) --
+//    schedule fuzzing: a missing barrier between a shared-memory write and a
+//    read by another warp turns into a wrong (or NaN) result under the checks;
+//  * srk_poison_smem(): dynamic shared memory is filled with NaN at kernel
+//    entry, so a read of a slot no thread wrote propagates into the output
+//    (initcheck for shared memory);
+//  * SRK_ASSERT: tile index bounds; mbarrier waits trap instead of hanging.
+// ---------------------------------------------------------------------------
+#ifdef SRK_DEBUG_CHECKS
+#include <cstdio>
+__device__ __forceinline__ unsigned srk_hash(unsigned a) {
+  a ^= a >> 16;
+  a *= 0x7feb352dU;
+  a ^= a >> 15;
+  a *= 0x846ca68bU;
+  a ^= a >> 16;
+  return a;
+}
+__device__ __forceinline__ void srk_fuzz(unsigned site) {
+  const unsigned h = srk_hash(blockIdx.x * 0x9E3779B9U ^ (threadIdx.x >> 5) * 0x85EBCA6BU ^ site * 0xC2B2AE35U ^
+                              (unsigned)(clock64() >> 20));
+  const long long t0 = clock64();
+  const long long d = (h & 7u) == 0 ? 0 : (long long)(h >> 21);  // 0 .. 2047 cycles
+  while (clock64() - t0 < d) {
+  }
+}
+#define SRK_BAR()        \
+  do {                   \
+    __syncthreads();     \
+    srk_fuzz(__LINE__);  \
+  } while (0)
+#define SRK_WBAR()       \
+  do {                   \
+    __syncwarp();        \
+    srk_fuzz(__LINE__);  \
+  } while (0)
+#define SRK_ASSERT(c)                                                                              \
+  do {                                                                                             \
+    if (!(c)) {                                                                                    \
+      printf("srk check failed: %s (%s:%d) block %d thread %d\n", #c, __FILE__, __LINE__, blockIdx.x, \
+             threadIdx.x);                                                                         \
+      __trap();                                                                                    \
+    }                                                                                              \
+  } while (0)
+__device__ __forceinline__ void srk_poison_smem(void* base) {
+  unsigned n;
+  asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(n));
+  unsigned long long* p = (unsigned long long*)base;
+  for (unsigned i = threadIdx.x; i < n / 8; i += blockDim.x) p[i] = 0x7FF8DEADBEEF0000ULL;  // quiet NaN
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // before TMA / bulk copies overwrite it
+  __syncthreads();
+}
+#else
+#define SRK_BAR() __syncthreads()
+#define SRK_WBAR() __syncwarp()
+#define SRK_ASSERT(c) \
+  do {                \
+  } while (0)
+__device__ __forceinline__ void srk_poison_smem(void*) {}
+#endif
+
 // ---------------------------------------------------------------------------
 // Programmatic dependent launch (PDL).  Every libsrk kernel is launched with
 // cudaLaunchAttributeProgrammaticStreamSerialization (host_util.cuh
@@ -252,6 +319,21 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       : "memory");
 }
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+#ifdef SRK_DEBUG_CHECKS
+  {
+    const long long t0 = clock64();
+    unsigned done = 0;
+    while (!done) {
+      asm volatile(
+          "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+          : "=r"(done)
+          : "r"(smem_u32(bar)), "r"(phase)
+          : "memory");
+      SRK_ASSERT(clock64() - t0 < (1LL << 34));  // ~8 s: a lost transaction, not a slow copy
+    }
+    return;
+  }
+#endif
   asm volatile(
       "{\n"
       ".reg .pred p;\n"

@@ -1,0 +1,20 @@
+#!/bin/bash
+# Hazard probes in place of compute-sanitizer (closed on this GPU pool): run the
+# small-N kernel workload and the small GPU parity tests against the SRK_DEBUG_CHECKS
+# build (schedule fuzzing at every barrier, NaN-poisoned shared memory, bounds
+# asserts, trapping mbarrier waits), and require bitwise-identical results to the
+# production build.  Run on a GPU box from the repo root; logs in gpurun_out/checks/.
+set -u
+OUT=gpurun_out/checks
+mkdir -p $OUT
+timeout 900 python tools/sanitize_cases.py --dump /tmp/srk_prod.npz > $OUT/prod.log 2>&1; echo "prod rc=$?" | tee -a $OUT/summary.txt
+SRK_LIB_PATH=$PWD/_lib_chk/libsrk.so timeout 1800 python tools/sanitize_cases.py --dump /tmp/srk_chk.npz > $OUT/chk.log 2>&1; echo "checks rc=$?" | tee -a $OUT/summary.txt
+python - <<'PY' | tee -a $OUT/summary.txt
+import numpy as np
+a, b = np.load("/tmp/srk_prod.npz"), np.load("/tmp/srk_chk.npz")
+bad = [k for k in a.files if not np.array_equal(a[k], b[k], equal_nan=False)]
+print(f"bitwise prod vs checks: {len(a.files) - len(bad)}/{len(a.files)} arrays identical", "differ:", bad[:10])
+PY
+SRK_LIB_PATH=$PWD/_lib_chk/libsrk.so timeout 2400 python -m pytest tests/test_gpu_parity.py tests/test_gpu_round2.py tests/test_gpu_behaviour.py tests/test_gpu_graphs.py tests/test_gpu_fused_stage.py -q -x -k "not 256 and not 512 and not 1024 and not fullsize and not 128" > $OUT/pytest_checks.log 2>&1
+echo "pytest under checks rc=$?" | tee -a $OUT/summary.txt
+tail -2 $OUT/pytest_checks.log | tee -a $OUT/summary.txt

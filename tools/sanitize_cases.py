@@ -2,6 +2,7 @@
 compute-sanitizer (memcheck / racecheck / synccheck, one tool per run):
 
     compute-sanitizer --tool racecheck --racecheck-report hazard python tools/sanitize_cases.py
+    SRK_LIB_PATH=_lib_chk/libsrk.so python tools/sanitize_cases.py --dump chk.npz   (hazard-probe build)
 
 Anisotropic grids put one long axis on each pass so the production plans run
 on a handful of tiles: an axis of n = 512 gives M = 768 (the 512^3 kernels:
@@ -28,6 +29,7 @@ from paper_1810_10197_b200.integrators import combine  # noqa: E402
 
 torch.cuda.init()
 RNG = np.random.default_rng(11)
+DUMP = {}
 
 
 def state(g, ncomp, amp=1.0):
@@ -49,11 +51,20 @@ def rhs_case(shape, density=False, lengths=None):
     _, y2, sums = rhs.refresh(0.0, y, 0.05)
     assert np.isfinite(sums[4])
     torch.cuda.synchronize()
+    assert bool(torch.isfinite(torch.view_as_real(f)).all()), f"non-finite RHS {shape} (poisoned shared memory read?)"
+    key = "x".join(map(str, shape)) + ("_b" if density else "")
+    DUMP[key + "_f"] = f.cpu().numpy()
+    DUMP[key + "_yn"] = yn.cpu().numpy()
+    DUMP[key + "_y2"] = y2.cpu().numpy()
+    DUMP[key + "_sums"] = np.array(sums)
     return float(f.abs().max())
 
 
 def main():
     t0 = time.time()
+    from paper_1810_10197_b200 import _native
+
+    print(f"libsrk {_native.LIB_PATH} build_info={_native.load().srk_build_info()}", flush=True)
     cases = [
         ((512, 8, 8), False), ((8, 512, 8), False), ((8, 8, 512), False),       # M = 768 (512^3 kernels)
         ((1024, 8, 8), False), ((8, 8, 1024), False), ((1024, 16), True),       # M = 1536
@@ -129,6 +140,8 @@ def main():
         err2 = float((torch.cat(fs, dim=2) - f_ref).abs().max() / f_ref.abs().max())
         assert err2 < 1e-13, f"slab peer {shape} P={P}: {err2}"
         print(f"slab {shape} P={P} ok {err:.1e} peer {err2:.1e}", flush=True)
+    if len(sys.argv) > 2 and sys.argv[1] == "--dump":
+        np.savez(sys.argv[2], **DUMP)
     print(f"all cases ok in {time.time() - t0:.1f} s", flush=True)
 
 
