@@ -515,22 +515,20 @@ __global__ void __launch_bounds__(SRK_RT_CH) k_reduce_tma(const RedArgs a) {
   }
 }
 
+// One warp per reduced quantity (blockDim = 32 * SRK_NQ): lane l sums partials
+// l, l + 32, ... in order, then a fixed xor-shuffle tree -- deterministic, and
+// all nine sums proceed at once (the earlier one-block, nine-pass shared-memory
+// tree took ~15 us, a visible share of a 2D 1024^2 BS5 attempt).
 __global__ void k_finalize(const double* __restrict__ partial, int nblk, double* __restrict__ out) {
   pdl_launch_dependents();
   pdl_wait();
-  __shared__ double sh[256];
-  for (int q = 0; q < SRK_NQ; ++q) {
-    double v = 0.0;
-    for (int i = threadIdx.x; i < nblk; i += blockDim.x) v += partial[q * nblk + i];
-    sh[threadIdx.x] = v;
-    SRK_BAR();
-    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-      if ((int)threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
-      SRK_BAR();
-    }
-    if (threadIdx.x == 0) out[q] = sh[0];
-    SRK_BAR();
-  }
+  const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (q >= SRK_NQ) return;
+  double v = 0.0;
+  for (int i = lane; i < nblk; i += 32) v += partial[q * nblk + i];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  if (lane == 0) out[q] = v;
 }
 
 void srk_launch_reduce(const RedArgs& a, double* out, cudaStream_t st) {
@@ -545,7 +543,7 @@ void srk_launch_reduce(const RedArgs& a, double* out, cudaStream_t st) {
 #undef CASE
     default: break;
   }
-  srk_launch_k(k_finalize, dim3(1), dim3(256), 0, st, (const double*)a.partial, (int)SRK_RT_BLOCKS, out);
+  srk_launch_k(k_finalize, dim3(1), dim3(32 * SRK_NQ), 0, st, (const double*)a.partial, (int)SRK_RT_BLOCKS, out);
 }
 
 // ---------------------------------------------------------------------------
@@ -606,7 +604,7 @@ bool srk_launch_project_refresh(const ProjArgs& a, double* out, cudaStream_t st)
     grid = a.density ? launch_project_tma<3, true, 0, true>(a, st) : launch_project_tma<3, false, 0, true>(a, st);
   else
     grid = a.density ? launch_project_tma<2, true, 0, true>(a, st) : launch_project_tma<2, false, 0, true>(a, st);
-  srk_launch_k(k_finalize, dim3(1), dim3(256), 0, st, (const double*)a.partial, grid, out);
+  srk_launch_k(k_finalize, dim3(1), dim3(32 * SRK_NQ), 0, st, (const double*)a.partial, grid, out);
   return true;
 }
 
