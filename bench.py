@@ -88,29 +88,25 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def lib_sha256():
-    import hashlib
-
+def source_hash():
+    """srk_source_hash() of the loaded libsrk: kernel sources + compile flags."""
     from paper_1810_10197_b200 import _native
 
-    h = hashlib.sha256()
-    with open(_native.LIB_PATH, "rb") as fh:
-        for blk in iter(lambda: fh.read(1 << 22), b""):
-            h.update(blk)
-    return h.hexdigest()
+    return _native.load().srk_source_hash().decode()
 
 
 def ncu_counters(n, kernel):
     """Per-launch ncu counters of `kernel` at N = n from profiles/ncu_kernels.json,
-    only if that capture was taken of the libsrk.so loaded now (sha256 match);
-    otherwise None -- stale counters are never reported."""
+    only if that capture was taken of a build of the same kernel sources and flags
+    as the library loaded now (srk_source_hash match); otherwise None -- stale
+    counters are never reported."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_kernels.json")) as fh:
             d = json.load(fh)
     except Exception:
         return None, "no profiles/ncu_kernels.json"
-    if d.get("lib_sha256") != lib_sha256():
-        return None, "profiles/ncu_kernels.json was captured from another libsrk.so build"
+    if d.get("source_hash") != source_hash():
+        return None, "profiles/ncu_kernels.json was captured from other kernel sources"
     e = d.get(str(n), {}).get(kernel)
     return e, d.get("report")
 

@@ -259,6 +259,9 @@ int srk_probe(int mode, int iters, int blocks_per_sm, void* scratch, void* strea
 /* Build flags: bit 0 = hazard-probe build (make checks: schedule fuzzing at every
  * barrier, NaN-poisoned shared memory, tile bounds asserts; tools/check_build.sh). */
 int srk_build_info(void);
+/* Hash of the kernel sources + compile flags of this build (evidence provenance:
+ * bench.py reports ncu counters only from a capture of the same sources). */
+const char* srk_source_hash(void);
 
 /* Number of kernel launches the last srk_rhs issued (launch accounting for
  * the bench's gpu_launches claim). */

@@ -473,6 +473,11 @@ extern "C" {
 
 int srk_abi_version(void) { return 1; }
 
+#ifndef SRK_SRC_HASH
+#define SRK_SRC_HASH "unknown"
+#endif
+const char* srk_source_hash(void) { return SRK_SRC_HASH; }
+
 int srk_build_info(void) {
 #ifdef SRK_DEBUG_CHECKS
   return 1;  // hazard-probe build (schedule fuzzing, NaN-poisoned shared memory, asserts)

@@ -2,15 +2,16 @@
 
     python tools/ncu_kernels.py <report.ncu-rep> --n 512 [--lib paper_1810_10197_b200/_lib/libsrk.so]
 
-The JSON records the sha256 of the libsrk.so the capture was taken from; bench.py
-reports these counters (roofline.traffic, the z-pass's shared-memory wavefronts
-and fp64 flops) only when the loaded library has the same hash.
+The JSON records srk_source_hash() of the libsrk.so the capture was taken from
+(kernel sources + compile flags); bench.py reports these counters
+(roofline.traffic, the z-pass's shared-memory wavefronts and fp64 flops) only
+when the loaded library was built from the same sources.
 Capture command (GPU box, one GPU):
     ncu --set full --metrics smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,\
 smsp__sass_thread_inst_executed_op_dadd_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum \
         --clock-control none -k regex:"k_colpass|k_zpass|k_project" -s 6 -c 6 -o <report> \
         python tools/rhs_timing.py --n 512 --reps 2
-and then, on the same box (the hash must be of the binary that ran):
+and then, on the same box (the hash must be of the library that ran):
     python tools/ncu_kernels.py <report> --n 512
 """
 import argparse
@@ -83,10 +84,14 @@ def main():
         d = json.load(open(a.out))
     except Exception:
         d = {}
-    sha = sha256(a.lib)
-    if d.get("lib_sha256") != sha:
+    import ctypes
+
+    h = ctypes.CDLL(a.lib).srk_source_hash
+    h.restype = ctypes.c_char_p
+    src = h().decode()
+    if d.get("source_hash") != src:
         d = {}
-    d.update({"lib_sha256": sha, "report": os.path.relpath(a.report, ROOT),
+    d.update({"source_hash": src, "lib_sha256": sha256(a.lib), "report": os.path.basename(a.report),
               "source": "ncu --set full + sass per-opcode fp64 counters, one srk_rhs (tools/ncu_kernels.py)"})
     d[str(a.n)] = per
     with open(a.out, "w") as fh:
