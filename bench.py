@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--dry-run", action="store_true",
                     help="launcher / rank plumbing only: gloo ranks on the CPU, no GPU work (tests)")
     ap.add_argument("--no-1024", action="store_true", help="N >= 4: skip the 1024^3 E_P leg")
+    ap.add_argument("--ep-test", type=int, nargs=2, default=None, metavar=("N_BIG", "N_BASE"),
+                    help="slab mode: run the E_P leg at any world size with N_BIG^3 slabs and an N_BASE^3 "
+                         "single-GPU baseline (exercises the 1024^3 code path on small grids)")
     return ap.parse_args()
 
 
@@ -686,13 +689,14 @@ def run_slab(args, rank, world, local_rank):
 
     big = None
     rhs_peer, rhs_chunks = rhs.peer, len(rhs.chunks)
-    if world >= 4 and n == 512 and not args.no_1024:
+    ep_test = args.ep_test is not None
+    if (world >= 4 and n == 512 and not args.no_1024) or ep_test:
         rhs.close()
         del s, rhs, b, yk, fk
         if not args.no_e2e:
             del s2, mirror, yd
         try:
-            big = leg_1024(args, rank, world)
+            big = leg_1024(args, rank, world, *(args.ep_test if ep_test else ()))
         except Exception as exc:  # evidence leg: never lose the main line
             big = {"workload": "forced_hit_bs5_1024^3", "error": repr(exc)[:300]}
     if rank != 0:
@@ -802,10 +806,11 @@ def slab_ms_per_stage(args, n, steps, warmup, rank, world):
     return t.item()
 
 
-def leg_1024(args, rank, world):
+def leg_1024(args, rank, world, n_big=1024, n_base=512, mem_per_point=725e9 / 1024 ** 3):
     """SURVEY M4 at 1024^3 (does not fit one GPU): E_P = (B_stage(1024) / (P T_P)) /
     (B_stage(512) / T_1(512)), T = time per RHS evaluation, T_1 measured here on
-    rank 0 with the single-GPU path, T_P with the y-slab path on all P ranks."""
+    rank 0 with the single-GPU path, T_P with the y-slab path on all P ranks.
+    n_big / n_base: smaller grids exercise the same code path on one GPU (--ep-test)."""
     import gc
 
     import torch
@@ -815,22 +820,22 @@ def leg_1024(args, rank, world):
     torch.cuda.empty_cache()
     t1 = torch.zeros(1, dtype=torch.float64, device="cuda")
     if rank == 0:
-        t1[0] = single_gpu_ms_per_stage(512, steps=3, warmup=2)
+        t1[0] = single_gpu_ms_per_stage(n_base, steps=3, warmup=2)
         gc.collect()
         torch.cuda.empty_cache()
     dist.broadcast(t1, 0)
-    need = 725e9 / world  # measured footprint of a 1024^3 y-slab BS5 run
+    need = mem_per_point * n_big ** 3 / world  # 1024^3 y-slab BS5 run: ~725 GB in all
     free = float(torch.cuda.mem_get_info()[0])
     fits = torch.tensor([1.0 if free > 1.05 * need else 0.0], device="cuda")
     dist.all_reduce(fits, op=dist.ReduceOp.MIN)
-    out = {"workload": "forced_hit_bs5_1024^3", "T1_512_ms_per_stage": t1.item(),
+    out = {"workload": f"forced_hit_bs5_{n_big}^3", "T1_ms_per_stage": t1.item(), "T1_workload": f"{n_base}^3 on 1 GPU",
            "need_GB_per_gpu": need / 1e9, "free_GB_per_gpu": free / 1e9}
     if fits.item() < 1.0:
-        out["skipped"] = "1024^3 y-slab state does not fit this GPU count"
+        out["skipped"] = f"{n_big}^3 y-slab state does not fit this GPU count"
         return out
-    tp = slab_ms_per_stage(args, 1024, steps=2, warmup=1, rank=rank, world=world)
-    b1024, b512 = model_bytes(1024)["b_stage_bs5"], model_bytes(512)["b_stage_bs5"]
-    out.update({"TP_ms_per_stage": tp, "stages_per_s": 1e3 / tp, "gpts_stage_per_s": 1024 ** 3 / (tp * 1e-3) / 1e9,
+    tp = slab_ms_per_stage(args, n_big, steps=2, warmup=1, rank=rank, world=world)
+    b1024, b512 = model_bytes(n_big)["b_stage_bs5"], model_bytes(n_base)["b_stage_bs5"]
+    out.update({"TP_ms_per_stage": tp, "stages_per_s": 1e3 / tp, "gpts_stage_per_s": n_big ** 3 / (tp * 1e-3) / 1e9,
                 "E_P": (b1024 / (world * tp)) / (b512 / t1.item()), "P": world,
                 "E_P_definition": "SURVEY M4: per-GPU achieved model bandwidth at P GPUs (1024^3) / 1-GPU (512^3)"})
     return out

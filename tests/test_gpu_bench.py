@@ -51,3 +51,21 @@ def test_bench_slab_peer_exchange():
     d = run_bench("--mode", "slab", "--exchange", "peer", "--grid", "64", "--steps", "2", "--warmup", "3", "--no-e2e",
                   env={"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(random.randint(20000, 40000))})
     assert d["value"] > 0 and "peer stores" in d["config"]["parallelism"]
+
+
+def test_bench_strong_scaling_leg_code_path():
+    """The 1024^3 E_P leg (run at N >= 4) on small grids with one rank: rank 0's
+    single-GPU baseline, the fit check, the slab loop and E_P."""
+    d = run_bench("--mode", "slab", "--grid", "64", "--steps", "2", "--warmup", "3", "--no-e2e",
+                  "--ep-test", "128", "64",
+                  env={"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(random.randint(20000, 40000))})
+    big = d["strong_1024"]
+    assert big["workload"] == "forced_hit_bs5_128^3", big
+    assert big["T1_ms_per_stage"] > 0 and big["TP_ms_per_stage"] > 0 and big["P"] == 1
+    assert 0.05 < big["E_P"] < 5.0
+
+
+def test_bench_single_gpu_line_on_chip_ceilings():
+    d = run_bench("--grid", "64", "--steps", "3", "--warmup", "3", "--no-cpu", "--no-e2e")
+    c = d["roofline"]["on_chip_ceilings"]
+    assert c["probe"]["fp64_tflops"] > 5 and c["probe"]["smem_GBps"] > 5000
