@@ -167,6 +167,25 @@ def round2_cases(srk):
     out["rt3d_rk4"] = dict(y=r.state.fields, rec=_records(r))
     r = run(shape, "rayleigh_taylor", 1600.0, "bs5", "adaptive", 0.3, tol=1e-6, lengths=L)
     out["rt3d_bs5"] = dict(y=r.state.fields, rec=_records(r))
+    # the reference's `spectrum` command (cli.py:90-103) on a checkpoint it wrote
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as td:
+        spec = srk.ProblemSpec(kind="hit", params=srk.PhysParams(reynolds=500.0), seed=9, a=4.0, energy=0.5)
+        c = srk.RunConfig(grid_shape=(16, 16, 16), problem=spec, integrator="bs5", mode="adaptive", t_end=0.02,
+                          output_dir=td)
+        srk.run_simulation(c)
+        ck = os.path.join(td, "final.srkl")
+        from spectralrk.cli import build_parser, main as cli_main  # noqa: F401
+        import io
+        import contextlib
+
+        buf = io.StringIO()
+        with contextlib.redirect_stdout(buf):
+            cli_main(["spectrum", ck])
+        with open(ck, "rb") as fh:
+            out["spectrum_cli"] = dict(srkl=np.frombuffer(fh.read(), dtype=np.uint8),
+                                       text=np.frombuffer(buf.getvalue().encode(), dtype=np.uint8))
     return out
 
 

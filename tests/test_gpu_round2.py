@@ -164,3 +164,22 @@ def test_rt3d_window_vs_reference(integ):
     gold = R2[f"rt3d_{integ}"]
     _check_records(res, gold)
     assert rel(res.state.fields, gold["y"]) <= 1e-10
+
+
+def test_spectrum_entry_point_vs_reference_cli(tmp_path):
+    """`python -m paper_1810_10197_b200.spectrum CK` (reference cli.py:90-103) on a
+    checkpoint the reference wrote: same text layout, values to 1e-13."""
+    from paper_1810_10197_b200.spectrum import main, spectrum_text
+
+    c = R2["spectrum_cli"]
+    ck = tmp_path / "final.srkl"
+    ck.write_bytes(bytes(c["srkl"]))
+    want = bytes(c["text"]).decode().strip().splitlines()
+    got = spectrum_text(ck).strip().splitlines()
+    assert got[0] == want[0] == "k,E" and len(got) == len(want)
+    a = np.array([[float(v) for v in ln.split(",")] for ln in got[1:]])
+    b = np.array([[float(v) for v in ln.split(",")] for ln in want[1:]])
+    assert np.array_equal(a[:, 0], b[:, 0])
+    np.testing.assert_allclose(a[:, 1], b[:, 1], rtol=1e-13, atol=1e-30)
+    out = tmp_path / "spec.csv"
+    assert main([str(ck), "--out", str(out)]) == 0 and out.read_text().startswith("k,E\n")
