@@ -28,14 +28,14 @@ from . import _native
 from .control import AdvanceOutcome, adaptive_advance, propose_step
 from .integrators import _FUSED_MAX_TERMS
 
-__all__ = ["AttemptGraph", "attempt_graph"]
+__all__ = ["AttemptGraph", "attempt_graph", "GRAPH_MAX_FIELD_BYTES"]
 
 # captured graphs outlive one run_simulation call (a capture costs about two
 # attempts): keyed by everything a graph bakes in -- plan, physics, tableau,
 # tolerances, device; small states only (a graph holds ~s + 4 state-sized buffers)
 _CACHE = {}
 _CACHE_MAX = 4
-_CACHE_MAX_FIELD_BYTES = 256 << 20
+GRAPH_MAX_FIELD_BYTES = 256 << 20  # run_simulation graphs states up to this size (128^3: 51 MB, 2D 1024^2: 25 MB)
 
 
 def attempt_graph(rhs, pair, config, grid):
@@ -50,7 +50,7 @@ def attempt_graph(rhs, pair, config, grid):
     elif g.rhs is not rhs:
         g.rhs = rhs  # same plan and physics: the recorded launches are identical
     field_bytes = g.Y[0].numel() * g.Y[0].element_size()
-    if field_bytes <= _CACHE_MAX_FIELD_BYTES:
+    if field_bytes <= GRAPH_MAX_FIELD_BYTES:
         _CACHE[key] = g
         while len(_CACHE) > _CACHE_MAX:
             _CACHE.pop(next(iter(_CACHE)))

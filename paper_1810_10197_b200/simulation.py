@@ -347,10 +347,14 @@ def _run_adaptive(drv, max_steps=None):
     # launch-bound sizes: replay each first attempt from a CUDA graph (graphs.py);
     # unforced FSAL runs only (forcing refreshes f_now every step)
     graph = None
+    field_bytes = drv.y.numel() * drv.y.element_size()
     if drv.graphs and pair.fsal and not cfg.forcing:
-        from .graphs import attempt_graph
+        from .graphs import GRAPH_MAX_FIELD_BYTES, attempt_graph
 
-        graph = attempt_graph(drv.rhs, pair, cfg.controller, drv.grid)
+        # only where launches matter: a graph holds ~s + 4 state-sized buffers of
+        # its own, and at 256^3+ one RHS is milliseconds of kernels
+        if field_bytes <= GRAPH_MAX_FIELD_BYTES:
+            graph = attempt_graph(drv.rhs, pair, cfg.controller, drv.grid)
     n = 0
     while drv.t < t_end and (max_steps is None or n < max_steps):
         remaining = t_end - drv.t
