@@ -38,15 +38,16 @@ _CACHE_MAX = 4
 GRAPH_MAX_FIELD_BYTES = 256 << 20  # run_simulation graphs states up to this size (128^3: 51 MB, 2D 1024^2: 25 MB)
 
 
-def attempt_graph(rhs, pair, config, grid):
-    """The cached AttemptGraph for this (plan, physics, pair, tolerances, device)."""
+def attempt_graph(rhs, pair, config, grid, fixed=False):
+    """The cached AttemptGraph for this (plan, physics, pair, tolerances, mode, device)."""
     p = rhs.params
+    tol = (0.0, 0.0) if fixed else (float(config.tol_abs), float(config.tol_rel))
     key = (rhs.plan.h.value if hasattr(rhs.plan.h, "value") else int(rhs.plan.h), tuple(grid.shape),
            tuple(grid.lengths), rhs.density, float(p.reynolds), float(p.richardson), float(p.prandtl), pair.name,
-           float(config.tol_abs), float(config.tol_rel), torch.cuda.current_device())
+           tol, bool(fixed), torch.cuda.current_device())
     g = _CACHE.pop(key, None)
     if g is None:
-        g = AttemptGraph(rhs, pair, config, grid)
+        g = AttemptGraph(rhs, pair, config, grid, fixed=fixed)
     elif g.rhs is not rhs:
         g.rhs = rhs  # same plan and physics: the recorded launches are identical
     field_bytes = g.Y[0].numel() * g.Y[0].element_size()
@@ -61,10 +62,11 @@ def attempt_graph(rhs, pair, config, grid):
 class AttemptGraph:
     """One replayable adaptive attempt of ``pair`` (FSAL, embedded) on ``rhs``."""
 
-    def __init__(self, rhs, pair, config, grid):
-        if not (pair.fsal and pair.b_hat is not None):
-            raise ValueError("AttemptGraph needs an FSAL pair with embedded weights")
+    def __init__(self, rhs, pair, config, grid, fixed=False):
+        if not fixed and not (pair.fsal and pair.b_hat is not None):
+            raise ValueError("an adaptive AttemptGraph needs an FSAL pair with embedded weights")
         self.rhs, self.pair, self.cfg, self.grid = rhs, pair, config, grid
+        self.fixed = bool(fixed)
         shape = (rhs.ncomp,) + tuple(grid.kshape)
         dev = torch.device("cuda", torch.cuda.current_device())
         self.Y = [torch.zeros(shape, dtype=torch.complex128, device=dev) for _ in range(2)]
@@ -97,15 +99,20 @@ class AttemptGraph:
             _native.count(1)
 
         # stage 2 input y + (h a21) F1 (integrators.py:327-333)
-        x = torch.empty_like(y) if s > 2 else self.Y[1 - p]
+        fsal = self.pair.fsal
+        y_new = self.Y[1 - p]
+        x = torch.empty_like(y) if s > 2 else y_new
         combine(y, [(A[1, j], stages[j]) for j in range(1) if A[1, j] != 0.0], x)
         for i in range(1, s):
             last = i == s - 1
-            f = self.FL[1 - p] if last else torch.empty_like(y)
-            row = A[i + 1] if i + 1 < s else None  # FSAL: the last stage's input is y_new
-            nxt = None
+            f = self.FL[1 - p] if (last and fsal) else torch.empty_like(y)
+            # the accumulation that consumes stage i: the next stage input (FSAL: the
+            # last stage's input is y_new) or, for non-FSAL pairs, y_new itself
+            if i + 1 < s:
+                row, nxt = A[i + 1], (y_new if (fsal and i + 1 == s - 1) else torch.empty_like(y))
+            else:
+                row, nxt = (None, None) if fsal else (b, y_new)
             if row is not None:
-                nxt = self.Y[1 - p] if i + 1 == s - 1 else torch.empty_like(y)
                 terms = [(row[j], stages[j]) for j in range(i) if row[j] != 0.0]
                 if row[i] != 0.0 and len(terms) <= _FUSED_MAX_TERMS:
                     Fs = [F for _, F in terms]
@@ -122,11 +129,22 @@ class AttemptGraph:
             if row is not None:
                 combine(y, [(row[j], stages[j]) for j in range(i + 1) if row[j] != 0.0], nxt)
                 x = nxt
+        fl = self.FL[1 - p]
+        if self.fixed:
+            # fixed step: the cached tendency of y_new (FSAL stage, or a fresh RHS --
+            # simulation.py:165-182) and the diagnostics record's sums (diagnostics.py:48-70)
+            if not fsal:
+                self.rhs(0.0, y_new, out=fl)
+            _native.check(lib.srk_step_reduce(
+                pl.bind(), _native.ptr(y), _native.ptr(y_new), 0, _native.ptr_array([]), _native.dbl_array([]),
+                _native.ptr(fl), y.shape[0], 0.0, 0.0, 2, _native.ptr(self.q_pin), _native.stream_ptr()),
+                "srk_step_reduce")
+            _native.count(2)
+            return
         # embedded error + E / eps / Z sums (control.py:51-79, diagnostics.py:48-70)
         d = b - self.pair.b_hat
         terms = [(d[i], stages[i]) for i in range(s) if d[i] != 0.0]
         Fs = [F for _, F in terms]
-        y_new, fl = self.Y[1 - p], self.FL[1 - p]
         _native.check(lib.srk_step_reduce_scaled(
             pl.bind(), _native.ptr(y), _native.ptr(y_new), len(Fs), _native.ptr_array(Fs),
             _native.dbl_array([a for a, _ in terms]), hp, _native.ptr(fl), y.shape[0], float(self.cfg.tol_abs),
@@ -159,6 +177,20 @@ class AttemptGraph:
         self.Y[0].copy_(y)
         self.FL[0].copy_(f_now)
         return 0
+
+    def step_fixed(self, y, h, f_now):
+        """One fixed step of run_simulation's loop (simulation.py:250-271): returns
+        (y_new, f_new, sums) with f_new the cached tendency of y_new (FSAL stage or a
+        fresh RHS) and sums the diagnostics record's reduce_sums values."""
+        p = self._slot(y, f_now)
+        if self.graphs[p] is None:
+            self._capture(p)
+        self.h_pin[0] = h
+        self.graphs[p].replay()
+        _native.count(self.launches[p])
+        self.replays += 1
+        torch.cuda.current_stream().synchronize()
+        return self.Y[1 - p], self.FL[1 - p], self.q_pin.tolist()
 
     def advance(self, y, t, state, first_stage):
         """adaptive_advance(y, t, pair, state, config, rhs, first_stage) with the first

@@ -292,8 +292,23 @@ def _run_fixed(drv, max_steps=None):
     total, n_full, h_last, time_at = _fixed_step_times(drv, h, t_end)
     if max_steps is not None:
         total = min(total, max_steps)
+    graph = None
+    if drv.graphs and not cfg.forcing and drv.y.numel() * drv.y.element_size() <= _graph_max_bytes():
+        from .graphs import attempt_graph
+
+        graph = attempt_graph(drv.rhs, pair, cfg.controller, drv.grid, fixed=True)
     for i in range(total):
         h_i = h if i < n_full else h_last
+        if graph is not None:  # the whole step + the cached tendency + the record's sums, one replay
+            drv.y, drv.f_now, sums = graph.step_fixed(drv.y, h_i, drv.f_now)
+            if sums[6] > 0:
+                raise NonFiniteStateError(f"non-finite state at t={time_at(i)}")
+            drv.evals += pair.s - 1 + (0 if pair.fsal else 1)
+            drv.t = time_at(i)
+            drv.steps += 1
+            drv.record(h_i, sums=sums)
+            drv.maybe_checkpoint()
+            continue
         stages, y_new, ev = run_stages(drv.rhs, drv.y, drv.t, h_i, pair, drv.f_now)
         drv.evals += ev
         drv.y = y_new
@@ -301,6 +316,9 @@ def _run_fixed(drv, max_steps=None):
         drv.after_accept(stages[-1] if pair.fsal else None, fsal_ok=pair.fsal)
         drv.record(h_i)
         drv.maybe_checkpoint()
+    if graph is not None:  # hand back buffers the graph will not overwrite
+        drv.y = drv.y.clone()
+        drv.f_now = drv.f_now.clone()
 
 
 def _run_ab2(drv, h, t_end, max_steps=None):
@@ -392,6 +410,12 @@ def _run_adaptive(drv, max_steps=None):
 
 
 USE_GRAPHS = True  # default for run_simulation(graphs=None)
+
+
+def _graph_max_bytes():
+    from .graphs import GRAPH_MAX_FIELD_BYTES
+
+    return GRAPH_MAX_FIELD_BYTES
 
 
 def run_simulation(config, resume=None, initial_state=None, max_steps=None, graphs=None):

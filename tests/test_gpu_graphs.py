@@ -58,3 +58,19 @@ def test_scaled_entry_points_equal_host_products():
                                          _native.dbl_array(a), _native.ptr(hd), _native.ptr(out),
                                          _native.stream_ptr()), "srk_combine_scaled")
     assert torch.equal(out, ref)
+
+
+@pytest.mark.parametrize("shape,kind,integ,h,t_end", [
+    ((32, 32, 32), "taylor_green", "rk4", 0.01, 0.305),   # config 1 RK4, uneven tail step
+    ((64, 256), "rayleigh_taylor", "rk4", 2e-3, 0.05),    # 2D Boussinesq (config 4 family)
+    ((16, 16, 16), "hit", "dp5", 0.02, 0.1),               # FSAL pair on fixed steps
+])
+def test_fixed_step_graph_bit_identical(shape, kind, integ, h, t_end):
+    lengths = srk.default_lengths(kind, shape)
+    spec = srk.ProblemSpec(kind, params=srk.PhysParams(1000.0), seed=5, a=4.0, energy=0.5)
+    cfg = srk.RunConfig(grid_shape=shape, problem=spec, integrator=integ, mode="fixed", t_end=t_end, h=h,
+                        lengths=lengths)
+    r0, r1 = _both(cfg)
+    assert r1.steps == r0.steps and r1.rhs_evals == r0.rhs_evals
+    assert np.array_equal(_records(r0), _records(r1))
+    assert torch.equal(r0.state.fields, r1.state.fields)

@@ -34,6 +34,17 @@ def case(name):
         cfg = srk.RunConfig(grid_shape=(1024, 1024), problem=rt, integrator="bs5", mode="adaptive", t_end=2.0,
                             lengths=g.lengths)
         return cfg, srk.rt_tanh_init(g, width=0.05, amp=1e-3, kmax=8, seed=4)
+    if name == "c1rk4":
+        return srk.RunConfig(grid_shape=(32,) * 3, problem=tg, integrator="rk4", mode="fixed", t_end=1.0, h=0.01), None
+    if name == "c2rk4":  # config 2's RK4 run, first quarter (t <= 0.5, 500 steps)
+        return srk.RunConfig(grid_shape=(128,) * 3, problem=tg, integrator="rk4", mode="fixed", t_end=0.5,
+                             h=1e-3), None
+    if name == "c4rk4":  # config 4's RK4 h = 1e-3 run, first 1000 steps
+        g = srk.Grid((1024, 1024))
+        rt = srk.ProblemSpec("rayleigh_taylor", params=srk.PhysParams(1e4, 1.0, 1.0))
+        cfg = srk.RunConfig(grid_shape=(1024, 1024), problem=rt, integrator="rk4", mode="fixed", t_end=1.0,
+                            h=1e-3, lengths=g.lengths)
+        return cfg, srk.rt_tanh_init(g, width=0.05, amp=1e-3, kmax=8, seed=4)
     raise SystemExit(name)
 
 
@@ -55,7 +66,8 @@ def run(name, graphs, reps=3):
 
 
 def main():
-    names = ["c1", "c4", "c2"] if len(sys.argv) < 2 or sys.argv[1] == "all" else sys.argv[1:]
+    names = (["c1", "c4", "c2", "c1rk4", "c4rk4", "c2rk4"] if len(sys.argv) < 2 or sys.argv[1] == "all"
+             else sys.argv[1:])
     for name in names:
         r0, rec0, w0 = run(name, False)
         r1, rec1, w1 = run(name, True)
