@@ -1014,9 +1014,11 @@ __global__ void __launch_bounds__(EngI::NT, (OP == ZOP_B2 ? SRK_ZB2P_MINB : (M <
           bulk_prefetch_l2(a.in + s * a.in_sig_stride + (long long)q0 * K, (unsigned)(K * 16));
     }
   }
+  // every thread waits on the mbarrier itself (the TMA rows are then visible to
+  // it); the twiddle table (cp.async by all threads) is first read in the second
+  // inverse stage, after the first stage's CTA barrier -- no barrier here
   mbar_wait(&mbar, 0);
   cp_async_wait_all();
-  SRK_BAR();
   SRK_TS(1)
   {
     ZHermLoad<M> ld{stg};

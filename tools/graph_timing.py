@@ -34,6 +34,12 @@ def case(name):
         cfg = srk.RunConfig(grid_shape=(1024, 1024), problem=rt, integrator="bs5", mode="adaptive", t_end=2.0,
                             lengths=g.lengths)
         return cfg, srk.rt_tanh_init(g, width=0.05, amp=1e-3, kmax=8, seed=4)
+    if name == "c4full":  # config 4 as BASELINE states it: BS5 tol 1e-6 to t = 10
+        g = srk.Grid((1024, 1024))
+        rt = srk.ProblemSpec("rayleigh_taylor", params=srk.PhysParams(1e4, 1.0, 1.0))
+        cfg = srk.RunConfig(grid_shape=(1024, 1024), problem=rt, integrator="bs5", mode="adaptive", t_end=10.0,
+                            lengths=g.lengths)
+        return cfg, srk.rt_tanh_init(g, width=0.05, amp=1e-3, kmax=8, seed=4)
     if name == "c1rk4":
         return srk.RunConfig(grid_shape=(32,) * 3, problem=tg, integrator="rk4", mode="fixed", t_end=1.0, h=0.01), None
     if name == "c2rk4":  # config 2's RK4 run, first quarter (t <= 0.5, 500 steps)
@@ -48,11 +54,12 @@ def case(name):
     raise SystemExit(name)
 
 
-def run(name, graphs, reps=3):
+def run(name, graphs, reps=None):
     """Best of `reps` full runs after a full warm-up run (plans, twiddles, graph captures)."""
     cfg, ic = case(name)
     st = ic if ic is not None else srk.make_initial_state(cfg)
-    srk.run_simulation(cfg, initial_state=st, graphs=graphs)  # warm-up
+    reps = reps or (1 if name.endswith("full") else 3)
+    srk.run_simulation(cfg, initial_state=st, graphs=graphs, max_steps=200 if name.endswith("full") else None)  # warm-up
     wall = None
     for _ in range(reps):
         torch.cuda.synchronize()
