@@ -10,7 +10,8 @@ timeout 2400 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.log 2>&1; echo "
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1
 timeout 900 python bench.py > $OUT/bench512.json 2> $OUT/bench512.err
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
-timeout 900 python tools/graph_timing.py c1 c4 > $OUT/graph_timing.jsonl 2>&1
+timeout 900 python bench.py --grid 256 --no-cpu > $OUT/bench256.json 2> $OUT/bench256.err
+timeout 1500 python tools/graph_timing.py c1 c1rk4 c4 c4rk4 c2 c2rk4 > $OUT/graph_timing.jsonl 2>&1
 timeout 600 python tools/cufft_passes.py > $OUT/cufft_passes.json 2> $OUT/cufft_passes.err
 M=smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,smsp__sass_thread_inst_executed_op_dadd_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum
 timeout 300 python tools/rhs_timing.py --n 512 --reps 2 > $OUT/rhs_plain.log 2>&1 && \
