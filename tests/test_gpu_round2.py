@@ -183,3 +183,16 @@ def test_spectrum_entry_point_vs_reference_cli(tmp_path):
     np.testing.assert_allclose(a[:, 1], b[:, 1], rtol=1e-13, atol=1e-30)
     out = tmp_path / "spec.csv"
     assert main([str(ck), "--out", str(out)]) == 0 and out.read_text().startswith("k,E\n")
+
+
+@pytest.mark.parametrize("shape", [(6, 10, 512), (8, 8, 512), (4, 6, 512)])
+def test_paired_zpass_pencil_counts_vs_oracle(shape):
+    """The 512-point z axis runs the paired z-pass (two pencils per CTA, A's P2 packed
+    into B's forward column): even and odd pencil counts (135 = 9 x 15: the last CTA
+    pairs its pencil with a zero pencil) vs the oracle."""
+    og = O.OGrid(shape)
+    rng = np.random.default_rng(12)
+    y = O.fwd(rng.standard_normal((3,) + shape), og)
+    f_ref = O.OracleRHS(og, 300.0)(0.0, y)
+    f = srk.FlowRHS(srk.Grid(shape), srk.PhysParams(300.0))(0.0, dev(y))
+    assert rel(f, f_ref) <= 1e-12
