@@ -250,8 +250,9 @@ int srk_debug_phase_buffer(srk_plan* plan, void* dev_buf, int launch_index);
 /* Throughput probe (not a compute entry point): one launch of blocks_per_sm
  * x SMs CTAs of 256 threads, each thread running `iters` trips of 8 ops:
  * mode 0 fp64 FMA, 1 fp64 add, 2 16-byte shared-memory loads, 3 warp
- * shuffles, 4 two shared loads + eight shuffles interleaved.  scratch: a
- * device buffer of >= blocks_per_sm * SMs doubles.  *ops_out = thread-level
+ * shuffles, 4 two shared loads + eight shuffles interleaved, 5 16-byte global
+ * loads hitting L1, 6 two global (L1-hit) + two shared loads interleaved.
+ * scratch: a device buffer of >= max(blocks_per_sm * SMs doubles, 64 KB).  *ops_out = thread-level
  * operations issued (time the launch with events on `stream`).  Used by
  * bench.py for the measured fp64 ceiling of the z-pass. */
 int srk_probe(int mode, int iters, int blocks_per_sm, void* scratch, void* stream, double* ops_out);

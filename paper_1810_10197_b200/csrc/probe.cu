@@ -5,6 +5,9 @@
 //   mode 2: LDS.128    -- shared-memory crossbar: 16 B loads, conflict free
 //   mode 3: SHFL.32    -- warp shuffles (xor pattern), 8 independent chains
 //   mode 4: LDS.128 + SHFL interleaved (do they share the MIO datapath?)
+//   mode 5: LDG.128 of L1-resident global data (16 B per lane, coalesced)
+//   mode 6: LDG.128 (L1 hits) + LDS.128 interleaved (does global-load data share
+//           the shared-memory datapath?)
 // Each thread runs `iters` loop trips; the result is folded into out[] so the
 // compiler cannot drop the work.  Units of work per trip and thread: 8 ops.
 #include <cuda_runtime.h>
@@ -16,9 +19,10 @@
 namespace {
 
 template <int MODE>
-__global__ void __launch_bounds__(256) k_probe(double* out, int iters, double b, double c) {
+__global__ void __launch_bounds__(256) k_probe(double* out, int iters, double b, double c, const uint4* gsrc) {
   __shared__ __align__(16) uint4 buf[2048];  // 32 KB
   const int tid = threadIdx.x;
+  const int salt = (iters >> 30) + 1;
   double acc[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc[i] = (double)(tid + i) * 1e-3;
@@ -56,6 +60,26 @@ __global__ void __launch_bounds__(256) k_probe(double* out, int iters, double b,
 #pragma unroll
         for (int i = 0; i < 8; ++i) x[i] = __shfl_xor_sync(0xffffffffu, x[i], 1 + (i & 15)) + (unsigned)it;
       }
+      if constexpr (MODE == 5 || MODE == 6) {
+        // 8 KB per warp slot, re-read every trip: L1 resident.  salt == 1 at run
+        // time, unknown to the compiler: the trip's addresses cannot be hoisted
+#pragma unroll
+        for (int i = 0; i < (MODE == 6 ? 2 : 8); ++i) {
+          const uint4 v = __ldg(gsrc + ((((it * salt * 8 + i) * 32 + lane) & 511) + (tid >> 5) * 512));
+          y.x ^= v.x;
+          y.y ^= v.y;
+          y.z ^= v.z;
+          y.w ^= v.w;
+        }
+      }
+      if constexpr (MODE == 6) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const uint4 v = buf[((it * 8 + i) * 32 + lane + (tid >> 5) * 256) & 2047];
+          y.x += v.x;
+          y.y += v.y;
+        }
+      }
     }
     unsigned s = y.x ^ y.y ^ y.z ^ y.w;
 #pragma unroll
@@ -71,20 +95,24 @@ __global__ void __launch_bounds__(256) k_probe(double* out, int iters, double b,
 }  // namespace
 
 extern "C" int srk_probe(int mode, int iters, int blocks_per_sm, void* scratch, void* stream, double* ops_out) {
-  if (mode < 0 || mode > 4 || iters < 1 || blocks_per_sm < 1 || !scratch) return SRK_ERR_INVALID;
+  if (mode < 0 || mode > 6 || iters < 1 || blocks_per_sm < 1 || !scratch) return SRK_ERR_INVALID;
   const int grid = blocks_per_sm * srk_sm_count();
   cudaStream_t st = (cudaStream_t)stream;
   double* out = (double*)scratch;
+  // modes 5/6 read 8 KB per warp of scratch (scratch must hold >= 8 warps x 8 KB = 64 KB)
+  const uint4* g = (const uint4*)scratch;
   switch (mode) {
-    case 0: k_probe<0><<<grid, 256, 0, st>>>(out, iters, 0.999999, 1e-7); break;
-    case 1: k_probe<1><<<grid, 256, 0, st>>>(out, iters, 0.999999, 1e-7); break;
-    case 2: k_probe<2><<<grid, 256, 0, st>>>(out, iters, 0.0, 0.0); break;
-    case 3: k_probe<3><<<grid, 256, 0, st>>>(out, iters, 0.0, 0.0); break;
-    default: k_probe<4><<<grid, 256, 0, st>>>(out, iters, 0.0, 0.0); break;
+    case 0: k_probe<0><<<grid, 256, 0, st>>>(out, iters, 0.999999, 1e-7, g); break;
+    case 1: k_probe<1><<<grid, 256, 0, st>>>(out, iters, 0.999999, 1e-7, g); break;
+    case 2: k_probe<2><<<grid, 256, 0, st>>>(out, iters, 0.0, 0.0, g); break;
+    case 3: k_probe<3><<<grid, 256, 0, st>>>(out, iters, 0.0, 0.0, g); break;
+    case 4: k_probe<4><<<grid, 256, 0, st>>>(out, iters, 0.0, 0.0, g); break;
+    case 5: k_probe<5><<<grid, 256, 0, st>>>(out, iters, 0.0, 0.0, g); break;
+    default: k_probe<6><<<grid, 256, 0, st>>>(out, iters, 0.0, 0.0, g); break;
   }
   // thread-level operations issued (mode 0: FMAs; mode 2: 16 B loads; mode 3: shuffles;
-  // mode 4: 2 loads + 8 shuffles per trip)
-  const double per_trip = mode == 4 ? 10.0 : 8.0;
+  // mode 4: 2 loads + 8 shuffles per trip; mode 5: 16 B global loads; mode 6: 2 + 2 loads)
+  const double per_trip = mode == 4 ? 10.0 : (mode == 6 ? 4.0 : 8.0);
   if (ops_out) *ops_out = per_trip * (double)iters * 256.0 * (double)grid;
   return cudaGetLastError() == cudaSuccess ? SRK_OK : SRK_ERR_CUDA;
 }

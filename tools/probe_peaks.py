@@ -58,7 +58,7 @@ def main():
     a = ap.parse_args()
     torch.cuda.init()
     nsm = torch.cuda.get_device_properties(0).multi_processor_count
-    scratch = torch.zeros(64 * nsm, dtype=torch.float64, device="cuda")
+    scratch = torch.zeros(max(64 * nsm, 8192), dtype=torch.float64, device="cuda")
     out = {"sms": nsm}
     run(0, 1000, 4, scratch, reps=2)  # warm-up
     ops, ms = run(0, 20000, 4, scratch)
@@ -81,6 +81,16 @@ def main():
     out["mix_lds_only_ms"] = round(ms_l, 4)
     out["mix_shfl_only_ms"] = round(ms_s, 4)
     out["shfl_shares_lds_path"] = bool(ms_mix > 0.8 * (ms_l + ms_s))
+    # global loads served from L1 vs shared loads: separate or shared datapath?
+    ops, ms = run(5, 4000, 4, scratch)
+    out["ldg128_L1hit_B_per_clk_sm_at_1965"] = round(16 * ops / (ms * 1e-3) / nsm / 1.965e9, 1)
+    _, ms_gl = run(6, 4000, 4, scratch)        # 2 LDG + 2 LDS per trip
+    _, ms_g = run(5, 1000, 4, scratch)         # 8 LDG per trip x 1000 = the same LDG count
+    _, ms_l2 = run(2, 1000, 4, scratch)        # 8 LDS per trip x 1000 = the same LDS count
+    out["mix_ldg_lds_ms"] = round(ms_gl, 4)
+    out["ldg_only_ms"] = round(ms_g, 4)
+    out["lds_only_ms"] = round(ms_l2, 4)
+    out["ldg_shares_lds_path"] = bool(ms_gl > 0.8 * (ms_g + ms_l2))
     out["device"] = torch.cuda.get_device_name(0)
     print(json.dumps(out))
 
