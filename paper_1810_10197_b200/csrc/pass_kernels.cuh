@@ -60,6 +60,7 @@ struct PassArgs {
   // rpb == 0 means plain rows.  y0 / n1g: global y of the slab's first row and
   // the global y extent (wavenumber labels in the curl).
   int in_rpb, out_rpb;
+  unsigned in_magic, out_magic;  // ceil(2^32 / rpb) of the row blocks (row_blk; set by launch_col)
   long long in_bstride, out_bstride;
   int y0, n1g;
   int xplanes;  // PK_INV_CURLY: x planes per signal (m0, or m0/P on a slab)
@@ -76,6 +77,8 @@ struct PassArgs {
   int tma_rows;  // rows per TMA box (divides the staged row count)
   int tma_out;   // 1: inverse passes write their output tile with 3D TMA stores
   int tmo_rows;  // rows per output box (divides M)
+  int probe;     // measurement only (SRK_PROBE_FWD, tools/pass_probe.sh): padded forward passes stage
+                 // their tile and return (1) or also store zeros in the output pattern (2)
   // Column groups (kz chunks of the pipelined slab RHS): the Qp columns of a
   // plane are ngrp groups of kc columns; group g, local column c sits at
   // memory column g*in_kst + in_k0 + c of the input (out_* for the output),
@@ -100,9 +103,14 @@ struct PassArgs {
     dbg_[i] = clock64();   \
   }
 
-SRK_DEV unsigned row_off(int row, unsigned rs, int rpb, long long bstride) {
+// magic = ceil(2^32 / rpb) (0 for rpb == 1): row / rpb = (row * magic) >> 32, exact for
+// row * rpb < 2^32 -- one multiply instead of a division per access (launch_col sets it)
+SRK_DEV int row_blk(int row, unsigned magic) {
+  return magic ? (int)(((unsigned long long)(unsigned)row * magic) >> 32) : row;
+}
+SRK_DEV unsigned row_off(int row, unsigned rs, int rpb, long long bstride, unsigned magic) {
   if (rpb <= 0) return (unsigned)row * rs;
-  const int blk = row / rpb;
+  const int blk = row_blk(row, magic);
   return (unsigned)blk * (unsigned)bstride + (unsigned)(row - blk * rpb) * rs;
 }
 
@@ -114,11 +122,11 @@ SRK_DEV unsigned row_off(int row, unsigned rs, int rpb, long long bstride) {
 // addresses).  Generic path: loaders read global memory directly.
 template <int C>
 __device__ __forceinline__ void stage_rows(cplx* dst, const cplx* __restrict__ src, int rows, unsigned rs,
-                                           int ncols, int rpb, long long bstride) {
+                                           int ncols, int rpb, long long bstride, unsigned magic) {
   const int tot = rows * C;
   for (int i = threadIdx.x; i < tot; i += blockDim.x) {
     const int r = i / C, c = i - (i / C) * C;
-    if (c < ncols) cp_async16(dst + i, src + row_off(r, rs, rpb, bstride) + (unsigned)c);
+    if (c < ncols) cp_async16(dst + i, src + row_off(r, rs, rpb, bstride, magic) + (unsigned)c);
   }
 }
 
@@ -166,7 +174,15 @@ __device__ __forceinline__ void tma_stage(cplx* sm, const CUtensorMap* tm, int w
     mbar_expect_tx(bar, bytes);
     // rows are (row in block, block) -- blocked slab receive layouts; plain rows
     // are one block of `rows`
-    if (rpb > 0) {  // 5D map
+    // a box is part of one row block or a run of whole blocks
+    if (rpb < 0) {  // blocked rows of an unchunked pass: 4D map {columns, row in block, block, plane}
+      const int rb = -rpb;
+      for (int b = 0; b < nb; ++b) {
+        const int r0 = b * box, blk = r0 / rb;
+        tma_load_4d(sm + b * box * C, tm, 2 * wl, r0 - blk * rb, blk, plA, bar);
+        if (plB >= 0) tma_load_4d(sm + boff + b * box * C, tm, 2 * wl, r0 - blk * rb, blk, plB, bar);
+      }
+    } else if (rpb > 0) {  // 5D map {columns, column group, row in block, block, plane}
       for (int b = 0; b < nb; ++b) {
         const int r0 = b * box, blk = r0 / rpb;
         tma_load_5d(sm + b * box * C, tm, 2 * wl, g, r0 - blk * rpb, blk, plA, bar);
@@ -225,10 +241,10 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
   const int orpb_ = (FL & PF_BOUT) ? a.out_rpb : 0;
   auto oel = [&](int row, int col) -> cplx& {
     if constexpr ((FL & PF_PEER) != 0) {
-      const int blk = row / orpb_;
+      const int blk = row_blk(row, a.out_magic);
       return s_peer[blk][(unsigned)(row - blk * orpb_) * rso_ + (unsigned)col];
     } else {
-      return outp[row_off(row, rso_, orpb_, a.out_bstride) + (unsigned)col];
+      return outp[row_off(row, rso_, orpb_, a.out_bstride, a.out_magic) + (unsigned)col];
     }
   };
   const int M = CTN ? Eng::M : a.M;
@@ -237,7 +253,8 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
   const int out_rpb = (FL & PF_BOUT) ? a.out_rpb : 0;
   // TMA staging: plain (unblocked) input rows of the fast engines
   constexpr bool kTMA = Eng::kFast && KIND != PK_INV_RHS;
-  const int trpb = in_rpb;  // > 0: blocked input rows (5D TMA map)
+  // > 0: blocked input rows (5D TMA map); < 0: blocked rows, one column group (4D map)
+  const int trpb = (in_rpb > 0 && a.tma == 2) ? -in_rpb : in_rpb;
   __shared__ __align__(8) unsigned long long tbar;
   const bool use_tma = kTMA && a.tma;
   // TMA output: the last stage writes a dense [M][C] tile in smem (over the
@@ -272,7 +289,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
       tma_stage<C>(sm, &tm, wl, g, n, a.tma_rows, trpb, plane, -1, 0, &tbar);
       SRK_TS(1)
     } else if constexpr (Eng::kFast) {
-      stage_rows<C>(sm, inp, n, rs, ncols, in_rpb, a.in_bstride);
+      stage_rows<C>(sm, inp, n, rs, ncols, in_rpb, a.in_bstride, a.in_magic);
       cp_async_wait_all();
       SRK_BAR();
       SRK_TS(1)
@@ -281,7 +298,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
       const int cr = pad_src(row, n, M);
       const bool ok = cr >= 0;
       const int r = ok ? cr : 0;
-      cplx v = Eng::kFast ? sm[r * C + col] : inp[row_off(r, rs, in_rpb, a.in_bstride) + (unsigned)col];
+      cplx v = Eng::kFast ? sm[r * C + col] : inp[row_off(r, rs, in_rpb, a.in_bstride, a.in_magic) + (unsigned)col];
       const double f = ok ? sc : 0.0;
       return cmk(v.x * f, v.y * f);
     };
@@ -331,8 +348,8 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
     const double sc = a.scale;
     cplx* sb_ = sm + (is_curl ? n * C : 0);
     if constexpr (Eng::kFast) {
-      stage_rows<C>(sm, pa, n, rs, ncols, in_rpb, a.in_bstride);
-      if (is_curl) stage_rows<C>(sm + n * C, pb, n, rs, ncols, in_rpb, a.in_bstride);
+      stage_rows<C>(sm, pa, n, rs, ncols, in_rpb, a.in_bstride, a.in_magic);
+      if (is_curl) stage_rows<C>(sm + n * C, pb, n, rs, ncols, in_rpb, a.in_bstride, a.in_magic);
       cp_async_wait_all();
       SRK_BAR();
       SRK_TS(1)
@@ -341,7 +358,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
       const int cr = pad_src(row, n, M);
       const bool ok = cr >= 0;
       const int r = ok ? cr : 0;
-      const unsigned off = row_off(r, rs, in_rpb, a.in_bstride) + (unsigned)col;
+      const unsigned off = row_off(r, rs, in_rpb, a.in_bstride, a.in_magic) + (unsigned)col;
       const cplx ua = Eng::kFast ? sm[r * C + col] : pa[off];
       const cplx ub = Eng::kFast ? sb_[r * C + col] : pb[off];
       // spectral.py:47-65: w = i k x u (k_a = mode_a * 2pi/L_a, grid.py:75-93)
@@ -368,7 +385,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
       tma_stage<C>(sm, &tm, wl, g, n, a.tma_rows, trpb, comp, -1, 0, &tbar);
       SRK_TS(1)
     } else if constexpr (Eng::kFast) {
-      stage_rows<C>(sm, pa, n, rs, ncols, in_rpb, a.in_bstride);
+      stage_rows<C>(sm, pa, n, rs, ncols, in_rpb, a.in_bstride, a.in_magic);
       cp_async_wait_all();
       SRK_BAR();
       SRK_TS(1)
@@ -377,7 +394,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
       const int cr = pad_src(row, n, M);
       const bool ok = cr >= 0;
       const int r = ok ? cr : 0;
-      const cplx u = Eng::kFast ? sm[r * C + col] : pa[row_off(r, rs, in_rpb, a.in_bstride) + (unsigned)col];
+      const cplx u = Eng::kFast ? sm[r * C + col] : pa[row_off(r, rs, in_rpb, a.in_bstride, a.in_magic) + (unsigned)col];
       const double kx = mode_full(r, n) * a.ck0;
       const double f = ok ? (use_kx ? kx * sc : sc) : 0.0;
       return cmk(u.x * f, u.y * f);
@@ -413,8 +430,8 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
       tma_stage<C>(sm, &tm, wl, g, n, a.tma_rows, trpb, ca * X + x, is_curl ? cb * X + x : -1, n * C, &tbar);
       SRK_TS(1)
     } else if constexpr (Eng::kFast) {
-      stage_rows<C>(sm, pa, n, rs, ncols, in_rpb, a.in_bstride);
-      if (is_curl) stage_rows<C>(sm + n * C, pb, n, rs, ncols, in_rpb, a.in_bstride);
+      stage_rows<C>(sm, pa, n, rs, ncols, in_rpb, a.in_bstride, a.in_magic);
+      if (is_curl) stage_rows<C>(sm + n * C, pb, n, rs, ncols, in_rpb, a.in_bstride, a.in_magic);
       cp_async_wait_all();
       SRK_BAR();
       SRK_TS(1)
@@ -423,7 +440,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
       const int cr = pad_src(row, n, M);
       const bool ok = cr >= 0;
       const int r = ok ? cr : 0;
-      const unsigned off = row_off(r, rs, in_rpb, a.in_bstride) + (unsigned)col;
+      const unsigned off = row_off(r, rs, in_rpb, a.in_bstride, a.in_magic) + (unsigned)col;
       const cplx A = Eng::kFast ? sm[r * C + col] : pa[off];
       const cplx B = Eng::kFast ? sb_[r * C + col] : pb[off];
       const double ky = mode_full(r, n) * a.ck1;
@@ -448,14 +465,20 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
     if (use_tma) {
       tma_stage<C>(sm, &tm, wl, g, M, a.tma_rows, trpb, plane, -1, 0, &tbar);
       SRK_TS(1)
+      if (a.probe) {  // access-pattern ceiling of the pass (no transform): not a compute path
+        if (a.probe == 2)
+          for (int r = threadIdx.x / C; r < n; r += Eng::NT / C)
+            if ((int)(threadIdx.x % C) < ncols) oel(r, threadIdx.x % C) = cmk(0.0, 0.0);
+        return;
+      }
     } else if constexpr (Eng::kFast) {
-      stage_rows<C>(sm, inp, M, rs, ncols, in_rpb, a.in_bstride);
+      stage_rows<C>(sm, inp, M, rs, ncols, in_rpb, a.in_bstride, a.in_magic);
       cp_async_wait_all();
       SRK_BAR();
       SRK_TS(1)
     }
     auto ld = [&](int row, int col) -> cplx {
-      return Eng::kFast ? sm[row * C + col] : inp[row_off(row, rs, in_rpb, a.in_bstride) + (unsigned)col];
+      return Eng::kFast ? sm[row * C + col] : inp[row_off(row, rs, in_rpb, a.in_bstride, a.in_magic) + (unsigned)col];
     };
     auto st = [&](int row, int col, cplx v) {
       const int c = trunc_dst(row, n, M, zn);
@@ -903,10 +926,41 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
 // redone per stage and NCOL * M/R butterflies looped over the CTA (each
 // thread keeps ceil(NCOL*M/R / NT) butterflies live across the barrier).
 // ---------------------------------------------------------------------------
+// A storer with a member kFin consumes the last stage's butterflies whole
+// (fin(v, col, j): outputs v[q] = row j + q*Ls, still in registers) instead of
+// row by row through shared memory -- no store barrier, no extraction pass.
+template <class T, class = void>
+struct st_has_fin : std::false_type {};
+template <class T>
+struct st_has_fin<T, decltype(void(T::kFin))> : std::true_type {};
+
 template <int M, class L, int SIGN, int NCOL, int NT, int Ls, int R, int... Rest>
 struct LoopStageZ {
   template <class ST>
   __device__ __forceinline__ static void go(cplx* sm, const cplx* tw, ST& st) {
+    constexpr int STRIDE = M / R;
+    constexpr int TOT = NCOL * STRIDE;
+    constexpr int NB = (TOT + NT - 1) / NT;
+    constexpr bool LAST = (sizeof...(Rest) == 0);
+    if constexpr (LAST && st_has_fin<ST>::value) {
+      static_assert(NB == 1 && Ls == STRIDE && STRIDE == 32, "fused last stage: one warp per column");
+      const int u = threadIdx.x;
+      if (u < TOT) {  // warp-uniform (TOT is a multiple of 32)
+        const int col = u / STRIDE, j = u - col * STRIDE;
+        cplx v[R];
+        const int a0 = L::idx(j, col);
+#pragma unroll
+        for (int t = 0; t < R; ++t) v[t] = sm[a0 + t * (STRIDE / 8) * L::STEP8];
+        stage_twiddle_sq<M, R, SIGN>(v, tw, (unsigned)j * (unsigned)(M / (Ls * R)));
+        DFT<R, SIGN>::run(v);
+        st.template fin<R>(v, col, j);
+      }
+    } else {
+      go_rows(sm, tw, st);
+    }
+  }
+  template <class ST>
+  __device__ __forceinline__ static void go_rows(cplx* sm, const cplx* tw, ST& st) {
     constexpr int STRIDE = M / R;
     constexpr int TOT = NCOL * STRIDE;
     constexpr int NB = (TOT + NT - 1) / NT;
@@ -969,6 +1023,51 @@ struct LoopStageZ {
 // SM with independent phases instead of 2 CTAs (12 warps) -- at the price of
 // one extra 768-point forward transform per two pencils (P2 rides alone).
 // ---------------------------------------------------------------------------
+// Last-stage consumer of the one-pencil NS3 z-pass (see LoopStageZ / st_has_fin).
+// Column 0 = FFT(P0 + i P1): P0[k] = (Z[k] + conj Z[M-k]) / 2, P1[k] = (Z[k] -
+// conj Z[M-k]) / (2i); column 1 = FFT(P2) stored directly.  Butterfly j of the
+// last stage (radix R = M/32, Ls = 32) holds rows j + 32 q; rows k < K - 1 are
+// q < R/3, and row M - k = (32 - j) + 32 (R - 1 - q) is output R - 1 - q of
+// lane 32 - j (j = 0: output R - q of lane 0 itself).
+template <int M>
+struct ZFinNS3 {
+  static constexpr int kFin = 1;
+  cplx* o;  // out + pen * K
+  long long ss;
+  template <int R>
+  __device__ __forceinline__ void fin(cplx (&v)[R], int col, int j) const {
+    constexpr int K = M / 3 + 1, QK = R / 3;
+    static_assert(M == 32 * R && R % 3 == 0, "one warp per column, K - 1 = 32 R / 3 rows kept");
+    if (col == 0) {
+      const int src = (32 - j) & 31;
+#pragma unroll
+      for (int q = 0; q < QK; ++q) {
+        const cplx Zk = v[q];
+        cplx Zm;
+        Zm.x = __shfl_sync(0xffffffffu, v[R - 1 - q].x, src);
+        Zm.y = __shfl_sync(0xffffffffu, v[R - 1 - q].y, src);
+        if (j == 0) Zm = v[(R - q) % R];
+        const int k = j + 32 * q;
+        o[k] = cmk(0.5 * (Zk.x + Zm.x), 0.5 * (Zk.y - Zm.y));
+        o[ss + k] = cmk(0.5 * (Zk.y + Zm.y), -0.5 * (Zk.x - Zm.x));
+      }
+      if (j == 0) o[K - 1] = o[ss + K - 1] = cmk(0.0, 0.0);  // kz = n/2 zeroed (narrow)
+    } else {
+#pragma unroll
+      for (int q = 0; q < QK; ++q) {
+        const int k = j + 32 * q;
+        o[2 * ss + k] = (k == 0) ? cmk(v[q].x, 0.0) : v[q];
+      }
+      if (j == 0) o[2 * ss + K - 1] = cmk(0.0, 0.0);
+    }
+  }
+};
+template <int M, int... FR>
+struct ns3p_fused_last {
+  static constexpr int RL = (FR, ...);  // last radix
+  static constexpr bool value = (M == 32 * RL) && (RL % 3 == 0);
+};
+
 #define SRK_ZP1_MINB 5   // CTAs per SM the register budget targets (shared memory allows 5)
 #define SRK_ZB2P_MINB 3  // CTAs per SM of the 2D Boussinesq variant (M = 1536, 128 threads)
 // OP = ZOP_B2 (2D Boussinesq, v15): 2 inverse columns [u0 + i u1][w + i rho],
@@ -1086,6 +1185,17 @@ __global__ void __launch_bounds__(EngI::NT, (OP == ZOP_B2 ? SRK_ZB2P_MINB : (M <
   }
   SRK_BAR();
   SRK_TS(3)
+  // ---- NS3, last forward stage on one warp per column (M/R = 32): the stage's
+  // outputs stay in registers; the mirror rows M - k of the two-for-one
+  // separation sit in lane 32 - j of the same warp (lane 0: in its own
+  // butterfly) and come over by shuffle, P2 is stored as computed -- the f2 ->
+  // extraction exchange (~8% of the pass's shared-memory wavefronts), its
+  // barrier and the extraction loop are gone (same arithmetic, bitwise).
+  if constexpr (OP == ZOP_NS3 && ns3p_fused_last<M, FR...>::value) {
+    ZFinNS3<M> fin{a.out + (long long)pen * K, a.out_sig_stride};
+    LoopStageZ<M, L, -1, 2, NT, 4, FR...>::go(sm, twp, fin);
+    return;
+  }
   // ---- forward suffix (Ls = 4 ...) on the 2 packed columns ----
   {
     // only rows the extraction reads: column 0 (two-for-one) needs k < K-1 and its

@@ -216,11 +216,23 @@ bool encode_pass_map(CUtensorMap* tm, const cplx* base, const PassArgs& a, long 
   srk_encode_tiled_fn enc = encode_tiled();
   if (!enc) return false;
   const cuuint64_t ks = (cuuint64_t)(a.ngrp > 1 ? kst : a.kc) * 16;
+  if (rpb > 0 && a.ngrp == 1) {  // rank 4: {columns, row in block, block, plane} (a.tma = 2)
+    cuuint64_t dims[4] = {(cuuint64_t)(2 * a.kc), (cuuint64_t)rpb, (cuuint64_t)(rows / rpb), (cuuint64_t)a.planes};
+    cuuint64_t strides[3] = {(cuuint64_t)rs * 16, (cuuint64_t)bstride * 16, (cuuint64_t)pst * 16};
+    cuuint32_t boxd[4] = {(cuuint32_t)(2 * cols), (cuuint32_t)(box < rpb ? box : rpb),
+                          (cuuint32_t)(box < rpb ? 1 : box / rpb), 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)base, dims, strides, boxd, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, pr,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
   if (rpb > 0) {  // rank 5: {columns, column groups, row in block, block, plane}
     cuuint64_t dims[5] = {(cuuint64_t)(2 * a.kc), (cuuint64_t)a.ngrp, (cuuint64_t)rpb, (cuuint64_t)(rows / rpb),
                           (cuuint64_t)a.planes};
     cuuint64_t strides[4] = {ks, (cuuint64_t)rs * 16, (cuuint64_t)bstride * 16, (cuuint64_t)pst * 16};
-    cuuint32_t boxd[5] = {(cuuint32_t)(2 * cols), 1, (cuuint32_t)box, 1, 1};
+    // a box covers `box` rows: part of one block, or whole blocks (box a multiple of rpb)
+    cuuint32_t boxd[5] = {(cuuint32_t)(2 * cols), 1, (cuuint32_t)(box < rpb ? box : rpb),
+                          (cuuint32_t)(box < rpb ? 1 : box / rpb), 1};
     cuuint32_t es[5] = {1, 1, 1, 1, 1};
     return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void*)base, dims, strides, boxd, es,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, pr,
@@ -249,15 +261,24 @@ void setup_tma(int kind, int cols, PassArgs& a, CUtensorMap* tm) {
   if ((kind == KK_INV_KX || kind == KK_INV_KX_SLAB || kind == KK_INV_KX_PEER) && a.comp_stride != a.in_plane_stride)
     return;
   const int rows = fwd ? a.M : a.n;
-  const int rb = a.in_rpb > 0 ? a.in_rpb : rows;  // boxes must not straddle row blocks
+  const int rb = a.in_rpb > 0 ? a.in_rpb : rows;
   if (rows % rb) return;
-  const int nb = (rb + 255) / 256;
-  if (rb % nb) return;
-  const int box = rb / nb;
+  // rows per box (<= 256): a divisor of a row block, or -- small blocks (the
+  // y-blocked RHS intermediates) -- as many whole blocks as fit
+  int box;
+  if (a.in_rpb > 0 && rb <= 128) {
+    int k = 256 / rb;
+    while (k > 1 && (rows / rb) % k) --k;
+    box = k * rb;
+  } else {
+    const int nb = (rb + 255) / 256;
+    if (rb % nb) return;
+    box = rb / nb;
+  }
   if (!encode_pass_map(tm, a.in + a.in_k0, a, a.in_kst, a.in_rs, a.in_plane_stride, rows, box, cols, promo(),
                        a.in_rpb, a.in_bstride))
     return;
-  a.tma = 1;
+  a.tma = (a.in_rpb > 0 && a.ngrp == 1) ? 2 : 1;  // 2: blocked rows through the rank-4 map
   a.tma_rows = box;
 }
 
@@ -298,24 +319,36 @@ void normalise_cols(PassArgs& a, int cols) {
 // occupancy in launch_z.
 int zpass_prefetch_distance() { return 2 * srk_sm_count(); }
 
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
+}
+
 int launch_col(srk_plan* p, int kind, PassArgs a, cudaStream_t st) {
   const bool padded_kind = kind == KK_INV_P || kind == KK_FWD_P || kind == KK_INV_RHS || kind >= KK_INV_RHS_SLAB;
   if (padded_kind && 3 * a.n != 2 * a.M) return fail(SRK_ERR_INVALID, "padded pass needs M = 3n/2");
   KEntry e;
   int rc = get_entry(kind, a.M, e, a.gp);
   if (rc) return rc;
-  if ((rc = get_tw(p, a.M, &a.tw))) return rc;
-  if ((rc = ensure_smem(e))) return rc;
-  normalise_cols(a, e.cols);
-  const long long grid = (long long)a.planes * a.tpp;
-  if (grid <= 0) return SRK_OK;
   a.dbg = (p->dbg && p->last_launches == p->dbg_launch) ? p->dbg : nullptr;
+  if ((rc = get_tw(p, a.M, &a.tw))) return rc;
+  normalise_cols(a, e.cols);
+  auto magic = [](int rpb) { return rpb > 1 ? 0xFFFFFFFFu / (unsigned)rpb + 1u : 0u; };
+  a.in_magic = magic(a.in_rpb);
+  a.out_magic = magic(a.out_rpb);
+  const long long ntiles = (long long)a.planes * a.tpp;
+  if (ntiles <= 0) return SRK_OK;
+  if (ntiles > 0x7fffffffLL) return fail(SRK_ERR_INVALID, "strided pass: too many tiles");
   alignas(64) CUtensorMap tm;
   memset(&tm, 0, sizeof(tm));
   setup_tma(kind, e.cols, a, &tm);
+  const long long grid = ntiles;
   alignas(64) CUtensorMap tmo;
   memset(&tmo, 0, sizeof(tmo));
   setup_tma_out(kind, e.cols, a, &tmo);
+  if ((rc = ensure_smem(e))) return rc;
+  static const int probe_fwd = env_int("SRK_PROBE_FWD", 0);
+  a.probe = ((kind == KK_FWD_P || kind == KK_FWD_P_SLABO) && a.tma) ? probe_fwd : 0;
   void* args[] = {&a, &tm, &tmo};
   cudaError_t err = srk_launch(e.fn, dim3((unsigned)grid), dim3(e.nt), args, e.smem, st);
   if (err != cudaSuccess) return fail(SRK_ERR_CUDA, std::string("colpass launch: ") + cudaGetErrorString(err));
@@ -706,6 +739,17 @@ int comb_after(srk_plan* p, const CombSpec* cs, const cplx* f, cudaStream_t st) 
   return check_launch("k_combine");
 }
 
+// Rows per y block of the x-padded intermediates (0: plain order).  Unsplit 3D
+// fast plans whose plain x rows reach 1 MB; SRK_YB overrides (0 = off).
+int rhs_yblock(const srk_plan* p) {
+  static const int env_yb = env_int("SRK_YB", -1);
+  init_registry();
+  if (p->dims != 3 || p->nranks != 1 || !g_fast || !g_fast->count(p->m0) || !g_fast->count(p->m1)) return 0;
+  int yb = env_yb >= 0 ? env_yb : ((long long)p->n1 * p->K * 16 >= (1 << 20) ? 64 : 0);
+  if (yb <= 0 || yb >= p->n1 || p->n1 % yb) return 0;
+  return yb;
+}
+
 int rhs_impl(srk_plan* p, const void* y_, void* f_, double nu, double ri, double re_pr, void* stream,
              const CombSpec* cs) {
   if (!p) return fail(SRK_ERR_INVALID, "null plan");
@@ -729,6 +773,23 @@ int rhs_impl(srk_plan* p, const void* y_, void* f_, double nu, double ri, double
   a.comp_stride = p->modes;
   a.y0 = p->y0;
   a.n1g = p->n1g;
+  // The x-padded intermediates between the x and y passes (K1 -> K2, K4 -> K5) are
+  // kept y-blocked, [yb][signal][x][y in block][kz] with YB rows per block, when an x
+  // row of the plain [signal][x][y][kz] order is >= 1 MB: an x-pass tile then spans
+  // ~100 instead of 768 (512^3) 2 MB pages per signal -- the plain order thrashes the
+  // TLB (x-forward loads 3.9 -> 6.4 TB/s, K5 1.76 -> 1.41 ms at 512^3) -- while a
+  // y-pass tile crosses n1 / YB blocks.  Same bytes, a permutation of A / B.
+  const int YB = rhs_yblock(p);
+  const long long ybK = (long long)YB * p->K;
+  if (YB) {
+    a.kc = (int)ybK;
+    a.ngrp = p->n1 / YB;
+    a.in_kst = ybK;  // the state keeps its plain order: group g = columns [g YB K, (g + 1) YB K)
+    a.in_rs = a.row_stride;
+    a.out_kst = (long long)p->S1 * p->m0 * ybK;
+    a.out_rs = ybK;
+    a.out_plane_stride = (long long)p->m0 * ybK;
+  }
   if ((rc = launch_col(p, d == 3 ? KK_INV_KX : KK_INV_RHS, a, st))) return rc;
   const cplx* zin = p->A;
   cplx* zout = p->B;
@@ -740,7 +801,14 @@ int rhs_impl(srk_plan* p, const void* y_, void* f_, double nu, double ri, double
     b.nsig = p->S;
     b.ck1 = p->ck1;
     b.ck2 = p->ck2;
-    if ((rc = launch_col(p, KK_INV_CURLY, b, st))) return rc;
+    int k2 = KK_INV_CURLY;
+    if (YB) {  // y-blocked rows in
+      b.in_plane_stride = ybK;
+      b.in_rpb = YB;
+      b.in_bstride = (long long)p->S1 * p->m0 * ybK;
+      k2 = KK_INV_CURLY_SLAB;
+    }
+    if ((rc = launch_col(p, k2, b, st))) return rc;
     zin = p->B;
     zout = p->A;
   }
@@ -762,7 +830,14 @@ int rhs_impl(srk_plan* p, const void* y_, void* f_, double nu, double ri, double
     // K4: forward y + truncate
     PassArgs b = y_pass(p, p->A, p->B, p->So, p->m0, p->m1, p->n1, p->m1, p->n1);
     b.zero_nyq = 1;
-    if ((rc = launch_col(p, KK_FWD_P, b, st))) return rc;
+    int k4 = KK_FWD_P;
+    if (YB) {  // y-blocked rows out ([yb][s][x][yi][kz])
+      b.out_plane_stride = ybK;
+      b.out_rpb = YB;
+      b.out_bstride = (long long)p->So * p->m0 * ybK;
+      k4 = KK_FWD_P_SLABO;
+    }
+    if ((rc = launch_col(p, k4, b, st))) return rc;
     xin = p->B;
   }
   // K5: forward x + truncate + 1/1.5^d + Nyquist / DC-imag zeroing -> G
@@ -775,6 +850,15 @@ int rhs_impl(srk_plan* p, const void* y_, void* f_, double nu, double ri, double
     init_registry();
     auto it = g_fast->find(p->m0);
     if (it != g_fast->end() && it->second.e[KK_FWD_P2D].fn) k5 = KK_FWD_P2D;
+  }
+  if (YB) {  // K5 reads the y-blocked layout: column groups of YB*K columns, x rows YB*K apart
+    c5.kc = (int)ybK;
+    c5.ngrp = p->n1 / YB;
+    c5.in_kst = (long long)p->So * p->m0 * ybK;
+    c5.in_rs = ybK;
+    c5.in_plane_stride = (long long)p->m0 * ybK;
+    c5.out_kst = ybK;
+    c5.out_rs = c5.row_stride;
   }
   if ((rc = launch_col(p, k5, c5, st))) return rc;
   // K6: projection + viscous (+ Boussinesq terms)

@@ -7,6 +7,8 @@
 set -u
 OUT=gpurun_out/checks
 mkdir -p $OUT
+# the hazard-probe library is a build artefact (git-ignored): build it where it is missing
+[ -f _lib_chk/libsrk.so ] || make -C paper_1810_10197_b200/csrc checks -j16 > $OUT/build_chk.log 2>&1
 timeout 900 python tools/sanitize_cases.py --dump /tmp/srk_prod.npz > $OUT/prod.log 2>&1; echo "prod rc=$?" | tee -a $OUT/summary.txt
 SRK_LIB_PATH=$PWD/_lib_chk/libsrk.so timeout 1800 python tools/sanitize_cases.py --dump /tmp/srk_chk.npz > $OUT/chk.log 2>&1; echo "checks rc=$?" | tee -a $OUT/summary.txt
 python - <<'PY' | tee -a $OUT/summary.txt

@@ -19,4 +19,10 @@ timeout 1500 ncu --set full --metrics $M --clock-control none --import-source on
     -s 6 -c 6 -f -o /tmp/rhs512 python tools/rhs_timing.py --n 512 --reps 2 > $OUT/ncu.log 2>&1 && \
 python tools/ncu_kernels.py /tmp/rhs512.ncu-rep --n 512 > $OUT/ncu_kernels.out 2>&1 && \
 cp profiles/ncu_kernels.json $OUT/ncu_kernels.json && python tools/ncu_summary.py /tmp/rhs512.ncu-rep > $OUT/ncu_summary.txt 2>&1
+for k in k_zpass k_colpass; do
+  ncu -i /tmp/rhs512.ncu-rep --page source --csv --print-source sass -k regex:$k --launch-count 2 > $OUT/source_$k.csv 2>/dev/null
+done
+# launch list of the bench command itself (shares of the step; times under ncu are serialised / cold-cache)
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file $OUT/launches_bench512.csv \
+    python bench.py --steps 2 --warmup 1 --no-cpu > $OUT/ncu_launches.log 2>&1
 bash tools/check_build.sh > $OUT/checks.out 2>&1
