@@ -86,6 +86,10 @@ struct PassArgs {
   // (normalised by the host).  tpg = tiles per group, tpp = ngrp * tpg.
   int kc, ngrp, tpg, in_k0, out_k0, kz0;
   long long in_kst, out_kst;
+  // kc_out > kc (y passes over pitch-padded rows): the pass also stores the pad columns
+  // up to kc_out (zeros: their input is the TMA's out-of-bounds fill), so that a row's
+  // last 32 B sector is written whole.
+  int kc_out;
   long long in_rs, out_rs;  // row strides of input / output (0 -> row_stride)
   // PF_PEER (slab all-to-all fused into the pass): output row block b goes to
   // peer[b] (rank b's receive buffer at this rank's source block, UVA / CUDA IPC
@@ -127,6 +131,7 @@ __device__ __forceinline__ void stage_rows(cplx* dst, const cplx* __restrict__ s
   for (int i = threadIdx.x; i < tot; i += blockDim.x) {
     const int r = i / C, c = i - (i / C) * C;
     if (c < ncols) cp_async16(dst + i, src + row_off(r, rs, rpb, bstride, magic) + (unsigned)c);
+    else dst[i] = cmk(0.0, 0.0);  // pad / out-of-range columns (the TMA path zero-fills them too)
   }
 }
 
@@ -216,7 +221,8 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
   const int bid = blockIdx.x;
   int plane, g, wl;
   tile_of<KIND, C>(a, bid, plane, g, wl);
-  const int ncols = min(C, a.kc - wl);
+  const int ncols_in = min(C, a.kc - wl);  // data columns of the tile
+  const int ncols = a.kc_out > a.kc ? min(C, a.kc_out - wl) : ncols_in;  // + pad columns stored
   const long long w_in = (long long)g * a.in_kst + a.in_k0 + wl;    // memory column of the tile
   const long long w_out = (long long)g * a.out_kst + a.out_k0 + wl;
   const unsigned rs = (unsigned)a.in_rs;    // intra-plane offsets fit in 32 bits
@@ -289,7 +295,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
       tma_stage<C>(sm, &tm, wl, g, n, a.tma_rows, trpb, plane, -1, 0, &tbar);
       SRK_TS(1)
     } else if constexpr (Eng::kFast) {
-      stage_rows<C>(sm, inp, n, rs, ncols, in_rpb, a.in_bstride, a.in_magic);
+      stage_rows<C>(sm, inp, n, rs, ncols_in, in_rpb, a.in_bstride, a.in_magic);
       cp_async_wait_all();
       SRK_BAR();
       SRK_TS(1)
@@ -348,8 +354,8 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
     const double sc = a.scale;
     cplx* sb_ = sm + (is_curl ? n * C : 0);
     if constexpr (Eng::kFast) {
-      stage_rows<C>(sm, pa, n, rs, ncols, in_rpb, a.in_bstride, a.in_magic);
-      if (is_curl) stage_rows<C>(sm + n * C, pb, n, rs, ncols, in_rpb, a.in_bstride, a.in_magic);
+      stage_rows<C>(sm, pa, n, rs, ncols_in, in_rpb, a.in_bstride, a.in_magic);
+      if (is_curl) stage_rows<C>(sm + n * C, pb, n, rs, ncols_in, in_rpb, a.in_bstride, a.in_magic);
       cp_async_wait_all();
       SRK_BAR();
       SRK_TS(1)
@@ -384,8 +390,14 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
     if (use_tma) {  // host guarantees comp_stride == in_plane_stride
       tma_stage<C>(sm, &tm, wl, g, n, a.tma_rows, trpb, comp, -1, 0, &tbar);
       SRK_TS(1)
+      if (a.probe) {  // access-pattern ceiling (see PK_FWD)
+        if (a.probe == 2)
+          for (int r = threadIdx.x / C; r < M; r += Eng::NT / C)
+            if ((int)(threadIdx.x % C) < ncols) oel(r, threadIdx.x % C) = cmk(0.0, 0.0);
+        return;
+      }
     } else if constexpr (Eng::kFast) {
-      stage_rows<C>(sm, pa, n, rs, ncols, in_rpb, a.in_bstride, a.in_magic);
+      stage_rows<C>(sm, pa, n, rs, ncols_in, in_rpb, a.in_bstride, a.in_magic);
       cp_async_wait_all();
       SRK_BAR();
       SRK_TS(1)
@@ -427,11 +439,25 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
     const double kz = (double)(a.kz0 + wl + mycol) * a.ck2;  // global kz of the column
     cplx* sb_ = sm + (is_curl ? n * C : 0);
     if (use_tma) {
+      if (a.probe == 5) {  // probe: stores only
+        SRK_BAR();
+      } else if (a.probe >= 3)  // probe: one staged plane per curl signal (5 distinct planes, 6 tile loads)
+        tma_stage<C>(sm, &tm, wl, g, n, a.tma_rows, trpb, (s == 4 ? cb : ca) * X + x, -1, n * C, &tbar);
+      else
       tma_stage<C>(sm, &tm, wl, g, n, a.tma_rows, trpb, ca * X + x, is_curl ? cb * X + x : -1, n * C, &tbar);
       SRK_TS(1)
+      if (a.probe) {  // access-pattern ceiling (see PK_FWD): the staged rows go out as they are
+        if (a.probe == 2 || a.probe >= 4) {
+          if (use_tmo) flush_out();
+          else
+            for (int r = threadIdx.x / C; r < M; r += Eng::NT / C)
+              if ((int)(threadIdx.x % C) < ncols) oel(r, threadIdx.x % C) = cmk(0.0, 0.0);
+        }
+        return;
+      }
     } else if constexpr (Eng::kFast) {
-      stage_rows<C>(sm, pa, n, rs, ncols, in_rpb, a.in_bstride, a.in_magic);
-      if (is_curl) stage_rows<C>(sm + n * C, pb, n, rs, ncols, in_rpb, a.in_bstride, a.in_magic);
+      stage_rows<C>(sm, pa, n, rs, ncols_in, in_rpb, a.in_bstride, a.in_magic);
+      if (is_curl) stage_rows<C>(sm + n * C, pb, n, rs, ncols_in, in_rpb, a.in_bstride, a.in_magic);
       cp_async_wait_all();
       SRK_BAR();
       SRK_TS(1)
@@ -472,7 +498,7 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
         return;
       }
     } else if constexpr (Eng::kFast) {
-      stage_rows<C>(sm, inp, M, rs, ncols, in_rpb, a.in_bstride, a.in_magic);
+      stage_rows<C>(sm, inp, M, rs, ncols_in, in_rpb, a.in_bstride, a.in_magic);
       cp_async_wait_all();
       SRK_BAR();
       SRK_TS(1)
@@ -512,6 +538,8 @@ struct ZArgs {
   int M;  // padded z length (real)
   int n;  // coarse z length
   int K;  // stored modes n/2+1
+  int Kp; // pencil pitch of the spectral buffers in complex elements (0: K); the RHS pads it so
+          // that every pencil row starts on a 32 B sector (rhs_impl)
   int P;  // pencils
   int S;  // input real signals per pencil
   int So; // output real signals per pencil
@@ -577,6 +605,7 @@ __global__ void __launch_bounds__(Eng::NT, (PPC == 1 && Eng::NT <= 128 ? 3 : (En
   constexpr bool kCT = Eng::kFast && OP >= ZOP_NS3;
   const int M = kCT ? Eng::M : a.M;
   const int K = kCT ? Eng::M / 3 + 1 : a.K;
+  const int KP = a.Kp ? a.Kp : K;  // pencil pitch in the spectral buffers
   if constexpr (OP != ZOP_R2C) {
     // ---- stage the 2*S input rows (K contiguous modes each) in smem.  Fast
     // path: one elected thread issues 1D TMA bulk copies (cp.async.bulk) that
@@ -598,7 +627,7 @@ __global__ void __launch_bounds__(Eng::NT, (PPC == 1 && Eng::NT <= 128 ? 3 : (En
         for (int g = 0; g < PPC * S; ++g) {
           const int pp = g / S, s = g - pp * S, pen = p0 + pp;
           if (pen < a.P)
-            bulk_g2s(stg + g * K, a.in + s * a.in_sig_stride + (long long)pen * K, (unsigned)(K * 16), &mbar);
+            bulk_g2s(stg + g * K, a.in + s * a.in_sig_stride + (long long)pen * KP, (unsigned)(K * 16), &mbar);
         }
       }
       // rows of a missing second pencil (odd P) are zero
@@ -609,7 +638,7 @@ __global__ void __launch_bounds__(Eng::NT, (PPC == 1 && Eng::NT <= 128 ? 3 : (En
     } else {
       for (int g = 0; g < PPC * S; ++g) {
         const int pp = g / S, s = g - pp * S, pen = p0 + pp;
-        const cplx* __restrict__ src = a.in + s * a.in_sig_stride + (long long)pen * K;
+        const cplx* __restrict__ src = a.in + s * a.in_sig_stride + (long long)pen * KP;
         for (int k = threadIdx.x; k < K; k += blockDim.x) stg[g * K + k] = (pen < a.P) ? src[k] : cmk(0.0, 0.0);
       }
       SRK_BAR();
@@ -708,7 +737,7 @@ __global__ void __launch_bounds__(Eng::NT, (PPC == 1 && Eng::NT <= 128 ? 3 : (En
       const int g = 2 * c + h;
       if (g >= PPC * So) break;
       const int pp = g / So, s = g - pp * So, pen = p0 + pp;
-      if (pen < a.P) a.out[s * a.out_sig_stride + (long long)pen * K + k] = h ? B : A;
+      if (pen < a.P) a.out[s * a.out_sig_stride + (long long)pen * KP + k] = h ? B : A;
     }
   }
 }
@@ -777,6 +806,7 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
   srk_poison_smem(smraw);
   tw_fill<M>(smraw, a.tw);  // cp.async; waited for before the staging barrier
   constexpr int S = 6, So = 3, NT = M / 4, K = M / 3 + 1, Q = M / 4;
+  const int KP = a.Kp ? a.Kp : K;  // pencil pitch in the spectral buffers
   static_assert(EngI::NT == NT, "inverse prefix must use M/4 threads");
   const int p0 = 2 * blockIdx.x;
   const int tid = threadIdx.x;
@@ -797,14 +827,14 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
     mbar_expect_tx(&mbar, bytes);
     for (int g = 0; g < 2 * S; ++g) {
       const int pp = g / S, s = g - pp * S, pen = p0 + pp;
-      if (pen < a.P) bulk_g2s(stg + g * K, a.in + s * a.in_sig_stride + (long long)pen * K, (unsigned)(K * 16), &mbar);
+      if (pen < a.P) bulk_g2s(stg + g * K, a.in + s * a.in_sig_stride + (long long)pen * KP, (unsigned)(K * 16), &mbar);
     }
     // warm L2 with the rows of the pencil pair about one wave of CTAs ahead
     if (a.pf_dist) {
       const int q0 = p0 + 2 * a.pf_dist;
       for (int g = 0; g < 2 * S; ++g) {
         const int pp = g / S, s = g - pp * S, pen = q0 + pp;
-        if (pen < a.P) bulk_prefetch_l2(a.in + s * a.in_sig_stride + (long long)pen * K, (unsigned)(K * 16));
+        if (pen < a.P) bulk_prefetch_l2(a.in + s * a.in_sig_stride + (long long)pen * KP, (unsigned)(K * 16));
       }
     }
   }
@@ -909,7 +939,7 @@ __global__ void __launch_bounds__(M / 4, (M / 4 <= 224 ? 2 : 1)) k_zpass_ns3f(co
   if (tid == 0) {
     for (int g = 0; g < 2 * So; ++g) {
       const int pp = g / So, s = g - pp * So, pen = p0 + pp;
-      if (pen < a.P) bulk_s2g(a.out + s * a.out_sig_stride + (long long)pen * K, ost + g * K, (unsigned)(K * 16));
+      if (pen < a.P) bulk_s2g(a.out + s * a.out_sig_stride + (long long)pen * KP, ost + g * K, (unsigned)(K * 16));
     }
     bulk_commit_and_wait_read();
   }
@@ -1032,8 +1062,9 @@ struct LoopStageZ {
 template <int M>
 struct ZFinNS3 {
   static constexpr int kFin = 1;
-  cplx* o;  // out + pen * K
+  cplx* o;  // out + pen * pitch
   long long ss;
+  bool pad;  // pitch > K
   template <int R>
   __device__ __forceinline__ void fin(cplx (&v)[R], int col, int j) const {
     constexpr int K = M / 3 + 1, QK = R / 3;
@@ -1051,14 +1082,20 @@ struct ZFinNS3 {
         o[k] = cmk(0.5 * (Zk.x + Zm.x), 0.5 * (Zk.y - Zm.y));
         o[ss + k] = cmk(0.5 * (Zk.y + Zm.y), -0.5 * (Zk.x - Zm.x));
       }
-      if (j == 0) o[K - 1] = o[ss + K - 1] = cmk(0.0, 0.0);  // kz = n/2 zeroed (narrow)
+      if (j == 0) {
+        o[K - 1] = o[ss + K - 1] = cmk(0.0, 0.0);  // kz = n/2 zeroed (narrow)
+        if (pad) o[K] = o[ss + K] = cmk(0.0, 0.0);   // pad column: the row's last 32 B sector is written whole
+      }
     } else {
 #pragma unroll
       for (int q = 0; q < QK; ++q) {
         const int k = j + 32 * q;
         o[2 * ss + k] = (k == 0) ? cmk(v[q].x, 0.0) : v[q];
       }
-      if (j == 0) o[2 * ss + K - 1] = cmk(0.0, 0.0);
+      if (j == 0) {
+        o[2 * ss + K - 1] = cmk(0.0, 0.0);
+        if (pad) o[2 * ss + K] = cmk(0.0, 0.0);
+      }
     }
   }
 };
@@ -1086,6 +1123,7 @@ __global__ void __launch_bounds__(EngI::NT, (OP == ZOP_B2 ? SRK_ZB2P_MINB : (M <
   static_assert(OP == ZOP_NS3 || OP == ZOP_B2, "NS3 or 2D Boussinesq");
   // NT = M/8 (E = 24: two fused-middle rows per thread); B2: M/12 (three rows)
   constexpr int S = OP == ZOP_B2 ? 2 : 3, NT = EngI::NT, K = M / 3 + 1, Q = M / 4, RPT = Q / NT;
+  const int KP = a.Kp ? a.Kp : K;  // pencil pitch in the spectral buffers
   static_assert(OP == ZOP_B2 ? NT == M / 12 : NT == M / 8, "inverse prefix thread count");
   static_assert(L::C == S, "one tile column per inverse complex signal");
   static_assert(Q % NT == 0, "whole fused-middle rows per thread");
@@ -1105,12 +1143,12 @@ __global__ void __launch_bounds__(EngI::NT, (OP == ZOP_B2 ? SRK_ZB2P_MINB : (M <
   if (tid == 0) {
     mbar_expect_tx(&mbar, (unsigned)(2 * S * K * 16));
     for (int s = 0; s < 2 * S; ++s)
-      bulk_g2s(stg + s * K, a.in + s * a.in_sig_stride + (long long)pen * K, (unsigned)(K * 16), &mbar);
+      bulk_g2s(stg + s * K, a.in + s * a.in_sig_stride + (long long)pen * KP, (unsigned)(K * 16), &mbar);
     if (a.pf_dist) {
       const int q0 = pen + a.pf_dist;
       if (q0 < a.P)
         for (int s = 0; s < 2 * S; ++s)
-          bulk_prefetch_l2(a.in + s * a.in_sig_stride + (long long)q0 * K, (unsigned)(K * 16));
+          bulk_prefetch_l2(a.in + s * a.in_sig_stride + (long long)q0 * KP, (unsigned)(K * 16));
     }
   }
   // every thread waits on the mbarrier itself (the TMA rows are then visible to
@@ -1192,7 +1230,7 @@ __global__ void __launch_bounds__(EngI::NT, (OP == ZOP_B2 ? SRK_ZB2P_MINB : (M <
   // extraction exchange (~8% of the pass's shared-memory wavefronts), its
   // barrier and the extraction loop are gone (same arithmetic, bitwise).
   if constexpr (OP == ZOP_NS3 && ns3p_fused_last<M, FR...>::value) {
-    ZFinNS3<M> fin{a.out + (long long)pen * K, a.out_sig_stride};
+    ZFinNS3<M> fin{a.out + (long long)pen * KP, a.out_sig_stride, KP > K};
     LoopStageZ<M, L, -1, 2, NT, 4, FR...>::go(sm, twp, fin);
     return;
   }
@@ -1214,7 +1252,7 @@ __global__ void __launch_bounds__(EngI::NT, (OP == ZOP_B2 ? SRK_ZB2P_MINB : (M <
     const cplx Zk = live ? sm[L::idx(k, 0)] : cmk(0.0, 0.0);
     const cplx Zm = live ? sm[L::idx(k == 0 ? 0 : M - k, 0)] : cmk(0.0, 0.0);
     const cplx P2 = live ? sm[L::idx(k, 1)] : cmk(0.0, 0.0);
-    cplx* o = a.out + (long long)pen * K + k;
+    cplx* o = a.out + (long long)pen * KP + k;
     o[0] = cmk(0.5 * (Zk.x + Zm.x), 0.5 * (Zk.y - Zm.y));
     o[a.out_sig_stride] = cmk(0.5 * (Zk.y + Zm.y), -0.5 * (Zk.x - Zm.x));
     if constexpr (OP == ZOP_B2) {  // column 1 = [P2 + i P3]: two-for-one as well

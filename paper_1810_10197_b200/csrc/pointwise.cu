@@ -173,8 +173,23 @@ __global__ void __launch_bounds__(proj_chunk<DIMS, DENS, NTC, DIAG>()) k_project
     const unsigned cnt = (unsigned)min((long long)CH, n - i0);
     cplx* st = psm + b * NS * CH;
     mbar_expect_tx(&mb[b], cnt * 16u * NS);
+    if (a.Gp > a.g.K) {
+      // G rows have a padded pitch: the chunk's modes [i0, i0 + cnt) are row segments of G
+      const unsigned K = (unsigned)a.g.K, Kp = (unsigned)a.Gp;
+      const long long nG = n / K * Kp;  // modes per component at the padded pitch
+      unsigned done = 0;
+      while (done < cnt) {
+        const unsigned i = (unsigned)i0 + done, r = i / K, c = i - r * K;
+        const unsigned len = min(cnt - done, K - c);
 #pragma unroll
-    for (int j = 0; j < NG; ++j) bulk_g2s(st + j * CH, a.G + j * n + i0, cnt * 16u, &mb[b]);
+        for (int j = 0; j < NG; ++j)
+          bulk_g2s(st + j * CH + done, a.G + j * nG + (long long)r * Kp + c, len * 16u, &mb[b]);
+        done += len;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < NG; ++j) bulk_g2s(st + j * CH, a.G + j * n + i0, cnt * 16u, &mb[b]);
+    }
 #pragma unroll
     for (int j = 0; j < NY; ++j) bulk_g2s(st + (NG + j) * CH, a.y + j * n + i0, cnt * 16u, &mb[b]);
     if constexpr (NTC >= 0 && !DIAG) {

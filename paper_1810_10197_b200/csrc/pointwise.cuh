@@ -18,6 +18,8 @@ struct GeomArgs {
 struct ProjArgs {
   GeomArgs g;
   const cplx* G;  // narrow output: [u x w (d), (rho u)(d) if density]
+  int Gp;         // pitch of G's kz rows in complex elements (0: g.K, the state's): the RHS pads
+                  // its intermediates to whole 32 B sectors per row (rhs_pitch)
   const cplx* y;  // state [u (d), rho]
   cplx* f;
   long long modes;  // n0*n1*K

@@ -179,13 +179,46 @@ int get_tw(srk_plan* p, int M, const cplx** out) {
   return SRK_OK;
 }
 
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
+}
+
+// Layout of the RHS intermediates of unsplit 3D fast plans (rhs_impl):
+//  * pencil pitch Kp = K rounded up to 4 complex: K = n2/2 + 1 is odd, so with pitch K
+//    every other row of a y pass starts 16 B into a 32 B sector and its 64 B tile pieces
+//    are partial-sector writes (K2's stores ran at 3.1 TB/s; 7.7 TB/s with an even pitch);
+//  * the x-padded buffers (K1 -> K2, K4 -> K5) y-blocked, [yb][signal][x][y in block][kz],
+//    when a plain x row reaches 1 MB: an x-pass tile then spans ~100 instead of m0 2 MB
+//    pages per signal (the plain order thrashes the TLB).
+// SRK_KPAD=0 / SRK_YB=0 switch them off (A/B timing); both 0 for every other plan.
+bool rhs_fast3d(const srk_plan* p) {
+  init_registry();
+  return p->dims == 3 && p->nranks == 1 && p->modes < (1LL << 32) && g_fast->count(p->m0) && g_fast->count(p->m1) &&
+         g_fast->count(p->m2);
+}
+int rhs_pitch(const srk_plan* p) {
+  static const int env_kpad = env_int("SRK_KPAD", 1);
+  return (env_kpad && rhs_fast3d(p)) ? ((p->K + 3) & ~3) : p->K;
+}
+int rhs_yblock(const srk_plan* p) {
+  static const int env_yb = env_int("SRK_YB", -1);
+  if (!rhs_fast3d(p)) return 0;
+  int yb = env_yb >= 0 ? env_yb : ((long long)p->n1 * p->K * 16 >= (1 << 20) ? 64 : 0);
+  if (yb <= 0 || yb >= p->n1 || p->n1 % yb) return 0;
+  return yb;
+}
+
 int need_ws(srk_plan* p) {
   if (!p->A) return fail(SRK_ERR_WORKSPACE, "plan has no workspace bound (srk_plan_set_workspace)");
   return SRK_OK;
 }
 
 // ---- strided pass launch -------------------------------------------------
-int curly_xblk(int X) { return X % 2 == 0 ? 2 : 1; }
+int curly_xblk(int X) {
+  static const int xb = env_int("SRK_XBLK", 2);
+  return (xb > 0 && X % xb == 0) ? xb : 1;
+}
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
 typedef CUresult (*srk_encode_tiled_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -210,14 +243,16 @@ CUtensorMapL2promotion promo() { return CU_TENSOR_MAP_L2_PROMOTION_L2_256B; }
 // rows, planes} based at the chunk's first column, box {2*C, 1, rows/nb <= 256,
 // 1}.  Leaves a.tma = 0 when TMA does not apply (generic lengths, blocked slab
 // rows, 2D curl kinds, box constraints).
+// wcols: columns the map covers per group (a.kc, or the padded store width).
 bool encode_pass_map(CUtensorMap* tm, const cplx* base, const PassArgs& a, long long kst, long long rs,
                      long long pst, int rows, int box, int cols, CUtensorMapL2promotion pr, int rpb = 0,
-                     long long bstride = 0) {
+                     long long bstride = 0, int wcols = 0) {
   srk_encode_tiled_fn enc = encode_tiled();
   if (!enc) return false;
+  if (wcols <= 0) wcols = a.kc;
   const cuuint64_t ks = (cuuint64_t)(a.ngrp > 1 ? kst : a.kc) * 16;
   if (rpb > 0 && a.ngrp == 1) {  // rank 4: {columns, row in block, block, plane} (a.tma = 2)
-    cuuint64_t dims[4] = {(cuuint64_t)(2 * a.kc), (cuuint64_t)rpb, (cuuint64_t)(rows / rpb), (cuuint64_t)a.planes};
+    cuuint64_t dims[4] = {(cuuint64_t)(2 * wcols), (cuuint64_t)rpb, (cuuint64_t)(rows / rpb), (cuuint64_t)a.planes};
     cuuint64_t strides[3] = {(cuuint64_t)rs * 16, (cuuint64_t)bstride * 16, (cuuint64_t)pst * 16};
     cuuint32_t boxd[4] = {(cuuint32_t)(2 * cols), (cuuint32_t)(box < rpb ? box : rpb),
                           (cuuint32_t)(box < rpb ? 1 : box / rpb), 1};
@@ -227,7 +262,7 @@ bool encode_pass_map(CUtensorMap* tm, const cplx* base, const PassArgs& a, long 
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   }
   if (rpb > 0) {  // rank 5: {columns, column groups, row in block, block, plane}
-    cuuint64_t dims[5] = {(cuuint64_t)(2 * a.kc), (cuuint64_t)a.ngrp, (cuuint64_t)rpb, (cuuint64_t)(rows / rpb),
+    cuuint64_t dims[5] = {(cuuint64_t)(2 * wcols), (cuuint64_t)a.ngrp, (cuuint64_t)rpb, (cuuint64_t)(rows / rpb),
                           (cuuint64_t)a.planes};
     cuuint64_t strides[4] = {ks, (cuuint64_t)rs * 16, (cuuint64_t)bstride * 16, (cuuint64_t)pst * 16};
     // a box covers `box` rows: part of one block, or whole blocks (box a multiple of rpb)
@@ -239,7 +274,7 @@ bool encode_pass_map(CUtensorMap* tm, const cplx* base, const PassArgs& a, long 
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   }
   // rank 4: {columns, column groups, rows, plane}
-  cuuint64_t dims[4] = {(cuuint64_t)(2 * a.kc), (cuuint64_t)a.ngrp, (cuuint64_t)rows, (cuuint64_t)a.planes};
+  cuuint64_t dims[4] = {(cuuint64_t)(2 * wcols), (cuuint64_t)a.ngrp, (cuuint64_t)rows, (cuuint64_t)a.planes};
   cuuint64_t strides[3] = {ks, (cuuint64_t)rs * 16, (cuuint64_t)pst * 16};
   cuuint32_t boxd[4] = {(cuuint32_t)(2 * cols), 1, (cuuint32_t)box, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
@@ -287,14 +322,15 @@ void setup_tma(int kind, int cols, PassArgs& a, CUtensorMap* tm) {
 void setup_tma_out(int kind, int cols, PassArgs& a, CUtensorMap* tm) {
   a.tma_out = 0;
   const bool inv = kind == KK_INV_CURLY || kind == KK_INV_CURLY_SLAB;  // see kTMAO in k_colpass
-  if (!inv || a.out_rpb != 0 || !g_fast->count(a.M)) return;
+  static const int no_tmao = env_int("SRK_NO_TMAO", 0);
+  if (!inv || a.out_rpb != 0 || !g_fast->count(a.M) || no_tmao) return;
   const int nb = (a.M + 255) / 256;
   if (a.M % nb) return;
   const int box = a.M / nb;
   // the map ends at the chunk's last column: partial tiles are clipped, so a
   // chunk never writes its neighbour's columns
   if (!encode_pass_map(tm, a.out + a.out_k0, a, a.out_kst, a.out_rs, a.out_plane_stride, a.M, box, cols,
-                       CU_TENSOR_MAP_L2_PROMOTION_NONE))
+                       CU_TENSOR_MAP_L2_PROMOTION_NONE, 0, 0, a.kc_out > a.kc ? a.kc_out : 0))
     return;
   a.tma_out = 1;
   a.tmo_rows = box;
@@ -319,11 +355,6 @@ void normalise_cols(PassArgs& a, int cols) {
 // occupancy in launch_z.
 int zpass_prefetch_distance() { return 2 * srk_sm_count(); }
 
-int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return (v && *v) ? atoi(v) : dflt;
-}
-
 int launch_col(srk_plan* p, int kind, PassArgs a, cudaStream_t st) {
   const bool padded_kind = kind == KK_INV_P || kind == KK_FWD_P || kind == KK_INV_RHS || kind >= KK_INV_RHS_SLAB;
   if (padded_kind && 3 * a.n != 2 * a.M) return fail(SRK_ERR_INVALID, "padded pass needs M = 3n/2");
@@ -347,8 +378,12 @@ int launch_col(srk_plan* p, int kind, PassArgs a, cudaStream_t st) {
   memset(&tmo, 0, sizeof(tmo));
   setup_tma_out(kind, e.cols, a, &tmo);
   if ((rc = ensure_smem(e))) return rc;
-  static const int probe_fwd = env_int("SRK_PROBE_FWD", 0);
-  a.probe = ((kind == KK_FWD_P || kind == KK_FWD_P_SLABO) && a.tma) ? probe_fwd : 0;
+  // access-pattern probes (measurement only, tools/pass_probe.sh): 1 = stage the tile and
+  // return, 2 = also store in the output pattern, no transform
+  static const int probe_fwd = env_int("SRK_PROBE_FWD", 0), probe_inv = env_int("SRK_PROBE_INV", 0);
+  a.probe = 0;
+  if (a.tma && (kind == KK_FWD_P || kind == KK_FWD_P_SLABO)) a.probe = probe_fwd;
+  if (a.tma && (kind == KK_INV_KX || kind == KK_INV_CURLY || kind == KK_INV_CURLY_SLAB)) a.probe = probe_inv;
   void* args[] = {&a, &tm, &tmo};
   cudaError_t err = srk_launch(e.fn, dim3((unsigned)grid), dim3(e.nt), args, e.smem, st);
   if (err != cudaSuccess) return fail(SRK_ERR_CUDA, std::string("colpass launch: ") + cudaGetErrorString(err));
@@ -583,11 +618,12 @@ int srk_plan_create(srk_plan** out, int dims, const int64_t* shape, const double
   auto upA = [&](long long v) { A = std::max(A, v); };
   auto upB = [&](long long v) { B = std::max(B, v); };
   if (dims == 3) {
-    upA(p->S1 * m0 * n1 * K);  // K1 out
-    upB(p->S * m0 * m1 * K);   // K2 out
-    upA(p->So * m0 * m1 * K);  // K3 out
-    upB(p->So * m0 * n1 * K);  // K4 out
-    upA(p->So * n0 * n1 * K);  // K5 out (G)
+    const long long Kp = rhs_pitch(p);  // padded pencil pitch of the RHS intermediates
+    upA(p->S1 * m0 * n1 * K);   // K1 out
+    upB(p->S * m0 * m1 * Kp);   // K2 out
+    upA(p->So * m0 * m1 * Kp);  // K3 out
+    upB(p->So * m0 * n1 * Kp);  // K4 out
+    upA(p->So * n0 * n1 * Kp);  // K5 out (G)
     upA(c * m0 * n1 * K);
     upB(c * m0 * m1 * K);
     upA(c * m0 * m1 * K);
@@ -739,17 +775,6 @@ int comb_after(srk_plan* p, const CombSpec* cs, const cplx* f, cudaStream_t st) 
   return check_launch("k_combine");
 }
 
-// Rows per y block of the x-padded intermediates (0: plain order).  Unsplit 3D
-// fast plans whose plain x rows reach 1 MB; SRK_YB overrides (0 = off).
-int rhs_yblock(const srk_plan* p) {
-  static const int env_yb = env_int("SRK_YB", -1);
-  init_registry();
-  if (p->dims != 3 || p->nranks != 1 || !g_fast || !g_fast->count(p->m0) || !g_fast->count(p->m1)) return 0;
-  int yb = env_yb >= 0 ? env_yb : ((long long)p->n1 * p->K * 16 >= (1 << 20) ? 64 : 0);
-  if (yb <= 0 || yb >= p->n1 || p->n1 % yb) return 0;
-  return yb;
-}
-
 int rhs_impl(srk_plan* p, const void* y_, void* f_, double nu, double ri, double re_pr, void* stream,
              const CombSpec* cs) {
   if (!p) return fail(SRK_ERR_INVALID, "null plan");
@@ -773,22 +798,25 @@ int rhs_impl(srk_plan* p, const void* y_, void* f_, double nu, double ri, double
   a.comp_stride = p->modes;
   a.y0 = p->y0;
   a.n1g = p->n1g;
-  // The x-padded intermediates between the x and y passes (K1 -> K2, K4 -> K5) are
-  // kept y-blocked, [yb][signal][x][y in block][kz] with YB rows per block, when an x
-  // row of the plain [signal][x][y][kz] order is >= 1 MB: an x-pass tile then spans
-  // ~100 instead of 768 (512^3) 2 MB pages per signal -- the plain order thrashes the
-  // TLB (x-forward loads 3.9 -> 6.4 TB/s, K5 1.76 -> 1.41 ms at 512^3) -- while a
-  // y-pass tile crosses n1 / YB blocks.  Same bytes, a permutation of A / B.
-  const int YB = rhs_yblock(p);
-  const long long ybK = (long long)YB * p->K;
-  if (YB) {
-    a.kc = (int)ybK;
+  // layout of the intermediates (rhs_pitch / rhs_yblock):
+  //   X1 (K1 -> K2)           [yb][s][x][yi][kz]   pitch K (K1's flattened (y, kz) tiles stay
+  //                                                64 B-aligned on the state and on X1)
+  //   K2 -> K3 -> K4          [s][x][y][kz]        pitch Kp
+  //   X2 (K4 -> K5)           [yb][s][x][yi][kz]   pitch Kp
+  //   G  (K5 -> K6)           [s][x][y][kz]        pitch Kp
+  const int Kp = rhs_pitch(p), YB = rhs_yblock(p);
+  const bool lay = Kp != p->K || YB > 0;
+  const int YBe = YB ? YB : p->n1;
+  const long long yb1 = (long long)YBe * p->K;  // x-row stride of X1
+  const long long yb2 = (long long)YBe * Kp;    // x-row stride of X2
+  if (YB) {  // K1: column groups = y blocks of flattened (y, kz) columns
+    a.kc = (int)yb1;
     a.ngrp = p->n1 / YB;
-    a.in_kst = ybK;  // the state keeps its plain order: group g = columns [g YB K, (g + 1) YB K)
+    a.in_kst = yb1;  // the state keeps its plain order
     a.in_rs = a.row_stride;
-    a.out_kst = (long long)p->S1 * p->m0 * ybK;
-    a.out_rs = ybK;
-    a.out_plane_stride = (long long)p->m0 * ybK;
+    a.out_kst = (long long)p->S1 * p->m0 * yb1;
+    a.out_rs = yb1;
+    a.out_plane_stride = (long long)p->m0 * yb1;
   }
   if ((rc = launch_col(p, d == 3 ? KK_INV_KX : KK_INV_RHS, a, st))) return rc;
   const cplx* zin = p->A;
@@ -802,11 +830,16 @@ int rhs_impl(srk_plan* p, const void* y_, void* f_, double nu, double ri, double
     b.ck1 = p->ck1;
     b.ck2 = p->ck2;
     int k2 = KK_INV_CURLY;
-    if (YB) {  // y-blocked rows in
-      b.in_plane_stride = ybK;
-      b.in_rpb = YB;
-      b.in_bstride = (long long)p->S1 * p->m0 * ybK;
-      k2 = KK_INV_CURLY_SLAB;
+    if (lay) {
+      b.out_rs = Kp;
+      b.kc_out = Kp;
+      b.out_plane_stride = (long long)p->m1 * Kp;
+      if (YB) {  // y-blocked rows in
+        b.in_plane_stride = yb1;
+        b.in_rpb = YB;
+        b.in_bstride = (long long)p->S1 * p->m0 * yb1;
+        k2 = KK_INV_CURLY_SLAB;
+      }
     }
     if ((rc = launch_col(p, k2, b, st))) return rc;
     zin = p->B;
@@ -817,8 +850,9 @@ int rhs_impl(srk_plan* p, const void* y_, void* f_, double nu, double ri, double
   ZArgs z = z_args(p, p->m2, p->n2, P);
   z.in = zin;
   z.out = zout;
-  z.in_sig_stride = (long long)P * p->K;
-  z.out_sig_stride = (long long)P * p->K;
+  z.Kp = lay ? Kp : 0;
+  z.in_sig_stride = (long long)P * (lay ? Kp : p->K);
+  z.out_sig_stride = (long long)P * (lay ? Kp : p->K);
   z.zero_nyq = 1;
   z.dbg = (p->dbg && p->last_launches == p->dbg_launch) ? p->dbg : nullptr;
   z.pf_dist = zpass_prefetch_distance();
@@ -831,11 +865,16 @@ int rhs_impl(srk_plan* p, const void* y_, void* f_, double nu, double ri, double
     PassArgs b = y_pass(p, p->A, p->B, p->So, p->m0, p->m1, p->n1, p->m1, p->n1);
     b.zero_nyq = 1;
     int k4 = KK_FWD_P;
-    if (YB) {  // y-blocked rows out ([yb][s][x][yi][kz])
-      b.out_plane_stride = ybK;
-      b.out_rpb = YB;
-      b.out_bstride = (long long)p->So * p->m0 * ybK;
-      k4 = KK_FWD_P_SLABO;
+    if (lay) {
+      b.in_rs = b.out_rs = Kp;
+      b.kc_out = Kp;
+      b.in_plane_stride = (long long)p->m1 * Kp;
+      b.out_plane_stride = yb2;
+      if (YB) {  // y-blocked rows out
+        b.out_rpb = YB;
+        b.out_bstride = (long long)p->So * p->m0 * yb2;
+        k4 = KK_FWD_P_SLABO;
+      }
     }
     if ((rc = launch_col(p, k4, b, st))) return rc;
     xin = p->B;
@@ -851,20 +890,26 @@ int rhs_impl(srk_plan* p, const void* y_, void* f_, double nu, double ri, double
     auto it = g_fast->find(p->m0);
     if (it != g_fast->end() && it->second.e[KK_FWD_P2D].fn) k5 = KK_FWD_P2D;
   }
-  if (YB) {  // K5 reads the y-blocked layout: column groups of YB*K columns, x rows YB*K apart
-    c5.kc = (int)ybK;
-    c5.ngrp = p->n1 / YB;
-    c5.in_kst = (long long)p->So * p->m0 * ybK;
-    c5.in_rs = ybK;
-    c5.in_plane_stride = (long long)p->m0 * ybK;
-    c5.out_kst = ybK;
-    c5.out_rs = c5.row_stride;
+  if (lay) {  // K5: flattened (y, kz) columns at pitch Kp on both sides (pad columns transformed too)
+    c5.Qp = p->n1 * Kp;
+    c5.row_stride = (long long)p->n1 * Kp;
+    c5.in_plane_stride = (long long)p->m0 * yb2;
+    c5.out_plane_stride = (long long)p->n0 * p->n1 * Kp;
+    if (YB) {
+      c5.kc = (int)yb2;
+      c5.ngrp = p->n1 / YB;
+      c5.in_kst = (long long)p->So * p->m0 * yb2;
+      c5.in_rs = yb2;
+      c5.out_kst = yb2;
+      c5.out_rs = c5.row_stride;
+    }
   }
   if ((rc = launch_col(p, k5, c5, st))) return rc;
   // K6: projection + viscous (+ Boussinesq terms)
   ProjArgs pa{};
   pa.g = geom(p);
   pa.G = gbuf;
+  pa.Gp = lay ? Kp : 0;
   pa.y = y;
   pa.f = f;
   pa.modes = p->modes;
