@@ -184,7 +184,7 @@ int env_int(const char* name, int dflt) {
   return (v && *v) ? atoi(v) : dflt;
 }
 
-// Layout of the RHS intermediates of unsplit 3D fast plans (rhs_impl):
+// Layout of the RHS intermediates of unsplit fast plans (rhs_impl):
 //  * pencil pitch Kp = K rounded up to 4 complex: K = n2/2 + 1 is odd, so with pitch K
 //    every other row of a y pass starts 16 B into a 32 B sector and its 64 B tile pieces
 //    are partial-sector writes (K2's stores ran at 3.1 TB/s; 7.7 TB/s with an even pitch);
@@ -192,18 +192,18 @@ int env_int(const char* name, int dflt) {
 //    when a plain x row reaches 1 MB: an x-pass tile then spans ~100 instead of m0 2 MB
 //    pages per signal (the plain order thrashes the TLB).
 // SRK_KPAD=0 / SRK_YB=0 switch them off (A/B timing); both 0 for every other plan.
-bool rhs_fast3d(const srk_plan* p) {
+bool rhs_fast(const srk_plan* p) {  // unsplit plan on the compile-time FFT plans, 32-bit mode indices
   init_registry();
-  return p->dims == 3 && p->nranks == 1 && p->modes < (1LL << 32) && g_fast->count(p->m0) && g_fast->count(p->m1) &&
-         g_fast->count(p->m2);
+  return p->nranks == 1 && p->modes < (1LL << 32) && g_fast->count(p->m0) && g_fast->count(p->m2) &&
+         (p->dims == 2 || g_fast->count(p->m1));
 }
 int rhs_pitch(const srk_plan* p) {
   static const int env_kpad = env_int("SRK_KPAD", 1);
-  return (env_kpad && rhs_fast3d(p)) ? ((p->K + 3) & ~3) : p->K;
+  return (env_kpad && rhs_fast(p)) ? ((p->K + 3) & ~3) : p->K;
 }
 int rhs_yblock(const srk_plan* p) {
   static const int env_yb = env_int("SRK_YB", -1);
-  if (!rhs_fast3d(p)) return 0;
+  if (p->dims != 3 || !rhs_fast(p)) return 0;
   int yb = env_yb >= 0 ? env_yb : ((long long)p->n1 * p->K * 16 >= (1 << 20) ? 64 : 0);
   if (yb <= 0 || yb >= p->n1 || p->n1 % yb) return 0;
   return yb;
@@ -629,9 +629,10 @@ int srk_plan_create(srk_plan** out, int dims, const int64_t* shape, const double
     upA(c * m0 * m1 * K);
     upB(c * m0 * n1 * K);
   } else {
-    upA(p->S * m0 * K);
-    upB(p->So * m0 * K);
-    upA(p->So * n0 * K);
+    const long long Kp = rhs_pitch(p);
+    upA(p->S * m0 * Kp);
+    upB(p->So * m0 * Kp);
+    upA(p->So * n0 * Kp);
     upA(c * m0 * K);
   }
   p->A_elems = A;
@@ -817,6 +818,11 @@ int rhs_impl(srk_plan* p, const void* y_, void* f_, double nu, double ri, double
     a.out_kst = (long long)p->S1 * p->m0 * yb1;
     a.out_rs = yb1;
     a.out_plane_stride = (long long)p->m0 * yb1;
+  }
+  if (d == 2 && lay) {  // 2D: x-pass rows at pitch Kp (the state's rows keep pitch K)
+    a.out_rs = Kp;
+    a.kc_out = Kp;
+    a.out_plane_stride = (long long)p->m0 * Kp;
   }
   if ((rc = launch_col(p, d == 3 ? KK_INV_KX : KK_INV_RHS, a, st))) return rc;
   const cplx* zin = p->A;
