@@ -201,6 +201,14 @@ int rhs_pitch(const srk_plan* p) {
   static const int env_kpad = env_int("SRK_KPAD", 1);
   return (env_kpad && rhs_fast(p)) ? ((p->K + 3) & ~3) : p->K;
 }
+// Slab plans: the rank-local K2 -> K3 -> K4 buffers get the padded pitch too (the
+// exchange buffers keep the all-to-all layouts at pitch K).
+int slab_pitch(const srk_plan* p) {
+  static const int env_kpad = env_int("SRK_KPAD", 1);
+  init_registry();
+  const bool fast = g_fast->count(p->m0) && g_fast->count(p->m1) && g_fast->count(p->m2);
+  return (env_kpad && p->dims == 3 && fast) ? ((p->K + 3) & ~3) : p->K;
+}
 int rhs_yblock(const srk_plan* p) {
   static const int env_yb = env_int("SRK_YB", -1);
   if (p->dims != 3 || !rhs_fast(p)) return 0;
@@ -1150,8 +1158,9 @@ int srk_plan_create_slab(srk_plan** out, const int64_t* shape, const double* len
   p->Mx = p->m0 / nranks;
   p->modes = (long long)p->n0 * p->n1 * p->K;
   const long long K = p->K, Ny = p->n1, Mx = p->Mx, m1 = p->m1, n0 = p->n0;
-  long long A = std::max<long long>(p->So * Mx * m1 * K, p->So * n0 * Ny * K);
-  long long B = p->S * Mx * m1 * K;
+  const long long Kp = slab_pitch(p);
+  long long A = std::max<long long>(p->So * Mx * m1 * Kp, p->So * n0 * Ny * K);
+  long long B = p->S * Mx * m1 * Kp;
   (void)loc;
   p->A_elems = A;
   p->B_elems = B;
@@ -1203,8 +1212,11 @@ int srk_slab_middle(srk_plan* p, const void* recv1, void* send2, void* stream) {
   b.planes = p->S * p->Mx;
   b.Qp = p->K;
   b.row_stride = K;
+  const long long Kp = slab_pitch(p);  // pitch of the rank-local B / A buffers
   b.in_plane_stride = Ny * K;
-  b.out_plane_stride = m1 * K;
+  b.out_plane_stride = m1 * Kp;
+  b.out_rs = Kp;
+  b.kc_out = (int)Kp;
   b.in_rpb = (int)Ny;
   b.in_bstride = (long long)p->S1 * Mx * Ny * K;
   b.xplanes = p->Mx;
@@ -1218,8 +1230,9 @@ int srk_slab_middle(srk_plan* p, const void* recv1, void* send2, void* stream) {
   ZArgs z = z_args(p, p->m2, p->n2, P);
   z.in = p->B;
   z.out = p->A;
-  z.in_sig_stride = (long long)P * K;
-  z.out_sig_stride = (long long)P * K;
+  z.Kp = (int)Kp;
+  z.in_sig_stride = (long long)P * Kp;
+  z.out_sig_stride = (long long)P * Kp;
   z.zero_nyq = 1;
   if ((rc = launch_z(p, p->density ? KK_Z_B3 : KK_Z_NS3, z, 0, 0, st))) return rc;
   // K4: forward y + truncation into the all-to-all #2 send layout
@@ -1231,7 +1244,8 @@ int srk_slab_middle(srk_plan* p, const void* recv1, void* send2, void* stream) {
   c.planes = p->So * p->Mx;
   c.Qp = p->K;
   c.row_stride = K;
-  c.in_plane_stride = m1 * K;
+  c.in_rs = Kp;
+  c.in_plane_stride = m1 * Kp;
   c.out_plane_stride = Ny * K;
   c.out_rpb = (int)Ny;
   c.out_bstride = (long long)p->So * Mx * Ny * K;
@@ -1324,9 +1338,10 @@ int srk_slab_inverse_y_kz(srk_plan* p, const void* recv1, int k0, int kc, void* 
   b.out_k0 = k0;
   b.kz0 = k0;
   b.in_rs = kc;
-  b.out_rs = K;
+  b.out_rs = slab_pitch(p);
+  if (k0 + kc == p->K) b.kc_out = kc + (slab_pitch(p) - p->K);  // the last chunk stores the pad columns
   b.in_plane_stride = Ny * kc;
-  b.out_plane_stride = m1 * K;
+  b.out_plane_stride = m1 * slab_pitch(p);
   b.in_rpb = (int)Ny;
   b.in_bstride = (long long)p->S1 * Mx * Ny * kc;
   b.xplanes = p->Mx;
@@ -1346,8 +1361,9 @@ int srk_slab_zpass(srk_plan* p, void* stream) {
   ZArgs z = z_args(p, p->m2, p->n2, P);
   z.in = p->B;
   z.out = p->A;
-  z.in_sig_stride = (long long)P * K;
-  z.out_sig_stride = (long long)P * K;
+  z.Kp = slab_pitch(p);
+  z.in_sig_stride = (long long)P * z.Kp;
+  z.out_sig_stride = (long long)P * z.Kp;
   z.zero_nyq = 1;
   z.pf_dist = zpass_prefetch_distance();
   return launch_z(p, p->density ? KK_Z_B3 : KK_Z_NS3, z, 0, 0, (cudaStream_t)stream);
@@ -1370,9 +1386,9 @@ int srk_slab_forward_y_kz(srk_plan* p, void* send2, int k0, int kc, void* stream
   c.in_k0 = k0;
   c.out_k0 = 0;
   c.kz0 = k0;
-  c.in_rs = K;
+  c.in_rs = slab_pitch(p);
   c.out_rs = kc;
-  c.in_plane_stride = m1 * K;
+  c.in_plane_stride = m1 * slab_pitch(p);
   c.out_plane_stride = Ny * kc;
   c.out_rpb = (int)Ny;
   c.out_bstride = (long long)p->So * Mx * Ny * kc;
@@ -1453,9 +1469,9 @@ int srk_slab_forward_y_kz_peer(srk_plan* p, int k0, int kc, void* stream) {
   c.in_k0 = k0;
   c.out_k0 = 0;
   c.kz0 = k0;
-  c.in_rs = K;
+  c.in_rs = slab_pitch(p);
   c.out_rs = kc;
-  c.in_plane_stride = m1 * K;
+  c.in_plane_stride = m1 * slab_pitch(p);
   c.out_plane_stride = Ny * kc;
   c.out_rpb = (int)Ny;
   c.out_bstride = bs;
