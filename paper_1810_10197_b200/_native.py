@@ -203,3 +203,44 @@ def dbl_array(vals):
     for i, v in enumerate(vals):
         arr[i] = float(v)
     return arr
+
+
+# ---------------------------------------------------------------------------
+# NVTX ranges (SURVEY §5 tracing): SRK_NVTX=1 wraps every RHS evaluation, adaptive
+# attempt and step reduction in a named range for nsys / ncu --nvtx timelines.
+# Off by default: a no-op context manager, nothing on the hot path.
+# ---------------------------------------------------------------------------
+NVTX = os.environ.get("SRK_NVTX", "0") not in ("", "0")
+
+
+class _NoRange:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+_NO_RANGE = _NoRange()
+
+
+class _Range:
+    __slots__ = ("name",)
+
+    def __init__(self, name):
+        self.name = name
+
+    def __enter__(self):
+        import torch
+        torch.cuda.nvtx.range_push(self.name)
+        return self
+
+    def __exit__(self, *a):
+        import torch
+        torch.cuda.nvtx.range_pop()
+        return False
+
+
+def nvtx(name):
+    """``with nvtx("srk_rhs"):`` -- an NVTX range when SRK_NVTX=1, else a no-op."""
+    return _Range(name) if NVTX else _NO_RANGE

@@ -77,8 +77,8 @@ struct PassArgs {
   int tma_rows;  // rows per TMA box (divides the staged row count)
   int tma_out;   // 1: inverse passes write their output tile with 3D TMA stores
   int tmo_rows;  // rows per output box (divides M)
-  int probe;     // measurement only (SRK_PROBE_FWD, tools/pass_probe.sh): padded forward passes stage
-                 // their tile and return (1) or also store zeros in the output pattern (2)
+  int probe;     // measurement only (SRK_PROBE_INV / SRK_PROBE_FWD, tools/pass_probe.sh): the pass stages
+                 // its tile and returns (1), also stores in the output pattern (2), or (K2) only stores (5)
   // Column groups (kz chunks of the pipelined slab RHS): the Qp columns of a
   // plane are ngrp groups of kc columns; group g, local column c sits at
   // memory column g*in_kst + in_k0 + c of the input (out_* for the output),
@@ -439,15 +439,13 @@ __global__ void __launch_bounds__(Eng::NT, (Eng::NT <= 64 ? 6 : (Eng::NT <= 128 
     const double kz = (double)(a.kz0 + wl + mycol) * a.ck2;  // global kz of the column
     cplx* sb_ = sm + (is_curl ? n * C : 0);
     if (use_tma) {
-      if (a.probe == 5) {  // probe: stores only
+      if (a.probe == 5)  // probe: stores only
         SRK_BAR();
-      } else if (a.probe >= 3)  // probe: one staged plane per curl signal (5 distinct planes, 6 tile loads)
-        tma_stage<C>(sm, &tm, wl, g, n, a.tma_rows, trpb, (s == 4 ? cb : ca) * X + x, -1, n * C, &tbar);
       else
-      tma_stage<C>(sm, &tm, wl, g, n, a.tma_rows, trpb, ca * X + x, is_curl ? cb * X + x : -1, n * C, &tbar);
+        tma_stage<C>(sm, &tm, wl, g, n, a.tma_rows, trpb, ca * X + x, is_curl ? cb * X + x : -1, n * C, &tbar);
       SRK_TS(1)
       if (a.probe) {  // access-pattern ceiling (see PK_FWD): the staged rows go out as they are
-        if (a.probe == 2 || a.probe >= 4) {
+        if (a.probe == 2 || a.probe == 5) {
           if (use_tmo) flush_out();
           else
             for (int r = threadIdx.x / C; r < M; r += Eng::NT / C)

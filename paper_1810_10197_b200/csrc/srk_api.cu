@@ -223,10 +223,7 @@ int need_ws(srk_plan* p) {
 }
 
 // ---- strided pass launch -------------------------------------------------
-int curly_xblk(int X) {
-  static const int xb = env_int("SRK_XBLK", 2);
-  return (xb > 0 && X % xb == 0) ? xb : 1;
-}
+int curly_xblk(int X) { return X % 2 == 0 ? 2 : 1; }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
 typedef CUresult (*srk_encode_tiled_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -330,8 +327,7 @@ void setup_tma(int kind, int cols, PassArgs& a, CUtensorMap* tm) {
 void setup_tma_out(int kind, int cols, PassArgs& a, CUtensorMap* tm) {
   a.tma_out = 0;
   const bool inv = kind == KK_INV_CURLY || kind == KK_INV_CURLY_SLAB;  // see kTMAO in k_colpass
-  static const int no_tmao = env_int("SRK_NO_TMAO", 0);
-  if (!inv || a.out_rpb != 0 || !g_fast->count(a.M) || no_tmao) return;
+  if (!inv || a.out_rpb != 0 || !g_fast->count(a.M)) return;
   const int nb = (a.M + 255) / 256;
   if (a.M % nb) return;
   const int box = a.M / nb;

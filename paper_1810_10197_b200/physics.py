@@ -70,9 +70,10 @@ class FlowRHS:
         f = out if out is not None else torch.empty_like(y)
         p = self.params
         pl = self.plan
-        _native.check(pl.lib.srk_rhs(pl.bind(), _native.ptr(y), _native.ptr(f), 1.0 / p.reynolds,
-                                     float(p.richardson), float(p.reynolds) * float(p.prandtl),
-                                     _native.stream_ptr()), "srk_rhs")
+        with _native.nvtx("srk_rhs"):
+            _native.check(pl.lib.srk_rhs(pl.bind(), _native.ptr(y), _native.ptr(f), 1.0 / p.reynolds,
+                                         float(p.richardson), float(p.reynolds) * float(p.prandtl),
+                                         _native.stream_ptr()), "srk_rhs")
         self.calls += 1
         _native.count(pl.lib.srk_rhs_launch_count(pl.h))
         return from_device(f, was_np)
@@ -91,11 +92,12 @@ class FlowRHS:
         p = self.params
         pl = self.plan
         Fs = [F for _, F in terms]
-        _native.check(pl.lib.srk_rhs_combine(pl.bind(), _native.ptr(y), _native.ptr(f), 1.0 / p.reynolds,
-                                             float(p.richardson), float(p.reynolds) * float(p.prandtl),
-                                             _native.ptr(yb), len(Fs), _native.ptr_array(Fs),
-                                             _native.dbl_array([c for c, _ in terms]), float(coef_self),
-                                             _native.ptr(ynext), _native.stream_ptr()), "srk_rhs_combine")
+        with _native.nvtx("srk_rhs_combine"):
+            _native.check(pl.lib.srk_rhs_combine(pl.bind(), _native.ptr(y), _native.ptr(f), 1.0 / p.reynolds,
+                                                 float(p.richardson), float(p.reynolds) * float(p.prandtl),
+                                                 _native.ptr(yb), len(Fs), _native.ptr_array(Fs),
+                                                 _native.dbl_array([c for c, _ in terms]), float(coef_self),
+                                                 _native.ptr(ynext), _native.stream_ptr()), "srk_rhs_combine")
         self.calls += 1
         _native.count(pl.lib.srk_rhs_launch_count(pl.h))
         return f, ynext
@@ -113,10 +115,11 @@ class FlowRHS:
         p = self.params
         pl = self.plan
         out = _native.host_result(9)
-        _native.check(pl.lib.srk_rhs_refresh(pl.bind(), _native.ptr(y), _native.ptr(f), 1.0 / p.reynolds,
-                                             float(p.richardson), float(p.reynolds) * float(p.prandtl),
-                                             float(coef_self), _native.ptr(ynext), _native.ptr(out),
-                                             _native.stream_ptr()), "srk_rhs_refresh")
+        with _native.nvtx("srk_rhs_refresh"):
+            _native.check(pl.lib.srk_rhs_refresh(pl.bind(), _native.ptr(y), _native.ptr(f), 1.0 / p.reynolds,
+                                                 float(p.richardson), float(p.reynolds) * float(p.prandtl),
+                                                 float(coef_self), _native.ptr(ynext), _native.ptr(out),
+                                                 _native.stream_ptr()), "srk_rhs_refresh")
         self.calls += 1
         _native.count(pl.lib.srk_rhs_launch_count(pl.h))
         _native.wait_stream_point()

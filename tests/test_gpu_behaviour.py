@@ -337,3 +337,19 @@ def test_host_mirror_rejects_mismatched_tensors():
         m.push(torch.zeros((2, 4, 4, 2), dtype=torch.complex128, device="cuda"))
     with pytest.raises(TypeError):
         srk.HostMirror(torch.zeros(3))
+
+
+@pytest.mark.gpu
+def test_nvtx_ranges_wrap_rhs_calls(monkeypatch):
+    """With SRK_NVTX on, RHS calls and attempts run inside NVTX ranges and give the same results."""
+    from paper_1810_10197_b200 import _native
+
+    g = srk.Grid((32, 32, 32))
+    rhs = srk.FlowRHS(g, srk.PhysParams(1000.0))
+    y = srk.hit_init(g, srk.ProblemSpec("hit", a=4.0, energy=0.5, seed=3)).fields
+    f0 = rhs(0.0, y)
+    monkeypatch.setattr(_native, "NVTX", True)
+    f1 = rhs(0.0, y)
+    out = srk.adaptive_advance(y, 0.0, srk.make_bs5(), srk.ControllerState(h=1e-3), srk.ControllerConfig(), rhs, grid=g)
+    torch.cuda.synchronize()
+    assert torch.equal(f0, f1) and out.rhs_evals >= 7

@@ -149,3 +149,15 @@ def test_bench_self_launches_n_ranks_dry_run():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["ranks_seen"] == 2 and d["dry_run"]
+
+
+def test_nvtx_ranges_are_a_noop_unless_enabled(monkeypatch):
+    """SRK_NVTX gates the NVTX ranges around RHS calls / attempts (tracing)."""
+    from paper_1810_10197_b200 import _native
+
+    monkeypatch.setattr(_native, "NVTX", False)
+    with _native.nvtx("srk_rhs") as r:
+        assert r is _native._NO_RANGE
+    monkeypatch.setattr(_native, "NVTX", True)
+    assert isinstance(_native.nvtx("srk_rhs"), _native._Range)
+    assert _native.nvtx("bs5_attempt").name == "bs5_attempt"
