@@ -58,7 +58,11 @@ int srk_plan_create(srk_plan** out, int dims, const int64_t* shape, const double
 void srk_plan_destroy(srk_plan* plan);
 
 /* Device workspace the caller must allocate (bytes) and bind before any
- * compute call.  Replaces the numpy buffers of spectral.py:187-207. */
+ * compute call.  Replaces the numpy buffers of spectral.py:187-207.  The layout
+ * inside is the library's own: plans on the compile-time FFT lengths keep the RHS
+ * intermediates at a sector-aligned pencil pitch (ceil4(n_last/2 + 1) for n_last >=
+ * 256) and the x-padded buffers y-blocked, so the size is slightly larger than the
+ * reference's buffers (+1.2 % at 512^3); always query it here. */
 int srk_plan_workspace_bytes(const srk_plan* plan, int64_t* bytes);
 int srk_plan_set_workspace(srk_plan* plan, void* ptr, int64_t bytes);
 
