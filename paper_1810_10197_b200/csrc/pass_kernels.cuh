@@ -543,7 +543,8 @@ struct ZArgs {
   int So; // output real signals per pencil
   long long in_sig_stride, out_sig_stride;  // complex elements (P*K) or real (P*M)
   int zero_nyq;  // R2C: zero the kz = n/2 plane (narrow)
-  int mode;      // unused (kept for ABI stability of the struct)
+  int mode;      // measurement only (SRK_PROBE_Z, one-pencil NS3 pass): 1 = stage the rows and return,
+                 // 2 = also store zeros in the output pattern (no transforms)
   int pf_dist;   // NS3 z-pass: > 0 prefetch the inputs of block bid + pf_dist into L2
   unsigned long long* dbg;  // optional phase timestamps (tools/phase_timing.py)
 };
@@ -1155,6 +1156,12 @@ __global__ void __launch_bounds__(EngI::NT, (OP == ZOP_B2 ? SRK_ZB2P_MINB : (M <
   mbar_wait(&mbar, 0);
   cp_async_wait_all();
   SRK_TS(1)
+  if (a.mode) {  // measurement only (SRK_PROBE_Z): the pencil's access pattern without the transforms
+    if (a.mode == 2)
+      for (int k = tid; k < (KP > K ? K + 1 : K); k += NT)
+        for (int s = 0; s < ZSig<OP>::So; ++s) a.out[s * a.out_sig_stride + (long long)pen * KP + k] = cmk(0.0, 0.0);
+    return;
+  }
   {
     ZHermLoad<M> ld{stg};
     auto st = [&](int n, int c, cplx v) { sm[L::idx(n, c)] = v; };

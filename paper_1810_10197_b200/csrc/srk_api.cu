@@ -408,6 +408,8 @@ int launch_z(srk_plan* p, int kind, ZArgs a, int S_rt, int So_rt, cudaStream_t s
   if ((rc = get_tw(p, a.M, &a.tw))) return rc;
   if ((rc = ensure_smem(e))) return rc;
   int grid = e.ppc == 1 ? a.P : (a.P + 1) / 2;
+  static const int probe_z = env_int("SRK_PROBE_Z", 0);
+  a.mode = (e.ppc == 1 && kind == KK_Z_NS3) ? probe_z : 0;
   if (e.ppc == 1 && a.pf_dist)  // L2 warm-up one wave of resident CTAs ahead (in pencils)
     a.pf_dist = srk_blocks_per_sm(e.fn, e.nt, e.smem) * srk_sm_count();
   void* args[] = {&a, &S_rt, &So_rt};
