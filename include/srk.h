@@ -261,6 +261,13 @@ int srk_debug_phase_buffer(srk_plan* plan, void* dev_buf, int launch_index);
  * bench.py for the measured fp64 ceiling of the z-pass. */
 int srk_probe(int mode, int iters, int blocks_per_sm, void* scratch, void* stream, double* ops_out);
 
+/* Layout of the RHS intermediates inside the workspace (introspection, tests, docs):
+ * *pitch = pencil pitch in complex elements (n_last/2 + 1, or that rounded up to 4 for
+ * the sector-aligned layout), *yblock = rows per y block of the x-padded buffers
+ * (0: plain [signal][x][y][kz] order).  No reference counterpart: numpy owns the
+ * reference's buffers (spectral.py:187-207). */
+int srk_plan_layout(const srk_plan* plan, int* pitch, int* yblock);
+
 /* Build flags: bit 0 = hazard-probe build (make checks: schedule fuzzing at every
  * barrier, NaN-poisoned shared memory, tile bounds asserts; tools/check_build.sh). */
 int srk_build_info(void);

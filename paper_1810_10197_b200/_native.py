@@ -32,7 +32,7 @@ EXPORTS = (
     "srk_slab_forward_x_kz", "srk_slab_project", "srk_store_mapped", "srk_slab_set_peers",
     "srk_slab_forward_kz_peer", "srk_slab_forward_y_kz_peer", "srk_ipc_export", "srk_ipc_import", "srk_ipc_close",
     "srk_rhs_refresh", "srk_probe", "srk_combine_scaled", "srk_rhs_combine_scaled", "srk_step_reduce_scaled",
-    "srk_build_info", "srk_source_hash",
+    "srk_build_info", "srk_source_hash", "srk_plan_layout",
 )
 
 _lib = None
@@ -85,6 +85,7 @@ def load():
         "srk_store_mapped": (c_int, [vp, vp, c_int, vp]),
         "srk_probe": (c_int, [c_int, c_int, c_int, vp, vp, P(c_dbl)]),
         "srk_build_info": (c_int, []),
+        "srk_plan_layout": (c_int, [vp, P(c_int), P(c_int)]),
         "srk_source_hash": (ctypes.c_char_p, []),
         "srk_combine_scaled": (c_int, [i64, vp, c_int, P(vp), P(c_dbl), vp, vp, vp]),
         "srk_rhs_combine_scaled": (c_int, [vp, vp, vp, c_dbl, c_dbl, c_dbl, vp, c_int, P(vp), P(c_dbl), c_dbl, vp,

@@ -556,6 +556,13 @@ int srk_abi_version(void) { return 1; }
 #endif
 const char* srk_source_hash(void) { return SRK_SRC_HASH; }
 
+int srk_plan_layout(const srk_plan* p, int* pitch, int* yblock) {
+  if (!p || !pitch || !yblock) return fail(SRK_ERR_INVALID, "null argument");
+  *pitch = p->nranks == 1 ? rhs_pitch(p) : slab_pitch(p);
+  *yblock = rhs_yblock(p);
+  return SRK_OK;
+}
+
 int srk_build_info(void) {
 #ifdef SRK_DEBUG_CHECKS
   return 1;  // hazard-probe build (schedule fuzzing, NaN-poisoned shared memory, asserts)

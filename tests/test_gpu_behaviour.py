@@ -353,3 +353,25 @@ def test_nvtx_ranges_wrap_rhs_calls(monkeypatch):
     out = srk.adaptive_advance(y, 0.0, srk.make_bs5(), srk.ControllerState(h=1e-3), srk.ControllerConfig(), rhs, grid=g)
     torch.cuda.synchronize()
     assert torch.equal(f0, f1) and out.rhs_evals >= 7
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape, pitch, yblock", [
+    ((512, 512, 512), 260, 64),   # x rows of 2.1 MB: y-blocked; K = 257 -> 260
+    ((256, 256, 256), 132, 0),    # x rows of 528 KB: plain order; K = 129 -> 132
+    ((128, 128, 128), 65, 0),     # short rows: reference pitch
+    ((64, 512, 256), 132, 64),    # anisotropic: n1 * K * 16 B = 1 MB
+    ((1024, 1024), 516, 0),       # 2D: pitch only
+    ((16, 12, 10), 6, 0),         # runtime (generic) FFT plan: reference layout
+])
+def test_plan_layout_of_the_intermediates(shape, pitch, yblock):
+    """srk_plan_layout: sector-aligned pitch for n_last >= 256 on the compile-time plans, y-blocked
+    x-pass buffers once a plain x row reaches 1 MB."""
+    import ctypes
+
+    from paper_1810_10197_b200.spectral import get_plan
+
+    pl = get_plan(srk.Grid(shape), density=False)
+    kp, yb = ctypes.c_int(-1), ctypes.c_int(-1)
+    assert pl.lib.srk_plan_layout(pl.h, ctypes.byref(kp), ctypes.byref(yb)) == 0
+    assert (kp.value, yb.value) == (pitch, yblock)
