@@ -1237,6 +1237,11 @@ __global__ void __launch_bounds__(EngI::NT, (OP == ZOP_B2 ? SRK_ZB2P_MINB : (M <
   if constexpr (OP == ZOP_NS3 && ns3p_fused_last<M, FR...>::value) {
     ZFinNS3<M> fin{a.out + (long long)pen * KP, a.out_sig_stride, KP > K};
     LoopStageZ<M, L, -1, 2, NT, 4, FR...>::go(sm, twp, fin);
+    if (a.dbg) {  // phase stamps (tools/phase_timing.py): the suffix now includes the extraction
+      SRK_BAR();
+      SRK_TS(4)
+      SRK_TS(5)
+    }
     return;
   }
   // ---- forward suffix (Ls = 4 ...) on the 2 packed columns ----

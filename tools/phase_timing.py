@@ -14,6 +14,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1810_10197_b200 as srk  # noqa: E402
 from paper_1810_10197_b200 import _native  # noqa: E402
 
+# K3 one-pencil 768 kernel: the last forward stage keeps its outputs in registers and stores them,
+# so "forward_suffix" includes the extraction and "extraction" is empty there
 NAMES = {2: ["tma_wait", "inverse_prefix", "fused_middle", "forward_suffix", "extraction"]}
 COL = ["stage_wait", "fft_and_store"]
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 512
