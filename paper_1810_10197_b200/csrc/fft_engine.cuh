@@ -201,6 +201,14 @@ struct ld_has_range : std::false_type {};
 template <class T>
 struct ld_has_range<T, decltype(void(T::kRange))> : std::true_type {};
 
+// A first-stage loader with a member kColPrivate reads staged inputs that lie inside the
+// tile column it transforms: the load -> store hazard of the first stage is then private
+// to the warp(s) that own the column, like every later stage.
+template <class T, class = void>
+struct ld_col_private : std::false_type {};
+template <class T>
+struct ld_col_private<T, decltype(void(T::kColPrivate))> : std::true_type {};
+
 template <bool WS, int TPC>
 __device__ __forceinline__ void stage_sync() {
   if constexpr (WS && TPC <= 32)
@@ -335,10 +343,10 @@ struct FastStageW {
       }
     }
     if constexpr ((!FIRST || LD_SMEM) && (!LAST || ST_SMEM)) {
-      if constexpr (FIRST)
+      if constexpr (FIRST && !ld_col_private<LD>::value)
         SRK_BAR();  // staging may alias other columns
       else
-        stage_sync<true, TPC>();
+        stage_sync<true, TPC>();  // (a loader whose staged inputs lie inside its own tile column)
     }
     if (act) {
 #pragma unroll

@@ -751,25 +751,30 @@ __global__ void __launch_bounds__(Eng::NT, (PPC == 1 && Eng::NT <= 128 ? 3 : (En
 // inverse's staged-row reads were ~19% of the z-pass's shared-memory traffic).
 // irfft ignores Im of the DC mode (2k == M cannot occur inside the padded band).
 // ---------------------------------------------------------------------------
-template <int M>
-struct ZHermLoad {
+// CP > 0: the two staged rows of complex column c lie at stg + c * CP (+ K for the second),
+// i.e. inside tile column c itself (CP = the tile's column pitch): the first stage then
+// needs no CTA barrier (ld_col_private).  CP = 0: dense rows, 2c and 2c + 1.
+template <int M, int CP = 0>
+struct ZHermLoadT {
   static constexpr int kRange = 1;
   static constexpr int K = M / 3 + 1;
   const cplx* stg;
+  __device__ __forceinline__ static int rowA(int c) { return CP > 0 ? c * CP : (2 * c) * K; }
+  __device__ __forceinline__ static int rowB(int c) { return rowA(c) + K; }
   __device__ __forceinline__ static cplx pack(cplx A, cplx B) { return cmk(A.x - B.y, A.y + B.x); }
   __device__ __forceinline__ cplx head(int k, int c) const {
-    cplx A = stg[(2 * c) * K + k], B = stg[(2 * c + 1) * K + k];
+    cplx A = stg[rowA(c) + k], B = stg[rowB(c) + k];
     if (k == 0) A.y = B.y = 0.0;
     return pack(A, B);
   }
   __device__ __forceinline__ cplx tail(int k, int c) const {
-    const cplx A = stg[(2 * c) * K + (M - k)], B = stg[(2 * c + 1) * K + (M - k)];
+    const cplx A = stg[rowA(c) + (M - k)], B = stg[rowB(c) + (M - k)];
     return pack(cmk(A.x, -A.y), cmk(B.x, -B.y));
   }
   __device__ __forceinline__ cplx operator()(int k, int c) const {
     const bool hd = k < K, tl = k >= M - (K - 1);
     const int kk = hd ? k : (tl ? M - k : 0);
-    cplx A = stg[(2 * c) * K + kk], B = stg[(2 * c + 1) * K + kk];
+    cplx A = stg[rowA(c) + kk], B = stg[rowB(c) + kk];
     if (tl) {
       A.y = -A.y;
       B.y = -B.y;
@@ -783,6 +788,12 @@ struct ZHermLoad {
     if (rlo >= M - (K - 1)) return tail(k, c);
     return (*this)(k, c);
   }
+};
+template <int M>
+using ZHermLoad = ZHermLoadT<M, 0>;
+template <int M, int CP>
+struct ZHermLoadCol : ZHermLoadT<M, CP> {
+  static constexpr int kColPrivate = 1;
 };
 
 // ---------------------------------------------------------------------------
@@ -1131,6 +1142,10 @@ __global__ void __launch_bounds__(EngI::NT, (OP == ZOP_B2 ? SRK_ZB2P_MINB : (M <
   SRK_TS_INIT(a.dbg, 6)
   SRK_TS(0)
   // ---- staging: 6 real-signal rows of K modes via 1D TMA bulk copies ----
+  // When a warp owns a whole tile column (M / 24 = 32 threads per column), the two rows of
+  // complex column c are staged inside tile column c: the first inverse stage then needs
+  // no CTA barrier and the three warps run the whole prefix independently.
+  constexpr bool kColStg = (EngI::TPC <= 32) && (2 * K <= L::PITCH);
   cplx* stg = sm;
   __shared__ __align__(8) unsigned long long mbar;
   if (tid == 0) {
@@ -1142,7 +1157,8 @@ __global__ void __launch_bounds__(EngI::NT, (OP == ZOP_B2 ? SRK_ZB2P_MINB : (M <
   if (tid == 0) {
     mbar_expect_tx(&mbar, (unsigned)(2 * S * K * 16));
     for (int s = 0; s < 2 * S; ++s)
-      bulk_g2s(stg + s * K, a.in + s * a.in_sig_stride + (long long)pen * KP, (unsigned)(K * 16), &mbar);
+      bulk_g2s(stg + (kColStg ? (s >> 1) * L::PITCH + (s & 1) * K : s * K),
+               a.in + s * a.in_sig_stride + (long long)pen * KP, (unsigned)(K * 16), &mbar);
     if (a.pf_dist) {
       const int q0 = pen + a.pf_dist;
       if (q0 < a.P)
@@ -1152,9 +1168,13 @@ __global__ void __launch_bounds__(EngI::NT, (OP == ZOP_B2 ? SRK_ZB2P_MINB : (M <
   }
   // every thread waits on the mbarrier itself (the TMA rows are then visible to
   // it); the twiddle table (cp.async by all threads) is first read in the second
-  // inverse stage, after the first stage's CTA barrier -- no barrier here
+  // inverse stage, after the first stage's CTA barrier (or the one below)
   mbar_wait(&mbar, 0);
   cp_async_wait_all();
+  // column-private staging: the first stage has no CTA barrier to publish the twiddle
+  // table (filled by all threads) before the second stage reads it -- sync here, where the
+  // warps arrive together anyway (they all just left the same mbarrier)
+  if constexpr (kColStg) SRK_BAR();
   SRK_TS(1)
   if (a.mode) {  // measurement only (SRK_PROBE_Z): the pencil's access pattern without the transforms
     if (a.mode == 2)
@@ -1163,9 +1183,14 @@ __global__ void __launch_bounds__(EngI::NT, (OP == ZOP_B2 ? SRK_ZB2P_MINB : (M <
     return;
   }
   {
-    ZHermLoad<M> ld{stg};
     auto st = [&](int n, int c, cplx v) { sm[L::idx(n, c)] = v; };
-    EngI::template run_ws<+1, true, true>(a.gp, sm, twp, S, ld, st);
+    if constexpr (kColStg) {
+      ZHermLoadCol<M, L::PITCH> ld{stg};
+      EngI::template run_ws<+1, true, true>(a.gp, sm, twp, S, ld, st);
+    } else {
+      ZHermLoad<M> ld{stg};
+      EngI::template run_ws<+1, true, true>(a.gp, sm, twp, S, ld, st);
+    }
   }
   SRK_BAR();
   SRK_TS(2)
