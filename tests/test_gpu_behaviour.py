@@ -375,3 +375,33 @@ def test_plan_layout_of_the_intermediates(shape, pitch, yblock):
     kp, yb = ctypes.c_int(-1), ctypes.c_int(-1)
     assert pl.lib.srk_plan_layout(pl.h, ctypes.byref(kp), ctypes.byref(yb)) == 0
     assert (kp.value, yb.value) == (pitch, yblock)
+
+
+@pytest.mark.gpu
+def test_layout_switches_do_not_change_results(tmp_path):
+    """SRK_KPAD=0 / SRK_YB=0 (reference pitch / plain order of the RHS intermediates) run the
+    same arithmetic as the default sector-aligned, y-blocked layout: bitwise equal tendencies
+    (the switches are read once per process, hence subprocesses)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, numpy as np, torch; sys.path.insert(0, %r)\n"
+        "import paper_1810_10197_b200 as srk\n"
+        "g = srk.Grid((64, 512, 256))\n"          # x rows of 1 MB: y-blocked by default, K = 129 -> 132
+        "torch.manual_seed(7)\n"
+        "y = torch.randn((3,) + g.kshape, dtype=torch.complex128, device='cuda')\n"
+        "f = srk.FlowRHS(g, srk.PhysParams(500.0))(0.0, y)\n"
+        "np.save(sys.argv[1], f.cpu().numpy())\n" % root
+    )
+    outs = []
+    for name, env in (("default", {}), ("nopad", {"SRK_KPAD": "0"}), ("noyb", {"SRK_YB": "0"}),
+                      ("plain", {"SRK_KPAD": "0", "SRK_YB": "0"})):
+        out = str(tmp_path / f"{name}.npy")
+        subprocess.run([sys.executable, "-c", code, out], check=True, env={**os.environ, **env}, timeout=300)
+        outs.append(np.load(out))
+    assert np.isfinite(outs[0]).all() and np.abs(outs[0]).max() > 0
+    for o in outs[1:]:
+        assert np.array_equal(outs[0], o)
